@@ -1,0 +1,163 @@
+/* mlb.h - C ABI of the B200-native D3Q19 time-step loop (libmlb_d3q19.so).
+ *
+ * This is the drop-in boundary for the reference's plugin point
+ * `KernelPlan(...).step(fpre, fpost)` and the engine loop around it
+ * (reference = /root/reference/pkg/src/lb2d, cited as file:line below).
+ * Plain pointers and sizes only; no torch / numpy types.  Every function
+ * returns 0 on success or an MLB_E* code, with a human-readable message in
+ * mlb_last_error() (thread-local).  `stream` arguments are cudaStream_t
+ * values passed as void* (NULL = the legacy default stream).
+ *
+ * Memory model.  The CALLER owns every population buffer (in the Python
+ * host: torch tensors; only data_ptr() crosses) - mirroring the reference,
+ * where KernelPlan keeps no population copies (kernels.py:398-443).  The
+ * plan owns only what it derives from the flags (a per-cell class byte, the
+ * inlet/outlet index lists), reduction scratch and two timing events.
+ *
+ * Host layout (what the reference passes): dense C-contiguous
+ *   f[q][z][y][x],  q < 19, x fastest            ("(Q, N)" block)
+ *   flags[z][y][x]  uint8, codes 0..4 (boundaries.py:20-24)
+ * Device layout (mlb_layout): per population (nz + 2) z-planes - storage
+ * plane 0 and nz+1 are halo planes, slab plane lz lives at storage lz+1 -
+ * each plane ny rows of xp elements, xp = nx rounded up to a whole number
+ * of 128-byte lines:
+ *   element(q, x, y, lz) = q*pop + ((lz + 1)*ny + y)*xp + x
+ */
+#ifndef MLB_H
+#define MLB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MLB_ABI_VERSION 1
+#define MLB_Q 19
+
+/* dtype codes = the reference's Precision wire codes (fields.py:22-23) */
+enum { MLB_F32 = 0, MLB_F64 = 1 };
+/* how the pulls across the slab's z faces are served */
+enum { MLB_Z_PERIODIC = 0, /* whole domain on this GPU: wrap in-kernel      */
+       MLB_Z_HALO = 1 };   /* z-slab: read the halo planes (filled by the
+                              exchange, see mlb_halo_copy)                   */
+enum { MLB_OK = 0, MLB_EINVAL = 1, MLB_ECUDA = 2, MLB_ENOMEM = 3,
+       MLB_EUNSUPPORTED = 4 };
+
+typedef struct mlb_plan mlb_plan;
+
+typedef struct {
+    int32_t nx, ny, nz;   /* slab cells                                    */
+    int32_t itemsize;     /* 4 or 8                                        */
+    int64_t xp;           /* row pitch, elements                           */
+    int64_t plane;        /* elements per z-plane = ny*xp                  */
+    int64_t pop;          /* elements per population = (nz+2)*plane        */
+    int64_t total;        /* elements per population block = 19*pop        */
+    int64_t bytes;        /* total*itemsize                                */
+} mlb_layout;
+
+const char *mlb_last_error(void);
+int mlb_abi_version(void);
+/* number of CUDA kernel launches issued by this library in this process */
+int64_t mlb_launch_count(void);
+
+int mlb_layout_query(int nx, int ny, int nz, int dtype, mlb_layout *out);
+
+/* ---- plan: replaces KernelPlan.__init__ (kernels.py:408-443) -------------
+ * omega and wall_u are cast once to the compute dtype, as the reference
+ * does (kernels.py:429-432); inlet_u feeds the open-boundary pass
+ * (engine.py:167-171).  No flags yet: call mlb_plan_set_flags next. */
+int mlb_plan_create(mlb_plan **out, int nx, int ny, int nz, int dtype,
+                    double omega, const double wall_u[3], double inlet_u,
+                    int device, int z_mode);
+int mlb_plan_destroy(mlb_plan *plan);
+int mlb_plan_get_layout(const mlb_plan *plan, mlb_layout *out);
+int mlb_plan_set_physics(mlb_plan *plan, double omega, const double wall_u[3],
+                         double inlet_u);
+/* kernel variant used by mlb_step (0 = default); for tuning/benchmarks */
+int mlb_plan_set_variant(mlb_plan *plan, int variant);
+
+/* Flags: the reference's `mask` argument (kernels.py:408, a (N,) uint8 array
+ * in cell order).  h_flags is dense [nz][ny][nx] HOST memory.  h_halo_lo /
+ * h_halo_hi are dense [ny][nx] flag planes of the slabs below / above
+ * (MLB_Z_HALO); NULL means "wrap onto this slab" (the periodic whole
+ * domain).  Builds the class table and the inlet/outlet lists.  Rejects
+ * codes > 4 (as engine.restore does, engine.py:326-327) and outlet cells at
+ * x = 0 (MLB_EUNSUPPORTED). */
+int mlb_plan_set_flags(mlb_plan *plan, const uint8_t *h_flags,
+                       const uint8_t *h_halo_lo, const uint8_t *h_halo_hi);
+/* the flag bytes back, dense [nz][ny][nx], for bit-exact geometry checks */
+int mlb_plan_get_flags(const mlb_plan *plan, uint8_t *h_flags);
+
+/* ---- layout conversion: host dense (Q, N) <-> device padded SoA -----------
+ * Interior planes only; halo planes of d_f are left untouched.  h_dense may
+ * be pageable or pinned; the copies are asynchronous on `stream` when it is
+ * pinned. */
+int mlb_upload(const mlb_plan *plan, const void *h_dense, void *d_f, void *stream);
+int mlb_download(const mlb_plan *plan, const void *d_f, void *h_dense, void *stream);
+
+/* ---- the hot path --------------------------------------------------------
+ * mlb_step: KernelPlan.step (kernels.py:445-462) == numba `fused`
+ * (kernels.py:247-279): pull-stream + bounce-back + BGK collide in one
+ * pass.  Reads d_fpre only; writes every FLUID cell of d_fpost exactly once
+ * and no other cell (kernels.py:3-8).  d_fpre != d_fpost.  The _range form
+ * updates slab planes [z0, z1) only (boundary-first / interior overlap). */
+int mlb_step(mlb_plan *plan, const void *d_fpre, void *d_fpost, void *stream);
+int mlb_step_range(mlb_plan *plan, const void *d_fpre, void *d_fpost,
+                   int z0, int z1, void *stream);
+/* _OpenBoundaryPass.apply (engine.py:176-180) on d_fpost: inlet cells <-
+ * equilibrium(1, inlet_u, 0, 0) in compute dtype; outlet cells <- the fresh
+ * populations of their x-1 neighbour, all sources read before any write. */
+int mlb_open_pass(mlb_plan *plan, void *d_fpost, void *stream);
+int mlb_open_pass_range(mlb_plan *plan, void *d_fpost, int z0, int z1,
+                        void *stream);
+/* engine.run's timed loop body (engine.py:244-249) n times: step, open
+ * pass, swap.  MLB_Z_PERIODIC plans only.  The newest populations end in
+ * d_a when nsteps is even, d_b when odd.  If ms != NULL the loop is
+ * bracketed by CUDA events on `stream`, the call synchronises and *ms is
+ * the device time of the loop. */
+int mlb_run_steps(mlb_plan *plan, void *d_a, void *d_b, int nsteps,
+                  void *stream, float *ms);
+
+/* ---- z-slab halo exchange ----------------------------------
+ * Copies the 5 crossing populations of one boundary plane of d_src (a
+ * population block of a slab with the same nx, ny, dtype; possibly on a
+ * peer GPU with access enabled) into a halo plane of d_dst.
+ *   face 0: src plane lz = src_nz-1, populations with c_z = +1
+ *           -> dst halo below (lz = -1)
+ *   face 1: src plane lz = 0, populations with c_z = -1
+ *           -> dst halo above (lz = nz)                                   */
+int mlb_halo_copy(const mlb_plan *plan, void *d_dst, const void *d_src,
+                  int src_nz, int face, void *stream);
+
+/* ---- diagnostics ---------------------------------------------------------
+ * mlb_macro: SimState.macro (engine.py:104-118): rho, u in float64 for ALL
+ * cells, true division, rho = 0 -> u = 0.  Outputs are dense [nz][ny][nx]
+ * DEVICE arrays of double. */
+int mlb_macro(const mlb_plan *plan, const void *d_f, double *d_rho,
+              double *d_ux, double *d_uy, double *d_uz, void *stream);
+/* Deterministic (fixed-tree, no float atomics) reductions; synchronises.
+ * h_out[8] = total mass (all cells), momentum x,y,z over fluid cells,
+ * kinetic energy sum_fluid 1/2 rho |u|^2, max |u| over fluid cells,
+ * count of non-finite populations (SimState.check_finite,
+ * engine.py:123-125), number of fluid cells. */
+int mlb_diagnostics(mlb_plan *plan, const void *d_f, double h_out[8],
+                    void *stream);
+/* rho, ux, uy, uz (float64, macro conventions) of one cell, written to
+ * d_out4[0..3] on the device, asynchronously: the engine's per-step probe
+ * sample (engine.py:252-257) without a host round trip. */
+int mlb_probe(const mlb_plan *plan, const void *d_f, int x, int y, int lz,
+              double *d_out4, void *stream);
+
+/* ---- host-buffer entry points: what the reference's callers hold ---------
+ * mlb_step_host is KernelPlan.step(fpre, fpost) on HOST blocks: uploads
+ * both (the never-written cells of fpost must survive), steps, downloads
+ * fpost.  d_a / d_b are caller-owned device scratch blocks (layout.bytes
+ * each).  Synchronous, like the reference call. */
+int mlb_step_host(mlb_plan *plan, const void *h_fpre, void *h_fpost,
+                  void *d_a, void *d_b, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MLB_H */

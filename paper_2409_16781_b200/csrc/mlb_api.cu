@@ -1,0 +1,634 @@
+// mlb_api.cu - host side of the C ABI declared in include/mlb.h.
+//
+// Thin: argument checks, the flag-derived tables, launches.  All device
+// code lives in mlb_kernels.cuh.  Build (see csrc/Makefile):
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false
+//        -shared -Xcompiler -fPIC -o libmlb_d3q19.so mlb_api.cu
+#include "../../include/mlb.h"
+#include "mlb_kernels.cuh"
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+namespace {
+
+thread_local char g_err[512] = "";
+std::atomic<long long> g_launches{0};
+
+int fail(int code, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define MLB_CUDA(expr)                                                          \
+    do {                                                                        \
+        cudaError_t e_ = (expr);                                                \
+        if (e_ != cudaSuccess)                                                  \
+            return fail(MLB_ECUDA, "%s: %s (%s:%d)", #expr,                     \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);            \
+    } while (0)
+
+#define MLB_LAUNCHED()                                                          \
+    do {                                                                        \
+        g_launches.fetch_add(1, std::memory_order_relaxed);                     \
+        MLB_CUDA(cudaGetLastError());                                           \
+    } while (0)
+
+inline cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+struct mlb_plan {
+    int nx = 0, ny = 0, nz = 0, dtype = 0, device = 0, z_mode = 0, variant = 0;
+    double omega = 1.0, wall_u[3] = {0, 0, 0}, inlet_u = 0.0;
+    mlb_layout lay{};
+    mlb::Geom g{};
+    bool have_flags = false;
+    uint8_t *d_flags = nullptr;  // padded flag block incl. halo planes
+    uint8_t *d_cls = nullptr;    // class table, same shape
+    // open-boundary index lists, sorted by (lz, y, x); *_zoff[lz] = first entry of plane lz
+    long long n_in = 0, n_out = 0;
+    long long *d_in = nullptr, *d_out = nullptr;
+    std::vector<long long> in_zoff, out_zoff;
+    bool out_chained = false;
+    void *d_out_tmp = nullptr;
+    // reductions
+    int diag_blocks = 0;
+    double *d_partials = nullptr, *d_diag = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+int layout_of(int nx, int ny, int nz, int dtype, mlb_layout *out)
+{
+    if (nx < 1 || ny < 1 || nz < 1)
+        return fail(MLB_EINVAL, "grid %dx%dx%d is empty", nx, ny, nz);
+    if (dtype != MLB_F32 && dtype != MLB_F64)
+        return fail(MLB_EINVAL, "unknown dtype code %d (0 = f32, 1 = f64)", dtype);
+    if (ny > 65535 || nz > 65535)
+        return fail(MLB_EUNSUPPORTED, "ny and nz are limited to 65535 per slab");
+    const int sz = dtype == MLB_F32 ? 4 : 8;
+    const long long line = 128 / sz;
+    out->nx = nx; out->ny = ny; out->nz = nz; out->itemsize = sz;
+    out->xp = (nx + line - 1) / line * line;
+    out->plane = (long long)ny * out->xp;
+    out->pop = (long long)(nz + 2) * out->plane;
+    out->total = MLB_Q * out->pop;
+    out->bytes = out->total * sz;
+    return MLB_OK;
+}
+
+void set_geom(mlb_plan *p)
+{
+    p->g.nx = p->nx; p->g.ny = p->ny; p->g.nz = p->nz;
+    p->g.xp = p->lay.xp; p->g.plane = p->lay.plane; p->g.pop = p->lay.pop;
+    if (p->z_mode == MLB_Z_PERIODIC) {
+        p->g.zlo_src = p->nz;  // storage plane of lz = nz-1
+        p->g.zhi_src = 1;      // storage plane of lz = 0
+    } else {
+        p->g.zlo_src = 0;
+        p->g.zhi_src = p->nz + 1;
+    }
+}
+
+template <typename T>
+void wall_terms(const double *uw, T *k)
+{
+    // 6 w_i (c_i . u_w): one product per +direction, the opposite by
+    // negation, as kernels.py:249-256 builds its eight.
+    const T ms = T(1.0 / 3.0), md = T(1.0 / 6.0);
+    const T x = T(uw[0]), y = T(uw[1]), z = T(uw[2]);
+    k[0] = T(0.0);
+    k[1] = ms * x;        k[3] = -k[1];
+    k[2] = ms * y;        k[4] = -k[2];
+    k[5] = md * (x + y);  k[7] = -k[5];
+    k[6] = md * (y - x);  k[8] = -k[6];
+    k[9] = ms * z;        k[10] = -k[9];
+    k[11] = md * (x + z); k[13] = -k[11];
+    k[12] = md * (z - x); k[14] = -k[12];
+    k[15] = md * (y + z); k[17] = -k[15];
+    k[16] = md * (z - y); k[18] = -k[16];
+}
+
+// equilibrium(1, u_in, 0, 0) in compute dtype, lattice.py:60-109 factoring.
+// Host code: the Makefile passes -ffp-contract=off to the host compiler so
+// this is one rounding per operation, like the device code.
+template <typename T>
+void inlet_values(double u_in, T *e)
+{
+    const T one = T(1.0), c3 = T(3.0), c45 = T(4.5), c15 = T(1.5);
+    const T w0 = T(1.0 / 3.0), ws = T(1.0 / 18.0), wd = T(1.0 / 36.0);
+    const T rho = T(1.0), ux = T(u_in), uy = T(0.0), uz = T(0.0);
+    const T usq = ux * ux + uy * uy + uz * uz;
+    const T um = one - c15 * usq;
+    const T wr0 = w0 * rho, wrs = ws * rho, wrd = wd * rho;
+    auto pair = [&](T cu, T wr, int ip, int im) {
+        const T q = c45 * (cu * cu);
+        const T t = c3 * cu;
+        const T p = um + q;
+        e[ip] = wr * (p + t);
+        e[im] = wr * (p - t);
+    };
+    pair(ux, wrs, 1, 3);
+    pair(uy, wrs, 2, 4);
+    pair(ux + uy, wrd, 5, 7);
+    pair(ux - uy, wrd, 8, 6);
+    pair(uz, wrs, 9, 10);
+    pair(ux + uz, wrd, 11, 13);
+    pair(ux - uz, wrd, 14, 12);
+    pair(uy + uz, wrd, 15, 17);
+    pair(uy - uz, wrd, 18, 16);
+    e[0] = wr0 * um;
+}
+
+template <typename T>
+int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1,
+                cudaStream_t st)
+{
+    mlb::StepArgs<T> a;
+    a.fpre = static_cast<const T *>(fpre);
+    a.fpost = static_cast<T *>(fpost);
+    a.cls = p->d_cls;
+    a.g = p->g;
+    a.z0 = z0;
+    a.omega = T(p->omega);
+    wall_terms<T>(p->wall_u, a.k);
+    int bx = p->variant > 0 ? p->variant : 128;
+    while (bx > 32 && bx / 2 >= p->nx)
+        bx /= 2;
+    const dim3 grid((p->nx + bx - 1) / bx, p->ny, z1 - z0);
+    switch (bx) {
+    case 32: mlb::step_kernel<T, 32><<<grid, 32, 0, st>>>(a); break;
+    case 64: mlb::step_kernel<T, 64><<<grid, 64, 0, st>>>(a); break;
+    case 128: mlb::step_kernel<T, 128><<<grid, 128, 0, st>>>(a); break;
+    case 256: mlb::step_kernel<T, 256><<<grid, 256, 0, st>>>(a); break;
+    case 512: mlb::step_kernel<T, 512><<<grid, 512, 0, st>>>(a); break;
+    default: return fail(MLB_EINVAL, "variant %d is not a block width", p->variant);
+    }
+    MLB_LAUNCHED();
+    return MLB_OK;
+}
+
+template <typename T>
+int launch_open(mlb_plan *p, void *fpost, int z0, int z1, cudaStream_t st)
+{
+    T *f = static_cast<T *>(fpost);
+    const long long i0 = p->in_zoff[z0], i1 = p->in_zoff[z1];
+    if (i1 > i0) {
+        mlb::InletVals<T> v;
+        inlet_values<T>(p->inlet_u, v.v);
+        const long long n = i1 - i0;
+        mlb::inlet_kernel<T><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+            f, p->d_in + i0, n, p->lay.pop, v);
+        MLB_LAUNCHED();
+    }
+    const long long o0 = p->out_zoff[z0], o1 = p->out_zoff[z1];
+    if (o1 > o0) {
+        const long long n = o1 - o0;
+        const unsigned blocks = (unsigned)((n + 127) / 128);
+        T *tmp = static_cast<T *>(p->d_out_tmp);
+        if (!p->out_chained) {
+            mlb::outlet_kernel<T><<<blocks, 128, 0, st>>>(f, tmp, p->d_out + o0, n,
+                                                          p->lay.pop, p->n_out, 0);
+            MLB_LAUNCHED();
+        } else {
+            mlb::outlet_kernel<T><<<blocks, 128, 0, st>>>(f, tmp, p->d_out + o0, n,
+                                                          p->lay.pop, p->n_out, 1);
+            MLB_LAUNCHED();
+            mlb::outlet_kernel<T><<<blocks, 128, 0, st>>>(f, tmp, p->d_out + o0, n,
+                                                          p->lay.pop, p->n_out, 2);
+            MLB_LAUNCHED();
+        }
+    }
+    return MLB_OK;
+}
+
+int check_plan(const mlb_plan *p, bool need_flags)
+{
+    if (!p)
+        return fail(MLB_EINVAL, "plan is NULL");
+    if (need_flags && !p->have_flags)
+        return fail(MLB_EINVAL, "plan has no flags: call mlb_plan_set_flags first");
+    return MLB_OK;
+}
+
+int copy_dense(const mlb_plan *p, const void *src, void *dst, bool to_device,
+               cudaStream_t st)
+{
+    const int sz = p->lay.itemsize;
+    const size_t row = (size_t)p->nx * sz;
+    const size_t rows = (size_t)p->nz * p->ny;
+    const size_t dense_pop = rows * row;
+    for (int q = 0; q < MLB_Q; ++q) {
+        const char *h = static_cast<const char *>(to_device ? src : dst) + q * dense_pop;
+        const char *d = static_cast<const char *>(to_device ? dst : src)
+                      + ((size_t)q * p->lay.pop + p->lay.plane) * sz;
+        if (p->lay.xp == p->nx) {
+            if (to_device)
+                MLB_CUDA(cudaMemcpyAsync((void *)d, h, dense_pop, cudaMemcpyHostToDevice, st));
+            else
+                MLB_CUDA(cudaMemcpyAsync((void *)h, d, dense_pop, cudaMemcpyDeviceToHost, st));
+        } else {
+            if (to_device)
+                MLB_CUDA(cudaMemcpy2DAsync((void *)d, (size_t)p->lay.xp * sz, h, row, row, rows,
+                                           cudaMemcpyHostToDevice, st));
+            else
+                MLB_CUDA(cudaMemcpy2DAsync((void *)h, row, d, (size_t)p->lay.xp * sz, row, rows,
+                                           cudaMemcpyDeviceToHost, st));
+        }
+    }
+    return MLB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *mlb_last_error(void) { return g_err; }
+int mlb_abi_version(void) { return MLB_ABI_VERSION; }
+int64_t mlb_launch_count(void) { return g_launches.load(); }
+
+int mlb_layout_query(int nx, int ny, int nz, int dtype, mlb_layout *out)
+{
+    if (!out)
+        return fail(MLB_EINVAL, "out is NULL");
+    return layout_of(nx, ny, nz, dtype, out);
+}
+
+int mlb_plan_create(mlb_plan **out, int nx, int ny, int nz, int dtype, double omega,
+                    const double wall_u[3], double inlet_u, int device, int z_mode)
+{
+    if (!out)
+        return fail(MLB_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (z_mode != MLB_Z_PERIODIC && z_mode != MLB_Z_HALO)
+        return fail(MLB_EINVAL, "unknown z_mode %d", z_mode);
+    mlb_layout lay;
+    if (int rc = layout_of(nx, ny, nz, dtype, &lay))
+        return rc;
+    int ndev = 0;
+    MLB_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return fail(MLB_EINVAL, "device %d out of range (%d visible)", device, ndev);
+    MLB_CUDA(cudaSetDevice(device));
+    mlb_plan *p = new (std::nothrow) mlb_plan;
+    if (!p)
+        return fail(MLB_ENOMEM, "out of host memory");
+    p->nx = nx; p->ny = ny; p->nz = nz; p->dtype = dtype;
+    p->device = device; p->z_mode = z_mode; p->lay = lay;
+    set_geom(p);
+    if (int rc = mlb_plan_set_physics(p, omega, wall_u, inlet_u)) {
+        delete p;
+        return rc;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    p->diag_blocks = sms * 8;
+    cudaError_t e = cudaMalloc(&p->d_partials, sizeof(double) * mlb::DIAG_N * p->diag_blocks);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_diag, sizeof(double) * mlb::DIAG_N);
+    if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&p->ev1);
+    if (e != cudaSuccess) {
+        mlb_plan_destroy(p);
+        return fail(MLB_ECUDA, "plan setup: %s", cudaGetErrorString(e));
+    }
+    *out = p;
+    return MLB_OK;
+}
+
+int mlb_plan_destroy(mlb_plan *p)
+{
+    if (!p)
+        return MLB_OK;
+    cudaSetDevice(p->device);
+    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_in); cudaFree(p->d_out);
+    cudaFree(p->d_out_tmp); cudaFree(p->d_partials); cudaFree(p->d_diag);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+    delete p;
+    return MLB_OK;
+}
+
+int mlb_plan_get_layout(const mlb_plan *p, mlb_layout *out)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (!out) return fail(MLB_EINVAL, "out is NULL");
+    *out = p->lay;
+    return MLB_OK;
+}
+
+int mlb_plan_set_physics(mlb_plan *p, double omega, const double wall_u[3], double inlet_u)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    // omega = 0 is legal kernel input (pure streaming, test_kernels.py:152-164)
+    if (!(omega >= 0.0 && omega < 2.0))
+        return fail(MLB_EINVAL, "relaxation rate omega=%g outside [0, 2)", omega);
+    p->omega = omega;
+    for (int i = 0; i < 3; ++i)
+        p->wall_u[i] = wall_u ? wall_u[i] : 0.0;
+    p->inlet_u = inlet_u;
+    return MLB_OK;
+}
+
+int mlb_plan_set_variant(mlb_plan *p, int variant)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (variant != 0 && variant != 32 && variant != 64 && variant != 128
+        && variant != 256 && variant != 512)
+        return fail(MLB_EINVAL, "variant must be 0 or a block width in {32..512}");
+    p->variant = variant;
+    return MLB_OK;
+}
+
+int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
+                       const uint8_t *h_hi)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (!h_flags)
+        return fail(MLB_EINVAL, "h_flags is NULL");
+    MLB_CUDA(cudaSetDevice(p->device));
+    const int nx = p->nx, ny = p->ny, nz = p->nz;
+    const long long xp = p->lay.xp, plane = p->lay.plane;
+    const size_t padded = (size_t)(nz + 2) * plane;
+    std::vector<uint8_t> pad(padded, (uint8_t)1);  // row padding = solid
+    std::vector<long long> in_idx, out_idx;
+    p->in_zoff.assign(nz + 1, 0);
+    p->out_zoff.assign(nz + 1, 0);
+    const size_t dense_plane = (size_t)nx * ny;
+    for (int sz = 0; sz < nz + 2; ++sz) {
+        const uint8_t *src;
+        if (sz == 0)
+            src = h_lo ? h_lo : h_flags + (size_t)(nz - 1) * dense_plane;
+        else if (sz == nz + 1)
+            src = h_hi ? h_hi : h_flags;
+        else
+            src = h_flags + (size_t)(sz - 1) * dense_plane;
+        const bool interior = sz >= 1 && sz <= nz;
+        if (interior) {
+            p->in_zoff[sz - 1] = (long long)in_idx.size();
+            p->out_zoff[sz - 1] = (long long)out_idx.size();
+        }
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x) {
+                const uint8_t m = src[(size_t)y * nx + x];
+                if (m > 4)
+                    return fail(MLB_EINVAL, "flag array holds unknown cell code %d at "
+                                "(x=%d, y=%d, plane=%d)", (int)m, x, y, sz - 1);
+                const long long d = (long long)sz * plane + (long long)y * xp + x;
+                pad[d] = m;
+                if (!interior)
+                    continue;
+                if (m == 3)
+                    in_idx.push_back(d);
+                else if (m == 4) {
+                    if (x == 0)
+                        return fail(MLB_EUNSUPPORTED, "outlet cell at x = 0 (y=%d, z=%d): "
+                                    "its source would be the previous row's last cell", y, sz - 1);
+                    out_idx.push_back(d);
+                }
+            }
+    }
+    p->in_zoff[nz] = (long long)in_idx.size();
+    p->out_zoff[nz] = (long long)out_idx.size();
+    // an outlet cell whose source is itself an outlet cell forces the
+    // gather-then-scatter form (numpy evaluates the right-hand side first)
+    p->out_chained = false;
+    for (size_t j = 1; j < out_idx.size(); ++j)
+        if (out_idx[j] - 1 == out_idx[j - 1]) {
+            p->out_chained = true;
+            break;
+        }
+
+    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_in); cudaFree(p->d_out);
+    cudaFree(p->d_out_tmp);
+    p->d_flags = p->d_cls = nullptr; p->d_in = p->d_out = nullptr; p->d_out_tmp = nullptr;
+    p->have_flags = false;
+    MLB_CUDA(cudaMalloc(&p->d_flags, padded));
+    MLB_CUDA(cudaMalloc(&p->d_cls, padded));
+    MLB_CUDA(cudaMemcpy(p->d_flags, pad.data(), padded, cudaMemcpyHostToDevice));
+    p->n_in = (long long)in_idx.size();
+    p->n_out = (long long)out_idx.size();
+    if (p->n_in) {
+        MLB_CUDA(cudaMalloc(&p->d_in, sizeof(long long) * p->n_in));
+        MLB_CUDA(cudaMemcpy(p->d_in, in_idx.data(), sizeof(long long) * p->n_in,
+                            cudaMemcpyHostToDevice));
+    }
+    if (p->n_out) {
+        MLB_CUDA(cudaMalloc(&p->d_out, sizeof(long long) * p->n_out));
+        MLB_CUDA(cudaMemcpy(p->d_out, out_idx.data(), sizeof(long long) * p->n_out,
+                            cudaMemcpyHostToDevice));
+        if (p->out_chained)
+            MLB_CUDA(cudaMalloc(&p->d_out_tmp, (size_t)p->lay.itemsize * MLB_Q * p->n_out));
+    }
+    const dim3 grid((unsigned)((xp + 127) / 128), ny, nz + 2);
+    mlb::build_cls_kernel<<<grid, 128>>>(p->d_flags, p->d_cls, p->g);
+    MLB_LAUNCHED();
+    MLB_CUDA(cudaDeviceSynchronize());
+    p->have_flags = true;
+    return MLB_OK;
+}
+
+int mlb_plan_get_flags(const mlb_plan *p, uint8_t *h_flags)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (!h_flags) return fail(MLB_EINVAL, "h_flags is NULL");
+    MLB_CUDA(cudaSetDevice(p->device));
+    // from the class table's low bits: proves the bytes the kernel tests
+    const size_t padded = (size_t)(p->nz + 2) * p->lay.plane;
+    std::vector<uint8_t> pad(padded);
+    MLB_CUDA(cudaMemcpy(pad.data(), p->d_cls, padded, cudaMemcpyDeviceToHost));
+    for (int z = 0; z < p->nz; ++z)
+        for (int y = 0; y < p->ny; ++y)
+            for (int x = 0; x < p->nx; ++x)
+                h_flags[((size_t)z * p->ny + y) * p->nx + x] =
+                    pad[(size_t)(z + 1) * p->lay.plane + (size_t)y * p->lay.xp + x]
+                    & mlb::CLS_FLAG;
+    return MLB_OK;
+}
+
+int mlb_upload(const mlb_plan *p, const void *h_dense, void *d_f, void *stream)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (!h_dense || !d_f) return fail(MLB_EINVAL, "NULL buffer");
+    MLB_CUDA(cudaSetDevice(p->device));
+    return copy_dense(p, h_dense, d_f, true, S(stream));
+}
+
+int mlb_download(const mlb_plan *p, const void *d_f, void *h_dense, void *stream)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (!h_dense || !d_f) return fail(MLB_EINVAL, "NULL buffer");
+    MLB_CUDA(cudaSetDevice(p->device));
+    return copy_dense(p, d_f, h_dense, false, S(stream));
+}
+
+int mlb_step_range(mlb_plan *p, const void *d_fpre, void *d_fpost, int z0, int z1,
+                   void *stream)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (!d_fpre || !d_fpost) return fail(MLB_EINVAL, "NULL population block");
+    if (d_fpre == d_fpost)
+        return fail(MLB_EINVAL, "fpre and fpost must be distinct blocks");
+    if (z0 < 0 || z1 > p->nz || z0 > z1)
+        return fail(MLB_EINVAL, "plane range [%d, %d) outside [0, %d)", z0, z1, p->nz);
+    if (z0 == z1) return MLB_OK;
+    MLB_CUDA(cudaSetDevice(p->device));
+    return p->dtype == MLB_F32 ? launch_step<float>(p, d_fpre, d_fpost, z0, z1, S(stream))
+                               : launch_step<double>(p, d_fpre, d_fpost, z0, z1, S(stream));
+}
+
+int mlb_step(mlb_plan *p, const void *d_fpre, void *d_fpost, void *stream)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    return mlb_step_range(p, d_fpre, d_fpost, 0, p->nz, stream);
+}
+
+int mlb_open_pass_range(mlb_plan *p, void *d_fpost, int z0, int z1, void *stream)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (!d_fpost) return fail(MLB_EINVAL, "NULL population block");
+    if (z0 < 0 || z1 > p->nz || z0 > z1)
+        return fail(MLB_EINVAL, "plane range [%d, %d) outside [0, %d)", z0, z1, p->nz);
+    if (p->n_in == 0 && p->n_out == 0) return MLB_OK;
+    MLB_CUDA(cudaSetDevice(p->device));
+    return p->dtype == MLB_F32 ? launch_open<float>(p, d_fpost, z0, z1, S(stream))
+                               : launch_open<double>(p, d_fpost, z0, z1, S(stream));
+}
+
+int mlb_open_pass(mlb_plan *p, void *d_fpost, void *stream)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    return mlb_open_pass_range(p, d_fpost, 0, p->nz, stream);
+}
+
+int mlb_run_steps(mlb_plan *p, void *d_a, void *d_b, int nsteps, void *stream, float *ms)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (p->z_mode != MLB_Z_PERIODIC)
+        return fail(MLB_EUNSUPPORTED, "mlb_run_steps needs an MLB_Z_PERIODIC plan; a slab's "
+                    "halo exchange happens between steps, outside this library");
+    if (nsteps < 0) return fail(MLB_EINVAL, "nsteps < 0");
+    MLB_CUDA(cudaSetDevice(p->device));
+    if (ms) MLB_CUDA(cudaEventRecord(p->ev0, S(stream)));
+    void *pre = d_a, *post = d_b;
+    for (int t = 0; t < nsteps; ++t) {
+        if (int rc = mlb_step_range(p, pre, post, 0, p->nz, stream)) return rc;
+        if (int rc = mlb_open_pass_range(p, post, 0, p->nz, stream)) return rc;
+        void *tmp = pre; pre = post; post = tmp;
+    }
+    if (ms) {
+        MLB_CUDA(cudaEventRecord(p->ev1, S(stream)));
+        MLB_CUDA(cudaEventSynchronize(p->ev1));
+        MLB_CUDA(cudaEventElapsedTime(ms, p->ev0, p->ev1));
+    }
+    return MLB_OK;
+}
+
+int mlb_halo_copy(const mlb_plan *p, void *d_dst, const void *d_src, int src_nz, int face,
+                  void *stream)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (!d_dst || !d_src) return fail(MLB_EINVAL, "NULL population block");
+    if (src_nz < 1 || (face != 0 && face != 1))
+        return fail(MLB_EINVAL, "bad src_nz %d / face %d", src_nz, face);
+    MLB_CUDA(cudaSetDevice(p->device));
+    static const int UP[5] = {9, 11, 12, 15, 16};     // c_z = +1
+    static const int DOWN[5] = {10, 13, 14, 17, 18};  // c_z = -1
+    const long long plane = p->lay.plane;
+    const long long src_pop = (long long)(src_nz + 2) * plane;
+    mlb::HaloArgs h;
+    for (int j = 0; j < 5; ++j) {
+        const int q = face == 0 ? UP[j] : DOWN[j];
+        h.src_off[j] = q * src_pop + (face == 0 ? (long long)src_nz : 1LL) * plane;
+        h.dst_off[j] = q * p->lay.pop + (face == 0 ? 0LL : (long long)(p->nz + 1)) * plane;
+    }
+    h.words = plane * p->lay.itemsize / 16;
+    const dim3 grid((unsigned)((h.words + 255) / 256), 5);
+    mlb::halo_copy_kernel<<<grid, 256, 0, S(stream)>>>(d_src, d_dst, h, p->lay.itemsize);
+    MLB_LAUNCHED();
+    return MLB_OK;
+}
+
+int mlb_macro(const mlb_plan *p, const void *d_f, double *d_rho, double *d_ux, double *d_uy,
+              double *d_uz, void *stream)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (!d_f || !d_rho || !d_ux || !d_uy || !d_uz) return fail(MLB_EINVAL, "NULL buffer");
+    MLB_CUDA(cudaSetDevice(p->device));
+    const dim3 grid((p->nx + 127) / 128, p->ny, p->nz);
+    if (p->dtype == MLB_F32)
+        mlb::macro_kernel<float><<<grid, 128, 0, S(stream)>>>(
+            static_cast<const float *>(d_f), p->g, d_rho, d_ux, d_uy, d_uz);
+    else
+        mlb::macro_kernel<double><<<grid, 128, 0, S(stream)>>>(
+            static_cast<const double *>(d_f), p->g, d_rho, d_ux, d_uy, d_uz);
+    MLB_LAUNCHED();
+    return MLB_OK;
+}
+
+int mlb_diagnostics(mlb_plan *p, const void *d_f, double h_out[8], void *stream)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (!d_f || !h_out) return fail(MLB_EINVAL, "NULL buffer");
+    MLB_CUDA(cudaSetDevice(p->device));
+    if (p->dtype == MLB_F32)
+        mlb::diag_kernel<float><<<p->diag_blocks, mlb::DIAG_THREADS, 0, S(stream)>>>(
+            static_cast<const float *>(d_f), p->d_cls, p->g, p->d_partials);
+    else
+        mlb::diag_kernel<double><<<p->diag_blocks, mlb::DIAG_THREADS, 0, S(stream)>>>(
+            static_cast<const double *>(d_f), p->d_cls, p->g, p->d_partials);
+    MLB_LAUNCHED();
+    mlb::diag_final_kernel<<<1, mlb::DIAG_THREADS, 0, S(stream)>>>(p->d_partials,
+                                                                  p->diag_blocks, p->d_diag);
+    MLB_LAUNCHED();
+    MLB_CUDA(cudaMemcpyAsync(h_out, p->d_diag, sizeof(double) * mlb::DIAG_N,
+                             cudaMemcpyDeviceToHost, S(stream)));
+    MLB_CUDA(cudaStreamSynchronize(S(stream)));
+    return MLB_OK;
+}
+
+int mlb_probe(const mlb_plan *p, const void *d_f, int x, int y, int lz, double *d_out4,
+              void *stream)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (!d_f || !d_out4) return fail(MLB_EINVAL, "NULL buffer");
+    if (x < 0 || x >= p->nx || y < 0 || y >= p->ny || lz < 0 || lz >= p->nz)
+        return fail(MLB_EINVAL, "probe cell (%d, %d, %d) outside the slab", x, y, lz);
+    MLB_CUDA(cudaSetDevice(p->device));
+    if (p->dtype == MLB_F32)
+        mlb::probe_kernel<float><<<1, 1, 0, S(stream)>>>(static_cast<const float *>(d_f),
+                                                         p->g, x, y, lz, d_out4);
+    else
+        mlb::probe_kernel<double><<<1, 1, 0, S(stream)>>>(static_cast<const double *>(d_f),
+                                                          p->g, x, y, lz, d_out4);
+    MLB_LAUNCHED();
+    return MLB_OK;
+}
+
+int mlb_step_host(mlb_plan *p, const void *h_fpre, void *h_fpost, void *d_a, void *d_b,
+                  void *stream)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (!h_fpre || !h_fpost || !d_a || !d_b) return fail(MLB_EINVAL, "NULL buffer");
+    if (h_fpre == h_fpost)
+        return fail(MLB_EINVAL, "fpre and fpost must be distinct blocks");
+    if (p->z_mode != MLB_Z_PERIODIC)
+        return fail(MLB_EUNSUPPORTED, "mlb_step_host needs an MLB_Z_PERIODIC plan");
+    if (int rc = mlb_upload(p, h_fpre, d_a, stream)) return rc;
+    if (int rc = mlb_upload(p, h_fpost, d_b, stream)) return rc;
+    if (int rc = mlb_step(p, d_a, d_b, stream)) return rc;
+    if (int rc = mlb_download(p, d_b, h_fpost, stream)) return rc;
+    MLB_CUDA(cudaStreamSynchronize(S(stream)));
+    return MLB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,371 @@
+"""Time stepping and run orchestration on the CUDA path.
+
+Host-side mirror of /root/reference/pkg/src/lb2d/engine.py: `Schedule`
+(:36-60), `RunConfig` (:63-81), `SimState` (:84-125),
+`state_from_macroscopic` (:128-153), `build_plan` (:183-190), `step`
+(:193-205), `run` -> `RunStats` (:208-275).  Same names, argument meaning
+and error behaviour, one more dimension.  The reference's driver code keeps
+working against host `SimState`s; what changes is where a step executes:
+
+* the state's host arrays (dense `(19, N)` blocks, x fastest) stay the
+  user-visible truth, exactly as in the reference;
+* `run` uploads them to the padded device layout, advances on the GPU
+  through the C ABI (fused kernel, open-boundary pass, swap - the
+  reference's timed loop body, engine.py:244-249), fires the same hooks at
+  the same cadence with the host arrays synchronised first, and downloads
+  at the end.  `RunStats.seconds` is device time of the update loop from
+  CUDA events (the reference times the same region with perf_counter).
+* `Session` is the resident form of the same thing for callers that do not
+  want the upload/download around every `run`.
+
+Diagnostics (`macro`, `diagnostics`, `check_finite`, the per-step probe)
+execute on the device too; there is no CPU compute path in this package.
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import boundaries
+from .fields import (Layout, PopulationField, Precision, convert_precision,
+                     flatten_xyz)
+from .kernels import BACKEND, DeviceField, KernelPlan, pinned_empty  # noqa: F401
+from .lattice import Q, RelaxationParams, equilibrium
+
+
+class DivergenceError(RuntimeError):
+    """Raised when a safety check finds non-finite populations."""
+
+
+@dataclass
+class Schedule:
+    """Traversal policy: 'auto' or 'tiled' with explicit tile sizes.
+
+    On the GPU a tile's x extent selects the thread-block width; like the
+    reference's tiles it is a pure performance knob and never changes bits.
+    """
+
+    kind: str = "auto"
+    tx: int = 0
+    ty: int = 0
+    tz: int = 1
+
+    def __post_init__(self):
+        if self.kind not in ("auto", "tiled"):
+            raise ValueError(f"unknown schedule '{self.kind}'")
+        if self.kind == "tiled" and (self.tx < 1 or self.ty < 1 or self.tz < 1):
+            raise ValueError("tiled schedule needs positive tile sizes")
+
+    def resolve(self, nx, ny, nz, layout):
+        if self.kind == "auto":
+            return None
+        if self.tx > nx or self.ty > ny or self.tz > nz:
+            raise ValueError(f"tile {self.tx}x{self.ty}x{self.tz} exceeds the "
+                             f"{nx}x{ny}x{nz} grid")
+        return (self.tx, self.ty, self.tz)
+
+    def label(self):
+        return ("auto" if self.kind == "auto"
+                else f"tiled({self.tx},{self.ty},{self.tz})")
+
+
+@dataclass
+class RunConfig:
+    """Everything a run needs beyond the initial state."""
+
+    steps: int
+    precision: Precision = Precision.SINGLE
+    layout: Layout = Layout.ROW
+    schedule: Schedule = field(default_factory=Schedule)
+    threads: int = 0  # accepted for API parity; the GPU path has no thread pool
+    output_every: int = 0
+    checkpoint_every: int = 0
+    out_dir: str = "out"
+    device: int | None = None
+
+    def __post_init__(self):
+        if self.steps < 1:
+            raise ValueError("steps must be >= 1")
+        for name in ("threads", "output_every", "checkpoint_every"):
+            if getattr(self, name) < 0:
+                raise ValueError(f"{name} must be >= 0")
+
+
+@dataclass
+class SimState:
+    """Populations, geometry, and physics of one simulation (host view)."""
+
+    f_pre: PopulationField
+    f_post_: PopulationField | None
+    mask: np.ndarray
+    nx: int
+    ny: int
+    nz: int
+    layout: Layout
+    precision: Precision
+    t: int = 0
+    params: RelaxationParams | None = None
+    wall_u: tuple = (0.0, 0.0, 0.0)
+    inlet_u: float = 0.0
+    case: str = ""
+    session: "Session | None" = field(default=None, repr=False)
+
+    @property
+    def f_post(self):
+        """The second buffer.  Both buffers start identical (engine.py:148);
+        the host copy is materialised on first use so a state that only ever
+        steps on the GPU never pays for it."""
+        if self.f_post_ is None:
+            post = PopulationField(
+                pinned_empty(self.f_pre.data.shape, self.f_pre.data.dtype),
+                self.nx, self.ny, self.nz, self.layout)
+            if self.session is not None and self.session.host_stale:
+                self.session.plan.download(self.session.post, post.data)
+            else:
+                np.copyto(post.data, self.f_pre.data)
+            self.f_post_ = post
+        return self.f_post_
+
+    def swap(self):
+        self.f_pre, self.f_post_ = self.f_post, self.f_pre
+        if self.session is not None:
+            self.session.pre, self.session.post = self.session.post, self.session.pre
+
+    def _session_for_diagnostics(self):
+        if self.session is not None:
+            return self.session, False
+        omega = self.params.omega if self.params is not None else 1.0
+        plan = KernelPlan(self.nx, self.ny, self.nz, self.layout, self.precision,
+                          self.mask, omega, self.wall_u, inlet_u=self.inlet_u)
+        return Session(self, plan), True
+
+    def macro(self):
+        """Density and velocity as float64 a[x, y, z] grids (engine.py:104-118),
+        computed by the CUDA macro kernel."""
+        sess, temp = self._session_for_diagnostics()
+        try:
+            out = tuple(t.cpu().numpy().transpose(2, 1, 0)
+                        for t in sess.plan.macro(sess.pre))
+        finally:
+            if temp:
+                sess.close(sync=False)
+        return out
+
+    def diagnostics(self):
+        """Total mass, momentum, kinetic energy, max |u|, non-finite count,
+        fluid cells - deterministic device reductions."""
+        sess, temp = self._session_for_diagnostics()
+        try:
+            return sess.plan.diagnostics(sess.pre)
+        finally:
+            if temp:
+                sess.close(sync=False)
+
+    def fluid_cells(self):
+        return int(np.count_nonzero(self.mask == boundaries.FLUID))
+
+    def check_finite(self):
+        if self.diagnostics()["nonfinite"] != 0:
+            raise DivergenceError(f"divergence at step {self.t}")
+
+
+def state_from_macroscopic(rho, ux, uy, uz, mask_grid, layout, precision,
+                           params=None, wall_u=(0.0, 0.0, 0.0), inlet_u=0.0,
+                           case=""):
+    """Build a state from a[x, y, z] macroscopic grids at local equilibrium.
+
+    Initial populations are evaluated in float64 and converted once to the
+    storage precision under the strict overflow policy (engine.py:128-153).
+    Scalars are accepted for uniform fields: the nineteen equilibrium
+    values are then computed once and broadcast, which is the same
+    arithmetic on the same inputs per cell.
+    """
+    mask_grid = np.asarray(mask_grid, dtype=np.uint8)
+    nx, ny, nz = mask_grid.shape
+    n = nx * ny * nz
+    data = pinned_empty((Q, n), precision.storage)
+    if all(np.ndim(a) == 0 for a in (rho, ux, uy, uz)):
+        feq = equilibrium(float(rho), float(ux), float(uy), float(uz))
+        stored = convert_precision(feq, precision.storage, policy="strict")
+        for i in range(Q):
+            data[i].fill(stored[i])
+    else:
+        rho, ux, uy, uz = (np.broadcast_to(np.asarray(a, dtype=np.float64),
+                                           (nx, ny, nz)) for a in (rho, ux, uy, uz))
+        view = data.reshape(Q, nz, ny, nx)
+        for z in range(nz):  # plane by plane keeps the float64 temporaries small
+            feq = equilibrium(rho[:, :, z], ux[:, :, z], uy[:, :, z], uz[:, :, z])
+            stored = convert_precision(feq, precision.storage, policy="strict")
+            view[:, z] = stored.transpose(0, 2, 1)
+    f_pre = PopulationField(data, nx, ny, nz, layout)
+    return SimState(
+        f_pre=f_pre, f_post_=None, mask=boundaries.flatten_mask(mask_grid),
+        nx=nx, ny=ny, nz=nz, layout=layout, precision=precision,
+        params=params, wall_u=tuple(wall_u), inlet_u=float(inlet_u), case=case)
+
+
+def build_plan(state, config):
+    """KernelPlan for a state (engine.py:183-190), same error behaviour."""
+    if state.params is None:
+        raise ValueError("state has no relaxation parameters attached")
+    if state.params.has_source:
+        raise ValueError("the fused kernel runs the zero-source path only")
+    tile = config.schedule.resolve(state.nx, state.ny, state.nz, state.layout)
+    return KernelPlan(state.nx, state.ny, state.nz, state.layout, state.precision,
+                      state.mask, state.params.omega, state.wall_u, tile,
+                      inlet_u=state.inlet_u, device=config.device)
+
+
+class Session:
+    """A state resident on the GPU: two device blocks and the plan.
+
+    `attach` uploads the host arrays; stepping marks them stale; `sync_host`
+    downloads.  If the host never materialised its second buffer, the device
+    one is filled by a device-to-device copy (both start identical by
+    construction) and is not downloaded.
+    """
+
+    def __init__(self, state, plan):
+        self.state = state
+        self.plan = plan
+        self.pre = plan.alloc()
+        self.post = plan.alloc()
+        self.host_stale = False
+        self.upload()
+
+    def upload(self):
+        st = self.state
+        self.plan.upload(st.f_pre.data, self.pre)
+        if st.f_post_ is None:
+            self.post.tensor.copy_(self.pre.tensor)
+        else:
+            self.plan.upload(st.f_post_.data, self.post)
+        self.host_stale = False
+
+    def sync_host(self):
+        if not self.host_stale:
+            return
+        st = self.state
+        self.plan.download(self.pre, st.f_pre.data, sync=False)
+        if st.f_post_ is not None:
+            self.plan.download(self.post, st.f_post_.data, sync=False)
+        torch.cuda.current_stream(self.plan.device).synchronize()
+        self.host_stale = False
+
+    def advance(self, nsteps, timed=False):
+        """`nsteps` x (fused update, open-boundary pass, swap)."""
+        newest, other, ms = self.plan.run_steps(self.pre, self.post, nsteps, timed)
+        self.pre, self.post = newest, other
+        self.state.t += nsteps
+        self.host_stale = True
+        return ms
+
+    def close(self, sync=True):
+        if sync:
+            self.sync_host()
+        if self.state.session is self:
+            self.state.session = None
+        self.pre = self.post = None
+        self.plan.close()
+
+
+def open_session(state, config=None):
+    """Make `state` GPU-resident (uploads it) and return the session."""
+    if state.session is not None:
+        return state.session
+    config = config or RunConfig(steps=1, precision=state.precision,
+                                 layout=state.layout)
+    state.session = Session(state, build_plan(state, config))
+    return state.session
+
+
+def step(state, config=None, plan=None, open_pass=None):
+    """Advance the state one time step (engine.py:193-205).
+
+    Convenience form: makes the state resident if it is not, steps once and
+    brings the host arrays up to date, so callers written against the
+    reference see the new populations in `state.f_pre.data`.
+    """
+    own = state.session is None
+    sess = open_session(state, config)
+    sess.advance(1)
+    sess.sync_host()
+    if own:
+        sess.close()
+    return state
+
+
+@dataclass
+class RunStats:
+    steps: int
+    seconds: float
+    nx: int
+    ny: int
+    nz: int
+    mlups: float
+    probe_series: np.ndarray | None = None
+    probe_samples: np.ndarray | None = None
+
+
+def run(state, config, on_output=None, on_checkpoint=None, probe=None):
+    """Run `config.steps` steps, timing only the update loop (engine.py:208-275).
+
+    Hooks fire on multiples of their cadence: output hooks at every multiple
+    including the final step, checkpoint hooks only mid-run.  A finite check
+    runs at output cadence and raises DivergenceError on NaN/inf.  When
+    `probe` is an (x, y, z) cell its velocity is sampled every step on the
+    device; `RunStats.probe_series` is the y-velocity series as in the
+    reference, `probe_samples` the full (steps, 4) rho/u record.
+    """
+    own = state.session is None
+    sess = open_session(state, config)
+    if not own:
+        sess.upload()  # the host arrays are the truth at the start of a run
+    plan = sess.plan
+    dev = plan.device
+    end_t = state.t + config.steps
+    samples = (torch.zeros((config.steps, 4), dtype=torch.float64, device=dev)
+               if probe is not None else None)
+    events = []
+    done = 0
+    try:
+        while done < config.steps:
+            chunk = config.steps - done
+            if probe is not None:
+                chunk = 1
+            for every in (config.output_every, config.checkpoint_every):
+                if every:
+                    chunk = min(chunk, every - state.t % every)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.current_stream(dev))
+            sess.advance(chunk)
+            e1.record(torch.cuda.current_stream(dev))
+            events.append((e0, e1))
+            done += chunk
+            if samples is not None:
+                plan.probe(sess.pre, probe[0], probe[1], probe[2], samples[done - 1])
+            if config.output_every and state.t % config.output_every == 0:
+                state.check_finite()
+                if on_output is not None:
+                    sess.sync_host()
+                    on_output(state)
+            if (config.checkpoint_every and state.t < end_t
+                    and state.t % config.checkpoint_every == 0):
+                if on_checkpoint is not None:
+                    sess.sync_host()
+                    on_checkpoint(state)
+        sess.sync_host()
+        torch.cuda.current_stream(dev).synchronize()
+    finally:
+        if own:
+            sess.close(sync=False)
+    seconds = sum(a.elapsed_time(b) for a, b in events) * 1e-3
+    updates = state.nx * state.ny * state.nz * config.steps
+    mlups = updates / (seconds * 1e6) if seconds > 0.0 else float("inf")
+    rec = samples.cpu().numpy() if samples is not None else None
+    return RunStats(steps=config.steps, seconds=seconds, nx=state.nx, ny=state.ny,
+                    nz=state.nz, mlups=mlups,
+                    probe_series=(rec[:, 2].copy() if rec is not None else None),
+                    probe_samples=rec)

@@ -1,0 +1,307 @@
+"""The plugin boundary: `KernelPlan.step(fpre, fpost)` on CUDA.
+
+Host-side mirror of /root/reference/pkg/src/lb2d/kernels.py:398-462.  The
+reference's KernelPlan captures shape, precision, tile, wall velocity and
+relaxation rate and owns the backend machinery; `.step(fpre, fpost)` reads
+`fpre` and writes every fluid cell of `fpost` exactly once.  This one has
+the same shape (plus `nz`, a 3-component wall velocity, the inlet velocity
+the open-boundary pass needs, and a device), but its backend machinery is an
+opaque `mlb_plan*` from libmlb_d3q19.so (include/mlb.h) launching
+hand-written sm_100a kernels.  PyTorch appears here only as the owner of
+device buffers and streams: raw `data_ptr()` / `cuda_stream` values are all
+that cross the C ABI.
+
+`.step` accepts either the reference's HOST blocks - C-contiguous
+`(19, nx*ny*nz)` numpy arrays of the storage dtype, x fastest - in which
+case it is a synchronous upload / step / download like the reference call,
+or `DeviceField`s (the padded device layout), in which case it enqueues on
+the current CUDA stream and returns.
+
+Backend selection mirrors kernels.py:41-55: the environment variable
+`MLB_BACKEND` may be 'auto' or 'cuda'; anything else is a ValueError.
+There is exactly one backend and no CPU fallback.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+from . import _cabi
+from .fields import Layout, Precision
+from .lattice import Q
+
+
+def _pick_backend():
+    token = os.environ.get("MLB_BACKEND", "auto").strip().lower() or "auto"
+    if token in ("auto", "cuda"):
+        return "cuda"
+    raise ValueError(f"MLB_BACKEND must be 'auto' or 'cuda', got '{token}'")
+
+
+BACKEND = _pick_backend()
+
+_BLOCK_WIDTHS = (32, 64, 128, 256, 512)
+
+
+def _stream_ptr(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _host_ptr(a):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class DeviceField:
+    """One population block in the padded device layout, owned by torch.
+
+    `tensor` has shape (19, nz+2, ny, xp); storage plane 0 and nz+1 are the
+    halo planes, slab plane lz is storage plane lz+1, xp is nx rounded up
+    to a whole number of 128-byte lines (include/mlb.h).
+    """
+
+    def __init__(self, tensor, nx, ny, nz):
+        self.tensor = tensor
+        self.nx, self.ny, self.nz = nx, ny, nz
+
+    @property
+    def ptr(self):
+        return ctypes.c_void_p(self.tensor.data_ptr())
+
+    def plane(self, q, lz):
+        """View of population q, slab plane lz (-1 and nz are the halos)."""
+        return self.tensor[q, lz + 1]
+
+
+class KernelPlan:
+    """Everything one run needs to advance the populations one step."""
+
+    def __init__(self, nx, ny, nz, layout, precision, mask, omega,
+                 wall_u=(0.0, 0.0, 0.0), tile=None, backend=None, *,
+                 inlet_u=0.0, device=None, halo_lo=None, halo_hi=None,
+                 slab=False):
+        self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
+        if layout is not Layout.ROW:
+            raise ValueError("the CUDA path stores x fastest (Layout.ROW) only")
+        self.layout = layout
+        if not isinstance(precision, Precision):
+            precision = Precision.from_token(precision)
+        self.precision = precision
+        self.backend = backend or BACKEND
+        if self.backend != "cuda":
+            raise ValueError(f"unknown backend '{self.backend}'")
+        self.sx, self.sy, self.sz = layout.strides(self.nx, self.ny, self.nz)
+        if tile is None:
+            tile = (min(self.nx, 128), 1, 1)  # one contiguous line segment per block
+        tile = tuple(int(t) for t in tile) + (1,) * (3 - len(tile))
+        tx, ty, tz = tile
+        if not (1 <= tx <= self.nx and 1 <= ty <= self.ny and 1 <= tz <= self.nz):
+            raise ValueError(f"tile {tx}x{ty}x{tz} does not fit a "
+                             f"{self.nx}x{self.ny}x{self.nz} grid")
+        self.tile = tile
+        mask = np.ascontiguousarray(mask, dtype=np.uint8).reshape(-1)
+        if mask.size != self.nx * self.ny * self.nz:
+            raise ValueError(f"mask has {mask.size} cells, expected "
+                             f"{self.nx * self.ny * self.nz}")
+        self.mask = mask
+        self.wall_u = tuple(float(v) for v in wall_u) + (0.0,) * (3 - len(wall_u))
+        self.inlet_u = float(inlet_u)
+        self.omega = float(omega)
+        self.slab = bool(slab)
+
+        lib = _cabi.lib()  # raises RuntimeError if the extension is not built
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device is visible; the D3Q19 path has "
+                               "no CPU fallback")
+        self.device = torch.device("cuda", torch.cuda.current_device()
+                                   if device is None else int(device))
+        self._lib = lib
+        self._plan = ctypes.c_void_p()
+        uw = (ctypes.c_double * 3)(*self.wall_u)
+        _cabi.check(lib.mlb_plan_create(
+            ctypes.byref(self._plan), self.nx, self.ny, self.nz, precision.code,
+            self.omega, uw, self.inlet_u, self.device.index,
+            _cabi.MLB_Z_HALO if self.slab else _cabi.MLB_Z_PERIODIC))
+        self._layout = _cabi.Layout()
+        _cabi.check(lib.mlb_plan_get_layout(self._plan, ctypes.byref(self._layout)))
+        # block width: the largest supported width not above the tile's x extent
+        width = max([w for w in _BLOCK_WIDTHS if w <= max(tx, 32)])
+        _cabi.check(lib.mlb_plan_set_variant(self._plan, width))
+
+        def plane(h):
+            if h is None:
+                return None, ctypes.c_void_p(None)
+            h = np.ascontiguousarray(h, dtype=np.uint8).reshape(-1)
+            if h.size != self.nx * self.ny:
+                raise ValueError("halo flag plane must have nx*ny cells")
+            return h, _host_ptr(h)
+        lo, lo_p = plane(halo_lo)
+        hi, hi_p = plane(halo_hi)
+        _cabi.check(lib.mlb_plan_set_flags(self._plan, _host_ptr(mask), lo_p, hi_p))
+        self._scratch = None
+
+    # -- lifetime ----------------------------------------------------------
+    def close(self):
+        plan, self._plan = getattr(self, "_plan", None), None
+        if plan:
+            self._lib.mlb_plan_destroy(plan)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- geometry ----------------------------------------------------------
+    @property
+    def xp(self):
+        return int(self._layout.xp)
+
+    @property
+    def field_shape(self):
+        return (Q, self.nz + 2, self.ny, self.xp)
+
+    @property
+    def field_bytes(self):
+        return int(self._layout.bytes)
+
+    def alloc(self, zero=False):
+        """A caller-owned device population block (torch owns the memory)."""
+        make = torch.zeros if zero else torch.empty
+        t = make(self.field_shape, dtype=_torch_dtype(self.precision),
+                 device=self.device)
+        return DeviceField(t, self.nx, self.ny, self.nz)
+
+    def device_flags(self):
+        """The flag bytes the kernel tests, read back dense, for bit-exact
+        geometry checks."""
+        out = np.empty(self.nx * self.ny * self.nz, dtype=np.uint8)
+        _cabi.check(self._lib.mlb_plan_get_flags(self._plan, _host_ptr(out)))
+        return out
+
+    def set_physics(self, omega=None, wall_u=None, inlet_u=None):
+        if omega is not None:
+            self.omega = float(omega)
+        if wall_u is not None:
+            self.wall_u = tuple(float(v) for v in wall_u) + (0.0,) * (3 - len(wall_u))
+        if inlet_u is not None:
+            self.inlet_u = float(inlet_u)
+        uw = (ctypes.c_double * 3)(*self.wall_u)
+        _cabi.check(self._lib.mlb_plan_set_physics(self._plan, self.omega, uw,
+                                                   self.inlet_u))
+
+    def set_block_width(self, width):
+        _cabi.check(self._lib.mlb_plan_set_variant(self._plan, int(width)))
+
+    # -- host <-> device ---------------------------------------------------
+    def _check_host(self, a):
+        n = self.nx * self.ny * self.nz
+        if not (isinstance(a, np.ndarray) and a.shape == (Q, n)
+                and a.dtype == self.precision.storage and a.flags.c_contiguous):
+            raise ValueError(
+                f"host population block must be a C-contiguous ({Q}, {n}) "
+                f"{self.precision.storage} array")
+
+    def upload(self, host, dev):
+        self._check_host(host)
+        _cabi.check(self._lib.mlb_upload(self._plan, _host_ptr(host), dev.ptr,
+                                         _stream_ptr(self.device)))
+
+    def download(self, dev, host, sync=True):
+        self._check_host(host)
+        _cabi.check(self._lib.mlb_download(self._plan, dev.ptr, _host_ptr(host),
+                                           _stream_ptr(self.device)))
+        if sync:
+            torch.cuda.current_stream(self.device).synchronize()
+
+    # -- the hot path ------------------------------------------------------
+    def step(self, fpre, fpost):
+        """Advance one step: read fpre, write every fluid cell of fpost."""
+        if isinstance(fpre, DeviceField):
+            _cabi.check(self._lib.mlb_step(self._plan, fpre.ptr, fpost.ptr,
+                                           _stream_ptr(self.device)))
+            return
+        self._check_host(fpre)
+        self._check_host(fpost)
+        if self._scratch is None:
+            self._scratch = (self.alloc(), self.alloc())
+        a, b = self._scratch
+        _cabi.check(self._lib.mlb_step_host(self._plan, _host_ptr(fpre),
+                                            _host_ptr(fpost), a.ptr, b.ptr,
+                                            _stream_ptr(self.device)))
+
+    def step_range(self, fpre, fpost, z0, z1):
+        _cabi.check(self._lib.mlb_step_range(self._plan, fpre.ptr, fpost.ptr,
+                                             int(z0), int(z1),
+                                             _stream_ptr(self.device)))
+
+    def open_pass(self, fpost):
+        _cabi.check(self._lib.mlb_open_pass(self._plan, fpost.ptr,
+                                            _stream_ptr(self.device)))
+
+    def open_pass_range(self, fpost, z0, z1):
+        _cabi.check(self._lib.mlb_open_pass_range(self._plan, fpost.ptr, int(z0),
+                                                  int(z1), _stream_ptr(self.device)))
+
+    def run_steps(self, a, b, nsteps, timed=False):
+        """`nsteps` x (fused update, open-boundary pass, swap) on the device.
+
+        Returns (newest, other, ms): the block holding the newest
+        populations, the other one, and - when `timed` - the device time of
+        the loop in milliseconds from CUDA events on the launching stream
+        (the call then synchronises)."""
+        ms = ctypes.c_float(0.0)
+        _cabi.check(self._lib.mlb_run_steps(
+            self._plan, a.ptr, b.ptr, int(nsteps), _stream_ptr(self.device),
+            ctypes.byref(ms) if timed else None))
+        newest, other = (a, b) if nsteps % 2 == 0 else (b, a)
+        return newest, other, (ms.value if timed else None)
+
+    def halo_copy(self, dst, src, face):
+        """Fill one halo plane of `dst` from the matching boundary plane of
+        `src` (5 crossing populations), on this device or a peer."""
+        _cabi.check(self._lib.mlb_halo_copy(self._plan, dst.ptr, src.ptr,
+                                            int(src.nz), int(face),
+                                            _stream_ptr(self.device)))
+
+    # -- diagnostics -------------------------------------------------------
+    def macro(self, dev):
+        """rho, ux, uy, uz as float64 CUDA tensors of shape (nz, ny, nx)."""
+        out = [torch.empty((self.nz, self.ny, self.nx), dtype=torch.float64,
+                           device=self.device) for _ in range(4)]
+        _cabi.check(self._lib.mlb_macro(
+            self._plan, dev.ptr, *[ctypes.c_void_p(o.data_ptr()) for o in out],
+            _stream_ptr(self.device)))
+        return tuple(out)
+
+    def diagnostics(self, dev):
+        out = (ctypes.c_double * 8)()
+        _cabi.check(self._lib.mlb_diagnostics(self._plan, dev.ptr, out,
+                                              _stream_ptr(self.device)))
+        keys = ("mass", "px", "py", "pz", "kinetic_energy", "max_u",
+                "nonfinite", "fluid_cells")
+        return dict(zip(keys, list(out)))
+
+    def probe(self, dev, x, y, z, out4):
+        """Enqueue a (rho, ux, uy, uz) sample of one cell into a 4-double
+        CUDA tensor (no host round trip)."""
+        _cabi.check(self._lib.mlb_probe(self._plan, dev.ptr, int(x), int(y), int(z),
+                                        ctypes.c_void_p(out4.data_ptr()),
+                                        _stream_ptr(self.device)))
+
+
+def _torch_dtype(precision):
+    return torch.float32 if precision is Precision.SINGLE else torch.float64
+
+
+def pinned_empty(shape, dtype):
+    """A numpy array backed by page-locked host memory when CUDA is present
+    (so uploads/downloads are real asynchronous DMA), plain otherwise."""
+    dtype = np.dtype(dtype)
+    if torch.cuda.is_available():
+        tdt = {np.dtype(np.float32): torch.float32,
+               np.dtype(np.float64): torch.float64,
+               np.dtype(np.uint8): torch.uint8}[dtype]
+        return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+    return np.empty(shape, dtype=dtype)

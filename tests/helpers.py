@@ -1,0 +1,72 @@
+"""Shared test helpers: geometries, random fields, the z-projection bridge."""
+
+import numpy as np
+
+from paper_2409_16781_b200 import boundaries as B
+from paper_2409_16781_b200 import lattice as L
+
+
+def geometries3d():
+    """3-D counterparts of the reference's kernel-test geometries
+    (pkg/tests/test_kernels.py:25-33), small and ragged on purpose (no
+    extent is a multiple of the 128-byte line)."""
+    cavity = B.cavity_mask(9, 7, 5)
+    cavity[4, 3, 2] = B.SOLID  # interior obstacle
+    channel = B.channel_mask(14, 9, 8, B.sphere_cells(14, 9, 8, 4, 5.0, 4.0, 3.5))
+    duct = B.channel_mask(12, 8, 6, B.cylinder_cells(12, 8, 6, 4, 4.0, 3.5),
+                          z_walls=False)
+    periodic = B.open_mask(6, 5, 4)
+    return {"cavity": (cavity, (0.08, 0.0, 0.0), 0.0),
+            "cavity_oblique_lid": (cavity, (0.05, 0.0, -0.03), 0.0),
+            "channel": (channel, (0.0, 0.0, 0.0), 0.07),
+            "duct": (duct, (0.0, 0.0, 0.0), 0.05),
+            "periodic": (periodic, (0.0, 0.0, 0.0), 0.0)}
+
+
+def random_block(rng, n, dtype):
+    """Populations ~ U(0.02, 1) as the reference's tests draw them
+    (test_kernels.py:19-22)."""
+    return np.ascontiguousarray(
+        rng.uniform(0.02, 1.0, size=(19, n)).astype(dtype))
+
+
+def lift_2d(f2, nz):
+    """Lift a D2Q9 block (9, ny*nx) to a z-symmetric, z-invariant D3Q19
+    block (19, nz*ny*nx) whose sum over c_z is f2 exactly: each 2-D
+    population is split over its c_z group in proportion to the lattice
+    weights (dyadic fractions, so the split is exact in floating point)."""
+    n2 = f2.shape[1]
+    f3 = np.zeros((19, nz, n2), dtype=f2.dtype)
+    for k in range(9):
+        grp = L.PROJECT_2D[k]
+        wsum = L.W[grp].sum()
+        for i in grp:
+            f3[i] = (f2.dtype.type(L.W[i] / wsum) * f2[k])[None, :]
+    return np.ascontiguousarray(f3.reshape(19, nz * n2))
+
+
+def project_2d(f3, nz):
+    """Sum a D3Q19 block over c_z: (nz, 9, ny*nx) float64."""
+    f3 = np.asarray(f3, dtype=np.float64).reshape(19, nz, -1)
+    out = np.zeros((nz, 9, f3.shape[2]))
+    for k in range(9):
+        for i in L.PROJECT_2D[k]:
+            out[:, k] += f3[i]
+    return out
+
+
+def extrude_mask(mask2_flat, nx, ny, nz):
+    """(ny*nx,) ROW-ordered 2-D flags -> dense [nz][ny][nx] flags."""
+    m = np.asarray(mask2_flat, dtype=np.uint8).reshape(ny, nx)
+    return np.ascontiguousarray(np.broadcast_to(m[None], (nz, ny, nx))).reshape(-1)
+
+
+def to_xyzq(block, nx, ny, nz):
+    """(19, N) block -> (nx, ny, nz, 19) float64 array for the naive oracle."""
+    return np.ascontiguousarray(
+        np.asarray(block, dtype=np.float64).reshape(19, nz, ny, nx).transpose(3, 2, 1, 0))
+
+
+def from_xyzq(a):
+    nx, ny, nz, _ = a.shape
+    return np.ascontiguousarray(a.transpose(3, 2, 1, 0).reshape(19, nz * ny * nx))

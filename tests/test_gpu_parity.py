@@ -1,0 +1,181 @@
+"""GPU parity: the CUDA path, called through the C ABI, against the CPU
+oracle on identical inputs.  The bar for populations and macroscopic fields
+is BIT-EXACT (stronger than the 1e-12 / 1e-5 relative tolerance the
+north star allows): both sides perform the same IEEE operations in the
+same order, neither contracts multiplies and adds."""
+
+import numpy as np
+import pytest
+
+from oracle.cpu import CpuOracle
+from oracle.ref3d import ref3d_open_pass, ref3d_step
+from paper_2409_16781_b200 import boundaries as B
+from paper_2409_16781_b200.fields import Layout, Precision
+
+from .helpers import (extrude_mask, from_xyzq, geometries3d, lift_2d,
+                      project_2d, random_block, to_xyzq)
+
+pytestmark = pytest.mark.gpu
+
+PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE}
+
+
+def make_plan(grid, prec, omega, wall_u, inlet_u=0.0, **kw):
+    from paper_2409_16781_b200.kernels import KernelPlan
+    nx, ny, nz = grid.shape
+    return KernelPlan(nx, ny, nz, Layout.ROW, prec, B.flatten_mask(grid), omega,
+                      wall_u, inlet_u=inlet_u, **kw)
+
+
+def make_oracle(grid, omega, wall_u, inlet_u=0.0):
+    nx, ny, nz = grid.shape
+    return CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u, inlet_u)
+
+
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+@pytest.mark.parametrize("geom", list(geometries3d()))
+def test_one_step_bitwise(geom, tag, rng):
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    prec = PREC[tag]
+    n = grid.size
+    f = random_block(rng, n, prec.storage)
+    post0 = random_block(rng, n, prec.storage)  # never-written cells must survive
+    omega = 1.41
+    want = post0.copy()
+    make_oracle(grid, omega, wall_u, inlet_u).step(f, want)
+    got = post0.copy()
+    make_plan(grid, prec, omega, wall_u, inlet_u).step(f, got)  # host-block call
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("geom", ["cavity", "channel", "periodic"])
+def test_one_step_matches_naive_oracle(geom, rng):
+    # the independent explicit-loop oracle, the reference's own tolerance
+    # for this check (test_kernels.py:61)
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    nx, ny, nz = grid.shape
+    f = random_block(rng, grid.size, np.float64)
+    got = f.copy()
+    make_plan(grid, Precision.DOUBLE, 1.41, wall_u, inlet_u).step(f, got)
+    want = ref3d_step(to_xyzq(f, nx, ny, nz), grid, 1.41, wall_u)
+    np.testing.assert_allclose(to_xyzq(got, nx, ny, nz), want, rtol=1e-13, atol=1e-16)
+
+
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+@pytest.mark.parametrize("geom", list(geometries3d()))
+def test_multi_step_with_open_pass_bitwise(geom, tag, rng):
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    prec = PREC[tag]
+    f = random_block(rng, grid.size, prec.storage)
+    omega, steps = 0.9, 7
+    a, b = f.copy(), f.copy()
+    want = make_oracle(grid, omega, wall_u, inlet_u).run(a, b, steps)
+    plan = make_plan(grid, prec, omega, wall_u, inlet_u)
+    da, db = plan.alloc(), plan.alloc()
+    plan.upload(f, da)
+    plan.upload(f, db)
+    newest, _, _ = plan.run_steps(da, db, steps)
+    got = np.empty_like(f)
+    plan.download(newest, got)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_never_writes_non_fluid_cells(rng):
+    # test_kernels.py:205-219
+    grid, wall_u, inlet_u = geometries3d()["channel"]
+    f = random_block(rng, grid.size, np.float64)
+    post = np.full_like(f, -7.5)
+    make_plan(grid, Precision.DOUBLE, 1.3, wall_u, inlet_u).step(f, post)
+    non_fluid = B.flatten_mask(grid) != B.FLUID
+    assert (post[:, non_fluid] == -7.5).all()
+    assert not (post[:, ~non_fluid] == -7.5).any()
+
+
+def test_pure_streaming_at_omega_zero(rng):
+    # omega = 0 turns the step into the pull permutation (test_kernels.py:152-164)
+    from paper_2409_16781_b200.lattice import C
+    nx, ny, nz = 6, 5, 7
+    grid = B.open_mask(nx, ny, nz)
+    f = random_block(rng, grid.size, np.float64)
+    got = f.copy()
+    make_plan(grid, Precision.DOUBLE, 0.0, (0, 0, 0)).step(f, got)
+    fx, gx = to_xyzq(f, nx, ny, nz), to_xyzq(got, nx, ny, nz)
+    for i in range(19):
+        want = np.roll(fx[..., i], tuple(C[i]), axis=(0, 1, 2))
+        np.testing.assert_array_equal(gx[..., i], want)
+
+
+def test_flags_byte_identical(rng):
+    for geom, (grid, wall_u, inlet_u) in geometries3d().items():
+        plan = make_plan(grid, Precision.SINGLE, 1.0, wall_u, inlet_u)
+        np.testing.assert_array_equal(plan.device_flags(), B.flatten_mask(grid))
+
+
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+def test_macro_bitwise_and_diagnostics(tag, rng):
+    grid, wall_u, inlet_u = geometries3d()["channel"]
+    prec = PREC[tag]
+    nx, ny, nz = grid.shape
+    f = random_block(rng, grid.size, prec.storage)
+    orc = make_oracle(grid, 1.0, wall_u, inlet_u)
+    plan = make_plan(grid, prec, 1.0, wall_u, inlet_u)
+    d = plan.alloc()
+    plan.upload(f, d)
+    got = [t.cpu().numpy().transpose(2, 1, 0) for t in plan.macro(d)]
+    for g, w in zip(got, orc.macro(f)):
+        np.testing.assert_array_equal(g, w)
+    gd, wd = plan.diagnostics(d), orc.diagnostics(f)
+    for key in wd:
+        assert gd[key] == pytest.approx(wd[key], rel=1e-12, abs=1e-12), key
+    assert gd["fluid_cells"] == np.count_nonzero(grid == 0)
+    f[3, 17] = np.nan
+    f[11, 5] = np.inf
+    plan.upload(f, d)
+    assert plan.diagnostics(d)["nonfinite"] == 2
+
+
+def test_ldc64_fp64_100_steps_bitwise():
+    """BASELINE.json config 1: D3Q19 BGK lid-driven cavity 64^3, 100 steps,
+    fp64, through the reference-shaped API (cases.init + engine.run)."""
+    from paper_2409_16781_b200 import cases, engine
+    spec = cases.CaseSpec("ldc", 64, 64, 64, re=100.0, u0=0.1)
+    state = cases.init(spec, Precision.DOUBLE)
+    f0 = state.f_pre.data.copy()
+    stats = engine.run(state, engine.RunConfig(steps=100, precision=Precision.DOUBLE))
+    assert state.t == 100 and stats.mlups > 0
+    orc = CpuOracle(64, 64, 64, state.mask, state.params.omega, state.wall_u,
+                    threads=8)
+    want = orc.run(f0.copy(), f0.copy(), 100)
+    np.testing.assert_array_equal(state.f_pre.data, want)
+    rho, ux, uy, uz = state.macro()
+    for g, w in zip((rho, ux, uy, uz), orc.macro(want)):
+        np.testing.assert_array_equal(g, w)
+    assert ux.max() > 1e-3  # the lid drags the fluid along +x
+
+
+@pytest.mark.parametrize("case,tag,tol", [("ldc24", "f64", 1e-13), ("tgv16", "f64", 1e-13),
+                                          ("vks48", "f64", 1e-13), ("ldc24", "f32", 1e-5)])
+def test_z_projection_bridge_to_lb2d(case, tag, tol, golden):
+    """The CUDA path against the REAL reference: a z-invariant, z-periodic
+    D3Q19 run summed over c_z equals the lb2d D2Q9 run (golden vectors from
+    tests/golden/make_golden.py)."""
+    p = f"{case}_{tag}_"
+    nx, ny, steps = int(golden[p + "nx"]), int(golden[p + "ny"]), int(golden[p + "steps"])
+    nz = 4
+    prec = PREC[tag]
+    from paper_2409_16781_b200.kernels import KernelPlan
+    wu = golden[p + "wall_u"]
+    plan = KernelPlan(nx, ny, nz, Layout.ROW, prec, extrude_mask(golden[p + "mask"], nx, ny, nz),
+                      float(golden[p + "omega"]), (wu[0], wu[1], 0.0),
+                      inlet_u=float(golden[p + "inlet_u"]))
+    f0 = lift_2d(golden[p + "f0"], nz)
+    da, db = plan.alloc(), plan.alloc()
+    plan.upload(f0, da)
+    plan.upload(f0, db)
+    newest, _, _ = plan.run_steps(da, db, steps)
+    got = np.empty_like(f0)
+    plan.download(newest, got)
+    want = golden[p + "f"].astype(np.float64)
+    proj = project_2d(got, nz)
+    scale = np.abs(want).max()
+    assert np.abs(proj - want[None]).max() / scale <= tol
