@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""bench.py - MLUPS of the D3Q19 BGK time-step loop on N B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Workload (BASELINE.json configs[2], the one the metric is quoted on):
+D3Q19 BGK lid-driven cavity, 512^3 cells per GPU, fp32, Re 1000, u0 0.1.
+With N > 1 (launched under torch.distributed.run, one rank per GPU) the
+cavity is 512 x 512 x (512 N), split into N z-slabs with 5-population halo
+exchange over NCCL - per-GPU work is fixed, i.e. weak scaling.
+
+One "step" is one lattice time step: the fused pull-stream + BGK collide
+kernel over all cells (plus the open-boundary pass, a no-op for the cavity,
+and the halo exchange when N > 1).  MLUPS counts ALL cells, solid included,
+like the reference (lb2d perfport.py:55-61, engine.py:270-271).
+
+The one JSON line carries
+  value      device-timed whole-job MLUPS, populations resident in HBM;
+             CUDA events on the launching stream, max over ranks;
+  e2e        the same K steps through the public host API
+             (`engine.run` on a host-resident state in pinned memory):
+             H2D of the populations + flags, K steps, D2H of the result,
+             all inside the timed region;
+  roofline   the fused kernel against the measured HBM bandwidth
+             (MEASURED_PEAKS.json): algorithmic bytes 2 x 19 x 4 B per
+             update (lb2d perfport.py:40-45 with Q = 19);
+  cpu_baseline  the CPU oracle (a port of the reference's algorithm,
+             OpenMP, all host cores) on a bounded sample of the workload.
+
+`--impl reference` times that CPU port alone, on the same config, each step
+a bounded z-slice of the cavity so the run ends within a few minutes.  The
+oracle is used here as the measured CPU arm only; it is never on the GPU
+path.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NX = NY = NZ_PER_GPU = 512
+RE, U0 = 1000.0, 0.1
+METRIC = "MLUPS (D3Q19 BGK)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="override the edge length (debug)")
+    ap.add_argument("--precision", default="single", choices=["single", "double"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--width", type=int, default=0, help="thread-block width (tuning)")
+    return ap.parse_args()
+
+
+def workload_config(n, nz_global, world, prec, omega):
+    size = f"{n}^3" if world == 1 else f"{n}x{n}x{nz_global}"
+    return {
+        "workload": f"D3Q19 BGK lid-driven cavity {size} {'fp32' if prec == 'single' else 'fp64'}"
+                    f" (BASELINE.json configs[2]{', z-slab weak scaling' if world > 1 else ''})",
+        "nx": n, "ny": n, "nz_per_gpu": n, "nz_global": nz_global,
+        "re": RE, "u0": U0, "omega": omega,
+        "decomposition": f"{world} z-slab(s), 5-population halos over NCCL" if world > 1 else "single GPU",
+        "l2_policy": "inputs exceed L2: two population blocks of "
+                     f"{19 * n ** 3 * (4 if prec == 'single' else 8) / 1e9:.1f} GB per GPU vs 126 MB L2",
+    }
+
+
+# --------------------------------------------------------------------------
+# clocks: sample nvidia-smi during the timed region (B200_PROFILING.md)
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 7:
+                continue
+            try:
+                sm.append(float(r[0])); mx.append(float(r[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+def slab_mask(n, rank, world):
+    """This rank's [x, y, z] flag block of the 512 x 512 x (512 world) cavity."""
+    import numpy as np
+    from paper_2409_16781_b200 import boundaries as B
+    m = B.cavity_mask(n, n, n, z_walls=False)
+    if rank == 0:
+        m[:, :, 0] = B.SOLID
+    if rank == world - 1:
+        m[:, :, -1] = B.SOLID
+    return np.ascontiguousarray(m)
+
+
+def cpu_arm(n, prec, steps, warmup, budget_s):
+    """Time the CPU port of the reference algorithm (the oracle, OpenMP over
+    all host cores) on a bounded z-slice of the cavity."""
+    import numpy as np
+    from oracle.cpu import CpuOracle
+    from paper_2409_16781_b200 import boundaries as B
+    from paper_2409_16781_b200.lattice import W, omega_from_reynolds
+    cores = os.cpu_count() or 1
+    dtype = np.float32 if prec == "single" else np.float64
+    omega = omega_from_reynolds(RE, U0, n).omega
+
+    def make(nz):
+        mask = B.flatten_mask(B.cavity_mask(n, n, nz))
+        f = np.empty((19, n * n * nz), dtype=dtype)
+        for q in range(19):
+            f[q].fill(W[q])
+        return CpuOracle(n, n, nz, mask, omega, (U0, 0.0, 0.0), threads=cores), f, f.copy()
+
+    # calibrate on a thin slice, then size the sample to the time budget
+    orc, a, b = make(8)
+    orc.step(a, b)
+    t0 = time.perf_counter(); orc.step(b, a); dt = time.perf_counter() - t0
+    rate = n * n * 8 / dt
+    nz = int(rate * budget_s / ((steps + warmup) * n * n))
+    nz = max(8, min(n, nz))
+    orc, a, b = make(nz)
+    for _ in range(warmup):
+        orc.step(a, b); a, b = b, a
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        orc.step(a, b); a, b = b, a
+    dt = time.perf_counter() - t0
+    mlups = n * n * nz * steps / dt / 1e6
+    return {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": "port",
+            "sample": f"{n}x{n}x{nz} z-slice of the cavity, {steps} steps after {warmup} warm-up, "
+                      f"{'fp32' if prec == 'single' else 'fp64'}, C/OpenMP port of the reference "
+                      f"algorithm (oracle/d3q19_oracle.c), {cores} threads"}, dt / steps * 1e3
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    n = args.n or NX
+    prec_tok = args.precision
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        from paper_2409_16781_b200.lattice import omega_from_reynolds
+        omega = omega_from_reynolds(RE, U0, n).omega
+        base, ms = cpu_arm(n, prec_tok, args.steps, args.warmup, budget_s=90.0)
+        line = {
+            "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "MLUPS",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if prec_tok == "single" else "f64", "data": "synthetic",
+            "config": workload_config(n, n * max(1, args.gpus), max(1, args.gpus), prec_tok, omega),
+            "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": "MLUPS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "gpu_launches": 0,
+        }
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2409_16781_b200 import _cabi, boundaries as B, cases, engine, slab
+    from paper_2409_16781_b200.fields import Layout, Precision
+    from paper_2409_16781_b200.kernels import KernelPlan, pinned_empty
+    from paper_2409_16781_b200.lattice import W, omega_from_reynolds
+
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torch.distributed.run "
+                             "(one rank per GPU)")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    prec = Precision.from_token(prec_tok)
+    itemsize = prec.storage.itemsize
+    nz_global = n * world
+    params = omega_from_reynolds(RE, U0, n)
+    cells_rank = n * n * n
+    cells_all = cells_rank * world
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- host state (pinned) and the plan ----------------------------------
+    if world == 1:
+        spec = cases.CaseSpec("ldc", n, n, n, re=RE, u0=U0)
+        state = cases.init(spec, prec)
+        mask_flat = state.mask
+        plan = KernelPlan(n, n, n, Layout.ROW, prec, mask_flat, params.omega,
+                          (U0, 0.0, 0.0), device=local)
+        host = state.f_pre.data
+    else:
+        m = slab_mask(n, rank, world)
+        mask_flat = B.flatten_mask(m)
+        lo, hi = slab.exchange_flag_halos(mask_flat.reshape(n, n, n), rank, world,
+                                          device=device)
+        plan = KernelPlan(n, n, n, Layout.ROW, prec, mask_flat, params.omega,
+                          (U0, 0.0, 0.0), device=local, halo_lo=lo, halo_hi=hi, slab=True)
+        host = pinned_empty((19, cells_rank), prec.storage)
+        for q in range(19):
+            host[q].fill(W[q])
+    if args.width:
+        plan.set_block_width(args.width)
+    a, b = plan.alloc(), plan.alloc()
+    plan.upload(host, a)
+    b.tensor.copy_(a.tensor)
+    runner = None
+    if world > 1:
+        runner = slab.DistSlab(slab.CudaStepper(plan), n, rank, world)
+        for r in runner.exchange(a):
+            r.wait()
+
+    def advance(x, y, k):
+        if runner is None:
+            newest, other, _ = plan.run_steps(x, y, k)
+            return newest, other
+        return runner.run(x, y, k)
+
+    # ---- device-timed run: W warm-up, then exactly K steps -------------------
+    a, b = advance(a, b, args.warmup)
+    barrier()
+    launches0 = _cabi.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        a, b = advance(a, b, args.steps)
+        e1.record()
+        barrier()
+    launches = _cabi.launch_count() - launches0
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+    nl = torch.tensor([launches], dtype=torch.int64, device=device)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(nl, op=dist.ReduceOp.SUM)
+    ms = float(ms.item())
+    value = cells_all * args.steps / (ms * 1e-3) / 1e6
+    diag = plan.diagnostics(a)
+    if diag["nonfinite"]:
+        raise SystemExit("bench: populations diverged")
+
+    # ---- end to end through the host API ------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        h2d = 19 * cells_rank * itemsize + cells_rank      # populations + flags
+        d2h = 19 * cells_rank * itemsize
+        del a, b
+        plan.close()
+        torch.cuda.empty_cache()
+        if world == 1:
+            cfg = engine.RunConfig(steps=args.steps, precision=prec, device=local)
+            warm = engine.RunConfig(steps=max(1, args.warmup), precision=prec, device=local)
+            engine.run(state, warm)              # allocator / page-lock warm-up, untimed
+            barrier()
+            t0 = time.perf_counter()
+            engine.run(state, cfg)               # H2D + K steps + D2H
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+        else:
+            def e2e_once(k):
+                p = KernelPlan(n, n, n, Layout.ROW, prec, mask_flat, params.omega,
+                               (U0, 0.0, 0.0), device=local, halo_lo=lo, halo_hi=hi, slab=True)
+                x, y = p.alloc(), p.alloc()
+                p.upload(host, x)
+                y.tensor.copy_(x.tensor)
+                rr = slab.DistSlab(slab.CudaStepper(p), n, rank, world)
+                for r in rr.exchange(x):
+                    r.wait()
+                x, y = rr.run(x, y, k)
+                p.download(x, host)
+                p.close()
+            e2e_once(max(1, args.warmup))
+            barrier()
+            t0 = time.perf_counter()
+            e2e_once(args.steps)
+            barrier()
+            dt = time.perf_counter() - t0
+        dtt = torch.tensor([dt], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(dtt, op=dist.ReduceOp.MAX)
+        dt = float(dtt.item())
+        e2e = {"value": cells_all * args.steps / dt / 1e6, "unit": "MLUPS",
+               "h2d_bytes_per_step": h2d * world / args.steps,
+               "d2h_bytes_per_step": d2h * world / args.steps,
+               "seconds": dt,
+               "call": "engine.run(host state, RunConfig(steps=K)): upload, K steps, download"
+                       if world == 1 else
+                       "per rank: KernelPlan + upload, DistSlab.run(K), download"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the fused kernel ---------------------------------------
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        peak, peak_src = json.load(open(peaks_path))["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs)"
+    else:
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    bytes_per_update = 2 * 19 * itemsize
+    kernel_ms = ms / args.steps           # one fused-kernel launch per step per GPU
+    achieved = bytes_per_update * cells_rank / (kernel_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        key = f"step_kernel_{'f32' if prec_tok == 'single' else 'f64'}_{n}"
+        traffic = json.load(open(tpath)).get(key)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "kernel": "mlb::step_kernel", "algorithmic_bytes_per_update": bytes_per_update,
+                "updates_per_launch": cells_rank, "kernel_ms": kernel_ms}
+
+    cpu_base = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu_base, _ = cpu_arm(n, prec_tok, steps=10, warmup=2, budget_s=15.0)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if prec_tok == "single" else "f64", "data": "synthetic",
+        "config": workload_config(n, nz_global, world, prec_tok, params.omega),
+        "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(nl.item()),
+        "roofline": roofline, "cpu_baseline": cpu_base,
+        "check": {"mass": diag["mass"], "max_u": diag["max_u"], "nonfinite": diag["nonfinite"]},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

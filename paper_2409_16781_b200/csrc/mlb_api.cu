@@ -377,25 +377,34 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
             p->in_zoff[sz - 1] = (long long)in_idx.size();
             p->out_zoff[sz - 1] = (long long)out_idx.size();
         }
-        for (int y = 0; y < ny; ++y)
+        for (int y = 0; y < ny; ++y) {
+            const uint8_t *row = src + (size_t)y * nx;
+            const long long d0 = (long long)sz * plane + (long long)y * xp;
+            std::memcpy(&pad[d0], row, (size_t)nx);
+            // rows of plain fluid/solid/lid cells (all but a few) need no
+            // per-cell work: one vectorisable scan finds the exceptions
+            uint8_t special = 0;
+            for (int x = 0; x < nx; ++x)
+                special |= (uint8_t)(row[x] >= 3);
+            if (!special)
+                continue;
             for (int x = 0; x < nx; ++x) {
-                const uint8_t m = src[(size_t)y * nx + x];
+                const uint8_t m = row[x];
                 if (m > 4)
                     return fail(MLB_EINVAL, "flag array holds unknown cell code %d at "
                                 "(x=%d, y=%d, plane=%d)", (int)m, x, y, sz - 1);
-                const long long d = (long long)sz * plane + (long long)y * xp + x;
-                pad[d] = m;
                 if (!interior)
                     continue;
                 if (m == 3)
-                    in_idx.push_back(d);
+                    in_idx.push_back(d0 + x);
                 else if (m == 4) {
                     if (x == 0)
                         return fail(MLB_EUNSUPPORTED, "outlet cell at x = 0 (y=%d, z=%d): "
                                     "its source would be the previous row's last cell", y, sz - 1);
-                    out_idx.push_back(d);
+                    out_idx.push_back(d0 + x);
                 }
             }
+        }
     }
     p->in_zoff[nz] = (long long)in_idx.size();
     p->out_zoff[nz] = (long long)out_idx.size();

@@ -58,7 +58,7 @@ def test_one_step_matches_naive_oracle(geom, rng):
     got = f.copy()
     make_plan(grid, Precision.DOUBLE, 1.41, wall_u, inlet_u).step(f, got)
     want = ref3d_step(to_xyzq(f, nx, ny, nz), grid, 1.41, wall_u)
-    np.testing.assert_allclose(to_xyzq(got, nx, ny, nz), want, rtol=1e-13, atol=1e-16)
+    np.testing.assert_allclose(to_xyzq(got, nx, ny, nz), want, rtol=1e-12, atol=1e-15)
 
 
 @pytest.mark.parametrize("tag", ["f64", "f32"])

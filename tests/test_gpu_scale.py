@@ -1,0 +1,136 @@
+"""BASELINE.json configs at their full sizes, through size-independent
+properties (the oracle cannot run 512^3 in seconds) plus bounded bit-exact
+windows against the oracle where it can."""
+
+import numpy as np
+import pytest
+
+from oracle.cpu import CpuOracle
+from paper_2409_16781_b200 import boundaries as B
+from paper_2409_16781_b200 import lattice as L
+from paper_2409_16781_b200.fields import Layout, Precision
+
+pytestmark = pytest.mark.gpu
+
+
+def test_tgv256_decay_rate_and_oracle_window():
+    """configs[1]: periodic Taylor-Green vortex 256^3 (the reference's exact
+    2-D field extruded in z).  (a) 12 steps bit-exact against the CPU oracle
+    in fp64 and fp32; (b) the fp64 decay rate of max|u| over 1000 steps
+    within 5 % of the analytic 2 nu k^2 and the velocity field within 2 % L2
+    of the exact solution - the reference's acceptance c03 (test_acceptance.py:81-105)."""
+    import torch
+    from paper_2409_16781_b200 import cases, engine
+    n, nz = 256, 256
+    for prec in (Precision.DOUBLE, Precision.SINGLE):
+        spec = cases.CaseSpec("tgv", n, n, nz, u0=0.04, omega=1.25)
+        state = cases.init(spec, prec)
+        f0 = state.f_pre.data.copy()
+        engine.run(state, engine.RunConfig(steps=12, precision=prec))
+        want = CpuOracle(n, n, nz, state.mask, 1.25, threads=16).run(f0.copy(), f0.copy(), 12)
+        np.testing.assert_array_equal(state.f_pre.data, want)
+        del want, f0
+    spec = cases.CaseSpec("tgv", n, n, nz, u0=0.04, omega=1.25)
+    state = cases.init(spec, Precision.DOUBLE)
+    nu = state.params.nu
+    sess = engine.open_session(state)
+    ts, amps = [], []
+    for _ in range(10):
+        sess.advance(100)
+        ts.append(state.t)
+        amps.append(sess.plan.diagnostics(sess.pre)["max_u"])
+    slope = np.polyfit(ts, np.log(amps), 1)[0]
+    want = -cases.tgv_decay_rate(n, nu)
+    assert abs(slope - want) <= 0.05 * abs(want)
+    rho, ux, uy, uz = state.macro()
+    _, rx, ry, rz = cases.tgv_fields(n, 0.04, nu, state.t, nz)
+    assert cases.l2_velocity_error((ux, uy), (rx, ry)) <= 0.02
+    assert np.abs(uz).max() <= 1e-14
+    sess.close(sync=False)
+    torch.cuda.empty_cache()
+
+
+def test_ldc512_fp32_properties():
+    """configs[2] at full size: determinism (two runs, same bits), mass
+    conservation in the closed box, never-written walls, finite fields, and
+    2 z-slabs == 1 domain bitwise."""
+    import torch
+    from paper_2409_16781_b200 import slab
+    from paper_2409_16781_b200.kernels import KernelPlan
+    from paper_2409_16781_b200.lattice import omega_from_reynolds
+    n, steps = 512, 20
+    omega = omega_from_reynolds(1000.0, 0.1, n).omega
+    grid = B.cavity_mask(n, n, n)
+    flags = B.flatten_mask(grid)
+    plan = KernelPlan(n, n, n, Layout.ROW, Precision.SINGLE, flags, omega, (0.1, 0.0, 0.0))
+    np.testing.assert_array_equal(plan.device_flags(), flags)
+
+    def fresh():
+        a, b = plan.alloc(), plan.alloc()
+        for q in range(19):
+            a.tensor[q].fill_(float(np.float32(L.W[q])))
+        b.tensor.copy_(a.tensor)
+        return a, b
+
+    a, b = fresh()
+    d0 = plan.diagnostics(a)
+    assert d0["fluid_cells"] == (n - 2) ** 3 and d0["nonfinite"] == 0
+    res, other, _ = plan.run_steps(a, b, steps)
+    d1 = plan.diagnostics(res)
+    assert d1["nonfinite"] == 0
+    assert abs(d1["mass"] - d0["mass"]) <= 2e-6 * d0["mass"]   # fp32 storage, 20 steps
+    assert 0.0 < d1["max_u"] < 0.2 and d1["px"] > 0.0          # the lid drags fluid along +x
+    # walls never written: every solid cell still holds the rest weights
+    wall = res.tensor[:, 1:-1, 0, :n]
+    assert all(bool((wall[q] == float(np.float32(L.W[q]))).all()) for q in range(19))
+    ref = res.tensor.clone()
+    del a, b, res, other
+    a, b = fresh()
+    res2, _, _ = plan.run_steps(a, b, steps)
+    assert torch.equal(res2.tensor[:, 1:-1], ref[:, 1:-1])     # bitwise reproducible
+    del a, b, res2
+    plan.close()
+    torch.cuda.empty_cache()
+
+    # two z-slabs of 256 planes, halo exchange through mlb_halo_copy
+    f3 = flags.reshape(n, n, n)
+    slabs = []
+    for (z0, z1) in slab.partition(n, 2):
+        lo, hi = slab.slab_halo_flags(f3, n, n, z0, z1)
+        p = KernelPlan(n, n, z1 - z0, Layout.ROW, Precision.SINGLE, f3[z0:z1], omega,
+                       (0.1, 0.0, 0.0), halo_lo=lo, halo_hi=hi, slab=True)
+        blocks = [p.alloc(), p.alloc()]
+        for blk in blocks:
+            for q in range(19):
+                blk.tensor[q].fill_(float(np.float32(L.W[q])))
+        slabs.append((p, blocks))
+    pre, post = 0, 1
+    for _ in range(steps):
+        for p, blocks in slabs:
+            p.step_range(blocks[pre], blocks[post], 0, p.nz)
+        for r, (p, blocks) in enumerate(slabs):
+            p.halo_copy(blocks[post], slabs[r - 1][1][post], face=0)
+            p.halo_copy(blocks[post], slabs[(r + 1) % 2][1][post], face=1)
+        pre, post = post, pre
+    assert torch.equal(slabs[0][1][pre].tensor[:, 1:-1], ref[:, 1:257])
+    assert torch.equal(slabs[1][1][pre].tensor[:, 1:-1], ref[:, 257:513])
+
+
+def test_omega_zero_roll_256_periodic():
+    """omega = 0 is the pure pull permutation (test_kernels.py:152-164) at a
+    size where every thread-block shape and wrap lane is exercised."""
+    import torch
+    from paper_2409_16781_b200.kernels import KernelPlan
+    nx, ny, nz = 256, 96, 40
+    plan = KernelPlan(nx, ny, nz, Layout.ROW, Precision.SINGLE,
+                      B.flatten_mask(B.open_mask(nx, ny, nz)), 0.0)
+    a, b = plan.alloc(), plan.alloc()
+    g = torch.Generator(device="cuda").manual_seed(20240917)
+    a.tensor.uniform_(0.02, 1.0, generator=g)
+    b.tensor.zero_()
+    plan.step(a, b)
+    for q in range(19):
+        src = a.tensor[q, 1:-1]
+        want = torch.roll(src, shifts=(int(L.C[q][2]), int(L.C[q][1]), int(L.C[q][0])),
+                          dims=(0, 1, 2))
+        assert torch.equal(b.tensor[q, 1:-1], want), q

@@ -1,0 +1,111 @@
+"""z-slab decomposition on the GPU: P logical slabs on ONE device (each
+with its own plan, halo planes and halo flags, exchanging the 5 crossing
+populations through mlb_halo_copy) must reproduce the single-domain run bit
+for bit; so must the DistSlab driver with its boundary-first / interior
+stream overlap."""
+
+import numpy as np
+import pytest
+
+from oracle.cpu import CpuOracle
+from paper_2409_16781_b200 import boundaries as B
+from paper_2409_16781_b200.fields import Layout, Precision
+
+from .helpers import geometries3d, random_block
+
+pytestmark = pytest.mark.gpu
+
+
+def single_domain(grid, prec, omega, wall_u, inlet_u, f, steps):
+    from paper_2409_16781_b200.kernels import KernelPlan
+    nx, ny, nz = grid.shape
+    plan = KernelPlan(nx, ny, nz, Layout.ROW, prec, B.flatten_mask(grid), omega, wall_u,
+                      inlet_u=inlet_u)
+    a, b = plan.alloc(), plan.alloc()
+    plan.upload(f, a)
+    plan.upload(f, b)
+    newest, _, _ = plan.run_steps(a, b, steps)
+    out = np.empty_like(f)
+    plan.download(newest, out)
+    return out
+
+
+def make_slabs(grid, prec, omega, wall_u, inlet_u, f, parts):
+    from paper_2409_16781_b200 import slab
+    from paper_2409_16781_b200.kernels import KernelPlan
+    nx, ny, nz = grid.shape
+    flags = B.flatten_mask(grid).reshape(nz, ny, nx)
+    dense = f.reshape(19, nz, ny, nx)
+    slabs = []
+    for (z0, z1) in slab.partition(nz, parts):
+        lo, hi = slab.slab_halo_flags(flags, nx, ny, z0, z1)
+        plan = KernelPlan(nx, ny, z1 - z0, Layout.ROW, prec, flags[z0:z1], omega, wall_u,
+                          inlet_u=inlet_u, halo_lo=lo, halo_hi=hi, slab=True)
+        blocks = [plan.alloc(), plan.alloc()]
+        part = np.ascontiguousarray(dense[:, z0:z1]).reshape(19, -1)
+        for blk in blocks:
+            blk.tensor.fill_(float("nan"))
+            plan.upload(part, blk)
+        slabs.append((plan, blocks, z0, z1))
+    return slabs
+
+
+def gather(slabs, which, like):
+    parts = []
+    for plan, blocks, z0, z1 in slabs:
+        out = np.empty((19, (z1 - z0) * plan.ny * plan.nx), dtype=like.dtype)
+        plan.download(blocks[which], out)
+        parts.append(out.reshape(19, z1 - z0, plan.ny, plan.nx))
+    return np.concatenate(parts, axis=1).reshape(19, -1)
+
+
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+@pytest.mark.parametrize("parts", [1, 2, 3])
+@pytest.mark.parametrize("geom", ["cavity_oblique_lid", "channel", "periodic"])
+def test_logical_slabs_equal_single_domain_bitwise(geom, parts, tag, rng):
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    prec = Precision.DOUBLE if tag == "f64" else Precision.SINGLE
+    f = random_block(rng, grid.size, prec.storage)
+    steps, omega = 5, 1.2
+    want = single_domain(grid, prec, omega, wall_u, inlet_u, f, steps)
+    slabs = make_slabs(grid, prec, omega, wall_u, inlet_u, f, parts)
+
+    def exchange(which):
+        for r, (plan, blocks, _, _) in enumerate(slabs):
+            below = slabs[(r - 1) % parts]
+            above = slabs[(r + 1) % parts]
+            plan.halo_copy(blocks[which], below[1][which], face=0)
+            plan.halo_copy(blocks[which], above[1][which], face=1)
+
+    exchange(0)
+    pre, post = 0, 1
+    for _ in range(steps):
+        for plan, blocks, z0, z1 in slabs:
+            plan.step_range(blocks[pre], blocks[post], 0, z1 - z0)
+            plan.open_pass_range(blocks[post], 0, z1 - z0)
+        exchange(post)
+        pre, post = post, pre
+    np.testing.assert_array_equal(gather(slabs, pre, f), want)
+    # and against the CPU oracle
+    nx, ny, nz = grid.shape
+    orc = CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u, inlet_u)
+    np.testing.assert_array_equal(want, orc.run(f.copy(), f.copy(), steps))
+
+
+@pytest.mark.parametrize("geom", ["cavity_oblique_lid", "channel", "periodic"])
+def test_distslab_overlap_path_single_rank(geom, rng):
+    """DistSlab on CUDA with world = 1: boundary planes on the high-priority
+    stream, interior on the main stream, ring closed on the slab itself."""
+    from paper_2409_16781_b200 import slab
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    f = random_block(rng, grid.size, np.float32)
+    steps, omega = 6, 1.5
+    want = single_domain(grid, Precision.SINGLE, omega, wall_u, inlet_u, f, steps)
+    (plan, blocks, z0, z1), = make_slabs(grid, Precision.SINGLE, omega, wall_u, inlet_u, f, 1)
+    runner = slab.DistSlab(slab.CudaStepper(plan), z1 - z0)
+    assert runner.overlap
+    runner.exchange(blocks[0])
+    newest, _ = runner.run(blocks[0], blocks[1], steps)
+    out = np.empty_like(f)
+    plan.download(newest, out)
+    np.testing.assert_array_equal(out, want)

@@ -1,0 +1,103 @@
+"""The N > 1 path on CPU: two processes, `gloo`, the real DistSlab driver
+(partition, flag-halo exchange at setup, per-step 5-population exchange,
+ring order) with the CPU oracle as the stepper.  The gathered result must be
+BITWISE the single-domain run - the reference's partition-independence
+property (test_kernels.py:107-126) carried to z-slabs."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle.cpu import CpuOracle, SlabOracle
+from paper_2409_16781_b200 import boundaries as B
+from paper_2409_16781_b200 import slab
+
+from .helpers import geometries3d, random_block
+
+
+class OracleStepper:
+    """CPU stand-in for slab.CudaStepper: same interface, oracle compute."""
+
+    def __init__(self, orc):
+        self.orc = orc
+
+    def tensor(self, block):
+        return torch.from_numpy(block)  # shares memory with the numpy block
+
+    def step_range(self, pre, post, z0, z1):
+        self.orc.step_range(pre, post, z0, z1)
+        self.orc.open_pass_range(post, z0, z1)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, geom, steps, omega, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        grid, wall_u, inlet_u = geometries3d()[geom]
+        nx, ny, nz = grid.shape
+        flags = B.flatten_mask(grid).reshape(nz, ny, nx)
+        f = random_block(np.random.default_rng(20240917), grid.size, np.float64)
+        z0, z1 = slab.partition(nz, world)[rank]
+        n = z1 - z0
+        xp = nx + 2
+        lo, hi = slab.exchange_flag_halos(flags[z0:z1], rank, world)
+        want_lo, want_hi = slab.slab_halo_flags(flags, nx, ny, z0, z1)
+        assert (lo == want_lo).all() and (hi == want_hi).all()
+        fl = np.ones((n + 2, ny, xp), dtype=np.uint8)
+        fl[1:-1, :, :nx], fl[0, :, :nx], fl[-1, :, :nx] = flags[z0:z1], lo, hi
+        blocks = []
+        for _ in range(2):
+            blk = np.full((19, n + 2, ny, xp), np.nan)
+            blk[:, 1:-1, :, :nx] = f.reshape(19, nz, ny, nx)[:, z0:z1]
+            blocks.append(blk)
+        runner = slab.DistSlab(OracleStepper(SlabOracle(nx, ny, n, xp, fl, omega, wall_u, inlet_u)),
+                               n, rank, world)
+        for r in runner.exchange(blocks[0]):
+            r.wait()
+        newest, _ = runner.run(blocks[0], blocks[1], steps)
+        np.save(os.path.join(out_dir, f"slab{rank}.npy"), newest[:, 1:-1, :, :nx])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("geom", ["cavity_oblique_lid", "channel", "periodic"])
+def test_two_rank_gloo_run_equals_single_domain(geom, tmp_path):
+    world, steps, omega = 2, 5, 1.3
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    nx, ny, nz = grid.shape
+    f = random_block(np.random.default_rng(20240917), grid.size, np.float64)
+    want = CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u, inlet_u).run(
+        f.copy(), f.copy(), steps)
+    mp.spawn(_worker, args=(world, _free_port(), geom, steps, omega, str(tmp_path)),
+             nprocs=world, join=True)
+    got = np.concatenate([np.load(tmp_path / f"slab{r}.npy") for r in range(world)], axis=1)
+    np.testing.assert_array_equal(got.reshape(19, -1), want)
+
+
+def test_single_rank_ring_closes_on_itself():
+    grid, wall_u, inlet_u = geometries3d()["periodic"]
+    nx, ny, nz = grid.shape
+    flags = B.flatten_mask(grid).reshape(nz, ny, nx)
+    f = random_block(np.random.default_rng(3), grid.size, np.float64)
+    want = CpuOracle(nx, ny, nz, flags, 1.1).run(f.copy(), f.copy(), 3)
+    lo, hi = slab.exchange_flag_halos(flags, 0, 1)
+    fl = np.ones((nz + 2, ny, nx), dtype=np.uint8)
+    fl[1:-1], fl[0], fl[-1] = flags, lo, hi
+    blocks = [np.full((19, nz + 2, ny, nx), np.nan) for _ in range(2)]
+    for blk in blocks:
+        blk[:, 1:-1] = f.reshape(19, nz, ny, nx)
+    runner = slab.DistSlab(OracleStepper(SlabOracle(nx, ny, nz, nx, fl, 1.1)), nz)
+    runner.exchange(blocks[0])
+    newest, _ = runner.run(blocks[0], blocks[1], 3)
+    np.testing.assert_array_equal(newest[:, 1:-1].reshape(19, -1), want)
