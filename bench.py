@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--precision", default="single", choices=["single", "double"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--width", type=int, default=0, help="thread-block width (tuning)")
+    ap.add_argument("--variant", type=int, default=0, help="kernel variant (tuning; see mlb_plan_set_variant)")
     return ap.parse_args()
 
 
@@ -257,8 +257,8 @@ def main():
         host = pinned_empty((19, cells_rank), prec.storage)
         for q in range(19):
             host[q].fill(W[q])
-    if args.width:
-        plan.set_block_width(args.width)
+    if args.variant:
+        plan.set_variant(args.variant)
     a, b = plan.alloc(), plan.alloc()
     plan.upload(host, a)
     b.tensor.copy_(a.tensor)

@@ -54,6 +54,7 @@ struct mlb_plan {
     bool have_flags = false;
     uint8_t *d_flags = nullptr;  // padded flag block incl. halo planes
     uint8_t *d_cls = nullptr;    // class table, same shape
+    unsigned long long *d_links = nullptr;  // per-cell bounce/moving link masks, same shape
     // open-boundary index lists, sorted by (lz, y, x); *_zoff[lz] = first entry of plane lz
     long long n_in = 0, n_out = 0;
     long long *d_in = nullptr, *d_out = nullptr;
@@ -162,7 +163,29 @@ int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1,
     a.z0 = z0;
     a.omega = T(p->omega);
     wall_terms<T>(p->wall_u, a.k);
-    int bx = p->variant > 0 ? p->variant : 128;
+    // variant: 0 = auto, 32..512 = scalar kernel with that block width,
+    // 1008 / 1016 / 1032 = vectorised kernel with 8 / 16 / 32 packs per warp row
+    constexpr int V = mlb::Vec<T>::V;
+    int variant = p->variant;
+    if (variant == 0)
+        variant = (p->nx % V == 0 && p->nx >= 8 * V) ? 1008 : 128;
+    if (variant >= 1000) {
+        if (p->nx % V != 0)
+            return fail(MLB_EINVAL, "the vectorised kernel needs nx %% %d == 0", V);
+        const int lx = variant - 1000;
+        const int rows = 128 / lx;  // rows per 128-thread block
+        const dim3 grid((p->nx / V + lx - 1) / lx, (p->ny + rows - 1) / rows, z1 - z0);
+        switch (lx) {
+        case 8: mlb::step_vec_kernel<T, 8><<<grid, 128, 0, st>>>(a, p->d_links); break;
+        case 16: mlb::step_vec_kernel<T, 16><<<grid, 128, 0, st>>>(a, p->d_links); break;
+        case 32: mlb::step_vec_kernel<T, 32><<<grid, 128, 0, st>>>(a, p->d_links); break;
+        default: return fail(MLB_EINVAL, "variant %d: packs per warp row must be 8, 16 or 32",
+                             p->variant);
+        }
+        MLB_LAUNCHED();
+        return MLB_OK;
+    }
+    int bx = variant;
     while (bx > 32 && bx / 2 >= p->nx)
         bx /= 2;
     const dim3 grid((p->nx + bx - 1) / bx, p->ny, z1 - z0);
@@ -310,8 +333,8 @@ int mlb_plan_destroy(mlb_plan *p)
     if (!p)
         return MLB_OK;
     cudaSetDevice(p->device);
-    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_in); cudaFree(p->d_out);
-    cudaFree(p->d_out_tmp); cudaFree(p->d_partials); cudaFree(p->d_diag);
+    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_links); cudaFree(p->d_in);
+    cudaFree(p->d_out); cudaFree(p->d_out_tmp); cudaFree(p->d_partials); cudaFree(p->d_diag);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
     delete p;
@@ -342,9 +365,10 @@ int mlb_plan_set_physics(mlb_plan *p, double omega, const double wall_u[3], doub
 int mlb_plan_set_variant(mlb_plan *p, int variant)
 {
     if (int rc = check_plan(p, false)) return rc;
-    if (variant != 0 && variant != 32 && variant != 64 && variant != 128
-        && variant != 256 && variant != 512)
-        return fail(MLB_EINVAL, "variant must be 0 or a block width in {32..512}");
+    if (variant != 0 && variant != 32 && variant != 64 && variant != 128 && variant != 256
+        && variant != 512 && variant != 1008 && variant != 1016 && variant != 1032)
+        return fail(MLB_EINVAL, "variant must be 0 (auto), a scalar block width in "
+                    "{32,64,128,256,512}, or 1008/1016/1032 (vectorised kernel)");
     p->variant = variant;
     return MLB_OK;
 }
@@ -417,12 +441,14 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
             break;
         }
 
-    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_in); cudaFree(p->d_out);
-    cudaFree(p->d_out_tmp);
-    p->d_flags = p->d_cls = nullptr; p->d_in = p->d_out = nullptr; p->d_out_tmp = nullptr;
+    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_links); cudaFree(p->d_in);
+    cudaFree(p->d_out); cudaFree(p->d_out_tmp);
+    p->d_flags = p->d_cls = nullptr; p->d_links = nullptr; p->d_in = p->d_out = nullptr;
+    p->d_out_tmp = nullptr;
     p->have_flags = false;
     MLB_CUDA(cudaMalloc(&p->d_flags, padded));
     MLB_CUDA(cudaMalloc(&p->d_cls, padded));
+    MLB_CUDA(cudaMalloc(&p->d_links, padded * sizeof(unsigned long long)));
     MLB_CUDA(cudaMemcpy(p->d_flags, pad.data(), padded, cudaMemcpyHostToDevice));
     p->n_in = (long long)in_idx.size();
     p->n_out = (long long)out_idx.size();
@@ -439,7 +465,7 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
             MLB_CUDA(cudaMalloc(&p->d_out_tmp, (size_t)p->lay.itemsize * MLB_Q * p->n_out));
     }
     const dim3 grid((unsigned)((xp + 127) / 128), ny, nz + 2);
-    mlb::build_cls_kernel<<<grid, 128>>>(p->d_flags, p->d_cls, p->g);
+    mlb::build_cls_kernel<<<grid, 128>>>(p->d_flags, p->d_cls, p->d_links, p->g);
     MLB_LAUNCHED();
     MLB_CUDA(cudaDeviceSynchronize());
     p->have_flags = true;

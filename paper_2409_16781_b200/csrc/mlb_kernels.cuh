@@ -186,10 +186,212 @@ __global__ void __launch_bounds__(BX) step_kernel(const StepArgs<T> a)
 }
 
 // ---------------------------------------------------------------------------
-// Class table from the padded flag block (halo planes already filled).
-// One thread per padded element of storage planes [0, nz+2).
+// Vectorised fused update: each thread owns a PACK of V = 16 / sizeof(T)
+// consecutive cells in x (one 16-byte word per population), a warp covers
+// LX packs in x by 32 / LX rows in y.  Per pack and population: one aligned
+// 16-byte load; the ten populations with c_x = +-1 need the word shifted by
+// one cell, which costs one extra scalar load of the element just outside
+// the pack (an L1 hit: the neighbouring lane's word holds it).  Stores are
+// aligned 16-byte words (pull scheme: destinations are never shifted).
+//
+// Walls stay branch-free: a warp whose packs are all bulk fluid takes the
+// plain path; any other warp takes the "general" path as a whole, where a
+// lane with wall links also loads its own cell's opposite populations and
+// selects per cell and direction with the precomputed link masks
+// (kernels.py:88-96: SOLID source -> own opposite population, MOVING_WALL
+// source -> that plus the wall term).  No flag reads, no divergence.
+template <typename T> struct Vec;
+template <> struct Vec<float>  { using type = float4;  static constexpr int V = 4; };
+template <> struct Vec<double> { using type = double2; static constexpr int V = 2; };
+
+template <typename T>
+__device__ __forceinline__ void unpack(const typename Vec<T>::type &v, T (&o)[Vec<T>::V]);
+template <>
+__device__ __forceinline__ void unpack<float>(const float4 &v, float (&o)[4])
+{ o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+template <>
+__device__ __forceinline__ void unpack<double>(const double2 &v, double (&o)[2])
+{ o[0] = v.x; o[1] = v.y; }
+
+__device__ __forceinline__ float4 pack(const float (&o)[4]) { return make_float4(o[0], o[1], o[2], o[3]); }
+__device__ __forceinline__ double2 pack(const double (&o)[2]) { return make_double2(o[0], o[1]); }
+
+// The V values pulled along a direction with x component CX from the row
+// starting at `row` (already offset to population, plane and row).
+template <typename T, int CX>
+__device__ __forceinline__ void pull_pack(const T *__restrict__ row, int x0, int xl, int xr,
+                                          T (&o)[Vec<T>::V])
+{
+    constexpr int V = Vec<T>::V;
+    using VT = typename Vec<T>::type;
+    T w[V];
+    unpack<T>(*reinterpret_cast<const VT *>(row + x0), w);
+    if (CX == 0) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) o[j] = w[j];
+    } else if (CX > 0) {  // source x - 1
+        o[0] = row[xl];
+#pragma unroll
+        for (int j = 1; j < V; ++j) o[j] = w[j - 1];
+    } else {              // source x + 1
+#pragma unroll
+        for (int j = 0; j < V - 1; ++j) o[j] = w[j + 1];
+        o[V - 1] = row[xr];
+    }
+}
+
+// direction table: X(i, c_x, plane offset, row offset)
+#define MLB_DIRS(X)                                                              \
+    X(1, 1, zc, rc)   X(2, 0, zc, rm)   X(3, -1, zc, rc)  X(4, 0, zc, rq)        \
+    X(5, 1, zc, rm)   X(6, -1, zc, rm)  X(7, -1, zc, rq)  X(8, 1, zc, rq)        \
+    X(9, 0, zm, rc)   X(10, 0, zq, rc)  X(11, 1, zm, rc)  X(12, -1, zm, rc)      \
+    X(13, -1, zq, rc) X(14, 1, zq, rc)  X(15, 0, zm, rm)  X(16, 0, zm, rq)       \
+    X(17, 0, zq, rq)  X(18, 0, zq, rm)
+
+template <typename T, int LX>
+__global__ void __launch_bounds__(128)
+step_vec_kernel(const StepArgs<T> a, const unsigned long long *__restrict__ links)
+{
+    constexpr int V = Vec<T>::V;
+    using VT = typename Vec<T>::type;
+    constexpr int RPW = 32 / LX;        // rows per warp
+    constexpr unsigned FULL = 0xffffffffu;
+    const Geom &gm = a.g;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int x0 = (blockIdx.x * LX + (lane % LX)) * V;
+    const int y = blockIdx.y * (4 * RPW) + warp * RPW + lane / LX;
+    const int lz = a.z0 + blockIdx.z;
+    const bool inrange = (x0 < gm.nx) && (y < gm.ny);
+
+    const long long zc = (long long)(lz + 1) * gm.plane;
+    const long long zm = (long long)((lz == 0) ? gm.zlo_src : lz) * gm.plane;
+    const long long zq = (long long)((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) * gm.plane;
+    const int yy = inrange ? y : 0;
+    const int ym = (yy == 0) ? gm.ny - 1 : yy - 1;
+    const int yq = (yy == gm.ny - 1) ? 0 : yy + 1;
+    const long long rc = (long long)yy * gm.xp, rm = (long long)ym * gm.xp,
+                    rq = (long long)yq * gm.xp;
+    const int xx = inrange ? x0 : 0;
+    const int xl = (xx == 0) ? gm.nx - 1 : xx - 1;
+    const int xr = (xx + V >= gm.nx) ? 0 : xx + V;
+    const long long d = zc + rc + xx;
+
+    // class bytes of the pack, one 16/32-bit word
+    unsigned c4;
+    if (V == 4)
+        c4 = *reinterpret_cast<const unsigned *>(a.cls + d);
+    else
+        c4 = *reinterpret_cast<const unsigned short *>(a.cls + d);
+    if (!inrange)
+        c4 = (V == 4) ? 0x01010101u : 0x0101u;  // nothing to do here
+    bool fluid[V];
+    bool anyfluid = false, allfluid = true;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        fluid[j] = ((c4 >> (8 * j)) & CLS_FLAG) == 0;
+        anyfluid |= fluid[j];
+        allfluid &= fluid[j];
+    }
+    const bool bulk = (c4 == 0);
+    const bool general = !__all_sync(FULL, bulk || !anyfluid);  // warp-uniform
+    if (!anyfluid)
+        return;
+
+    const T *__restrict__ f = a.fpre;
+    const long long P = gm.pop;
+    T g[Q][V];
+    unpack<T>(*reinterpret_cast<const VT *>(f + d), g[0]);
+
+    if (!general) {
+#define MLB_X(i, CX, Z, R) pull_pack<T, CX>(f + (long long)(i) * P + (Z) + (R), xx, xl, xr, g[i]);
+        MLB_DIRS(MLB_X)
+#undef MLB_X
+    } else {
+        // link masks of the pack (zero for bulk cells; garbage-free for
+        // non-fluid ones, which are never stored)
+        unsigned lo[V], hi[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) { lo[j] = 0u; hi[j] = 0u; }
+        if (!bulk) {
+#pragma unroll
+            for (int j = 0; j < V; j += 2) {
+                const ulonglong2 m = *reinterpret_cast<const ulonglong2 *>(links + d + j);
+                lo[j] = (unsigned)m.x;     hi[j] = (unsigned)(m.x >> 32);
+                lo[j + 1] = (unsigned)m.y; hi[j + 1] = (unsigned)(m.y >> 32);
+            }
+        }
+        unsigned anylo = 0u;
+#pragma unroll
+        for (int j = 0; j < V; ++j) anylo |= lo[j];
+#define MLB_X(i, CX, Z, R)                                                        \
+        {                                                                         \
+            pull_pack<T, CX>(f + (long long)(i) * P + (Z) + (R), xx, xl, xr, g[i]); \
+            if (anylo & (1u << (i))) {                                            \
+                T c_[V];                                                          \
+                unpack<T>(*reinterpret_cast<const VT *>(f + (long long)opp(i) * P + d), c_); \
+                _Pragma("unroll")                                                 \
+                for (int j = 0; j < V; ++j) {                                     \
+                    if (lo[j] & (1u << (i)))                                      \
+                        g[i][j] = (hi[j] & (1u << (i))) ? c_[j] + a.k[i] : c_[j]; \
+                }                                                                 \
+            }                                                                     \
+        }
+        MLB_DIRS(MLB_X)
+#undef MLB_X
+    }
+
+    // collide each cell of the pack (lattice.collide_cell order)
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        T gc[Q];
+#pragma unroll
+        for (int i = 0; i < Q; ++i) gc[i] = g[i][j];
+        collide<T>(gc, a.omega);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) g[i][j] = gc[i];
+    }
+
+    T *__restrict__ o = a.fpost + d;
+    if (allfluid) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+            *reinterpret_cast<VT *>(o + (long long)i * P) = pack(g[i]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            if (fluid[j]) {
+#pragma unroll
+                for (int i = 0; i < Q; ++i)
+                    o[(long long)i * P + j] = g[i][j];
+            }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Class table and link masks from the padded flag block (halo planes already
+// filled).  One thread per padded element of storage planes [0, nz+2).
+//   links[d] bit i      (1 <= i <= 18): the source cell of direction i is a
+//                        wall (SOLID or MOVING_WALL) -> bounce-back link
+//   links[d] bit 32 + i: that wall is a MOVING_WALL -> add the wall term k_i
+// Direction i's source is the neighbour at -c_i, with the same periodic
+// wrap / halo-plane rule as the step kernels.
+__device__ __forceinline__ constexpr int dir_index(int cx, int cy, int cz)
+{
+    // inverse of the velocity table in lattice.py; -1 for the 8 corners / rest
+    if (cz == 0) {
+        if (cy == 0) return cx == 1 ? 1 : cx == -1 ? 3 : 0;
+        if (cx == 0) return cy == 1 ? 2 : 4;
+        return cy == 1 ? (cx == 1 ? 5 : 6) : (cx == -1 ? 7 : 8);
+    }
+    if (cx == 0 && cy == 0) return cz == 1 ? 9 : 10;
+    if (cy == 0) return cz == 1 ? (cx == 1 ? 11 : 12) : (cx == -1 ? 13 : 14);
+    if (cx == 0) return cz == 1 ? (cy == 1 ? 15 : 16) : (cy == -1 ? 17 : 18);
+    return -1;
+}
+
 __global__ void build_cls_kernel(const uint8_t *__restrict__ flags,
-                                 uint8_t *__restrict__ cls, const Geom gm)
+                                 uint8_t *__restrict__ cls,
+                                 unsigned long long *__restrict__ links, const Geom gm)
 {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= gm.xp)
@@ -199,32 +401,40 @@ __global__ void build_cls_kernel(const uint8_t *__restrict__ flags,
     const long long d = (long long)sz * gm.plane + (long long)y * gm.xp + x;
     if (x >= gm.nx) {
         cls[d] = 1;  // row padding: solid, never written
+        links[d] = 0ull;
         return;
     }
     const uint8_t fl = flags[d];
     if (sz == 0 || sz == gm.nz + 1) {
         cls[d] = fl;  // halo planes are only ever sources
+        links[d] = 0ull;
         return;
     }
     const int lz = sz - 1;
+    // index 0: same, 1: the "minus" neighbour (source for c = +1), 2: the "plus" one
     const int xs[3] = {x, (x == 0) ? gm.nx - 1 : x - 1, (x == gm.nx - 1) ? 0 : x + 1};
     const int ys[3] = {y, (y == 0) ? gm.ny - 1 : y - 1, (y == gm.ny - 1) ? 0 : y + 1};
     const int zs[3] = {sz, (lz == 0) ? gm.zlo_src : lz, (lz == gm.nz - 1) ? gm.zhi_src : lz + 2};
-    bool wall = false;
+    const int cof[3] = {0, 1, -1};  // the c component served by index 0/1/2
+    unsigned long long lk = 0ull;
 #pragma unroll
     for (int dz = 0; dz < 3; ++dz)
 #pragma unroll
         for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
             for (int dx = 0; dx < 3; ++dx) {
-                const int nnz = (dx != 0) + (dy != 0) + (dz != 0);
-                if (nnz == 0 || nnz == 3)
-                    continue;  // D3Q19 has no corner links
+                const int i = dir_index(cof[dx], cof[dy], cof[dz]);
+                if (i <= 0)
+                    continue;  // rest particle / the 8 corners: no D3Q19 link
                 const uint8_t m = flags[(long long)zs[dz] * gm.plane
                                         + (long long)ys[dy] * gm.xp + xs[dx]];
-                wall |= (m == 1) || (m == 2);
+                if (m == 1 || m == 2)
+                    lk |= 1ull << i;
+                if (m == 2)
+                    lk |= 1ull << (32 + i);
             }
-    cls[d] = fl | (wall ? CLS_NEAR_WALL : 0);
+    cls[d] = fl | (lk ? CLS_NEAR_WALL : 0);
+    links[d] = (fl == 0) ? lk : 0ull;
 }
 
 // ---------------------------------------------------------------------------

@@ -92,7 +92,8 @@ class KernelPlan:
         if self.backend != "cuda":
             raise ValueError(f"unknown backend '{self.backend}'")
         self.sx, self.sy, self.sz = layout.strides(self.nx, self.ny, self.nz)
-        if tile is None:
+        auto_tile = tile is None
+        if auto_tile:
             tile = (min(self.nx, 128), 1, 1)  # one contiguous line segment per block
         tile = tuple(int(t) for t in tile) + (1,) * (3 - len(tile))
         tx, ty, tz = tile
@@ -125,9 +126,13 @@ class KernelPlan:
             _cabi.MLB_Z_HALO if self.slab else _cabi.MLB_Z_PERIODIC))
         self._layout = _cabi.Layout()
         _cabi.check(lib.mlb_plan_get_layout(self._plan, ctypes.byref(self._layout)))
-        # block width: the largest supported width not above the tile's x extent
-        width = max([w for w in _BLOCK_WIDTHS if w <= max(tx, 32)])
-        _cabi.check(lib.mlb_plan_set_variant(self._plan, width))
+        # schedule 'auto' lets the library pick (the vectorised kernel when
+        # the row length allows, see mlb_plan_set_variant); an explicit tile
+        # selects the one-cell-per-thread kernel with the largest supported
+        # block width not above the tile's x extent.  Never changes bits.
+        if not auto_tile:
+            width = max([w for w in _BLOCK_WIDTHS if w <= max(tx, 32)])
+            _cabi.check(lib.mlb_plan_set_variant(self._plan, width))
 
         def plane(h):
             if h is None:
@@ -191,8 +196,13 @@ class KernelPlan:
         _cabi.check(self._lib.mlb_plan_set_physics(self._plan, self.omega, uw,
                                                    self.inlet_u))
 
-    def set_block_width(self, width):
-        _cabi.check(self._lib.mlb_plan_set_variant(self._plan, int(width)))
+    def set_variant(self, variant):
+        """Kernel variant (tuning knob, never changes bits): 0 = auto,
+        32..512 = one cell per thread with that block width, 1008 / 1016 /
+        1032 = vectorised kernel with 8 / 16 / 32 packs per warp row."""
+        _cabi.check(self._lib.mlb_plan_set_variant(self._plan, int(variant)))
+
+    set_block_width = set_variant
 
     # -- host <-> device ---------------------------------------------------
     def _check_host(self, a):

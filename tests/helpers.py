@@ -16,7 +16,21 @@ def geometries3d():
     duct = B.channel_mask(12, 8, 6, B.cylinder_cells(12, 8, 6, 4, 4.0, 3.5),
                           z_walls=False)
     periodic = B.open_mask(6, 5, 4)
+    # row lengths that are multiples of the 16-byte pack: these exercise the
+    # vectorised kernel (several packs per row, walls inside and between packs)
+    cavity16 = B.cavity_mask(16, 9, 7)
+    cavity16[5:8, 3:5, 2:4] = B.SOLID
+    cavity16[11, 6, 4] = B.SOLID
+    channel40 = B.channel_mask(40, 10, 6, B.sphere_cells(40, 10, 6, 4, 9.0, 4.5, 2.5))
+    periodic8 = B.open_mask(8, 5, 4)
+    periodic8[3, 2, 1] = B.SOLID
+    periodic8[4, 2, 1] = B.MOVING_WALL
+    wide = B.open_mask(72, 4, 3)
     return {"cavity": (cavity, (0.08, 0.0, 0.0), 0.0),
+            "cavity16": (cavity16, (0.05, 0.0, -0.03), 0.0),
+            "channel40": (channel40, (0.0, 0.0, 0.0), 0.06),
+            "periodic8": (periodic8, (0.02, 0.03, -0.04), 0.0),
+            "wide": (wide, (0.0, 0.0, 0.0), 0.0),
             "cavity_oblique_lid": (cavity, (0.05, 0.0, -0.03), 0.0),
             "channel": (channel, (0.0, 0.0, 0.0), 0.07),
             "duct": (duct, (0.0, 0.0, 0.0), 0.05),

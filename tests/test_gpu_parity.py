@@ -80,6 +80,43 @@ def test_multi_step_with_open_pass_bitwise(geom, tag, rng):
     np.testing.assert_array_equal(got, want)
 
 
+VEC_GEOMS = ["cavity16", "channel40", "periodic8", "wide", "duct"]
+
+
+@pytest.mark.parametrize("variant", [64, 128, 1008, 1016, 1032])
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+@pytest.mark.parametrize("geom", VEC_GEOMS)
+def test_kernel_variants_never_change_bits(geom, tag, variant, rng):
+    """Block shape / vectorisation are pure performance knobs
+    (test_kernels.py:107-126): every variant, same bits as the oracle."""
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    prec = PREC[tag]
+    f = random_block(rng, grid.size, prec.storage)
+    sentinel = random_block(rng, grid.size, prec.storage)
+    omega, steps = 1.6, 3
+    a, b = f.copy(), sentinel.copy()
+    orc = make_oracle(grid, omega, wall_u, inlet_u)
+    want = orc.run(a, b, steps)
+    plan = make_plan(grid, prec, omega, wall_u, inlet_u)
+    plan.set_variant(variant)
+    da, db = plan.alloc(), plan.alloc()
+    plan.upload(f, da)
+    plan.upload(sentinel, db)
+    newest, _, _ = plan.run_steps(da, db, steps)
+    got = np.empty_like(f)
+    plan.download(newest, got)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_vector_kernel_rejects_ragged_rows():
+    grid, wall_u, inlet_u = geometries3d()["cavity"]  # nx = 9
+    plan = make_plan(grid, Precision.SINGLE, 1.0, wall_u)
+    plan.set_variant(1008)
+    a, b = plan.alloc(), plan.alloc()
+    with pytest.raises(ValueError, match="nx"):
+        plan.step(a, b)
+
+
 def test_never_writes_non_fluid_cells(rng):
     # test_kernels.py:205-219
     grid, wall_u, inlet_u = geometries3d()["channel"]

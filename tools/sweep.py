@@ -10,7 +10,7 @@ def run(n, prec, width, steps=30, omega=1.7):
     nx = ny = nz = n
     mask = B.flatten_mask(B.cavity_mask(nx, ny, nz))
     plan = KernelPlan(nx, ny, nz, Layout.ROW, prec, mask, omega, (0.1, 0, 0))
-    plan.set_block_width(width)
+    plan.set_variant(width)
     a, b = plan.alloc(), plan.alloc()
     from paper_2409_16781_b200.lattice import W
     for q in range(19):
@@ -29,5 +29,5 @@ if __name__ == "__main__":
     sizes = [int(s) for s in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["256", "512"])]
     for n in sizes:
         for prec in (Precision.SINGLE, Precision.DOUBLE):
-            for width in (64, 128, 256, 512):
+            for width in (128, 1008, 1016, 1032):
                 run(n, prec, width)
