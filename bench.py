@@ -262,6 +262,7 @@ def main():
     a, b = plan.alloc(), plan.alloc()
     plan.upload(host, a)
     b.tensor.copy_(a.tensor)
+    plan.set_passthrough(True)   # both blocks identical: what engine.Session establishes
     runner = None
     if world > 1:
         runner = slab.DistSlab(slab.CudaStepper(plan), n, rank, world)
@@ -320,6 +321,7 @@ def main():
                 x, y = p.alloc(), p.alloc()
                 p.upload(host, x)
                 y.tensor.copy_(x.tensor)
+                p.set_passthrough(True)
                 rr = slab.DistSlab(slab.CudaStepper(p), n, rank, world)
                 for r in rr.exchange(x):
                     r.wait()

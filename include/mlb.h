@@ -74,8 +74,18 @@ int mlb_plan_destroy(mlb_plan *plan);
 int mlb_plan_get_layout(const mlb_plan *plan, mlb_layout *out);
 int mlb_plan_set_physics(mlb_plan *plan, double omega, const double wall_u[3],
                          double inlet_u);
-/* kernel variant used by mlb_step (0 = default); for tuning/benchmarks */
+/* kernel variant used by mlb_step (tuning knob, never changes bits): 0 =
+ * default, 32..512 = one cell per thread with that block width, 1008 / 1016 /
+ * 1032 = 16-byte packs with 8 / 16 / 32 packs per warp row */
 int mlb_plan_set_variant(mlb_plan *plan, int variant);
+/* Pass-through stores (default off = the reference's contract, non-fluid
+ * cells of fpost are never written).  When on, mlb_step also stores every
+ * non-fluid cell, with the value it holds in d_fpre.  The caller asserts
+ * that d_fpre and d_fpost agree on non-fluid cells - true for any pair of
+ * buffers that started identical (engine.py:148) - so memory ends up
+ * byte-identical to the strict mode, while every warp store is a full
+ * 128-byte line instead of leaving partial sectors at each wall. */
+int mlb_plan_set_passthrough(mlb_plan *plan, int on);
 
 /* Flags: the reference's `mask` argument (kernels.py:408, a (N,) uint8 array
  * in cell order).  h_flags is dense [nz][ny][nx] HOST memory.  h_halo_lo /

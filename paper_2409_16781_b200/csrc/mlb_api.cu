@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -48,13 +49,14 @@ inline cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
 
 struct mlb_plan {
     int nx = 0, ny = 0, nz = 0, dtype = 0, device = 0, z_mode = 0, variant = 0;
+    int passthrough = 0;
     double omega = 1.0, wall_u[3] = {0, 0, 0}, inlet_u = 0.0;
     mlb_layout lay{};
     mlb::Geom g{};
     bool have_flags = false;
     uint8_t *d_flags = nullptr;  // padded flag block incl. halo planes
-    uint8_t *d_cls = nullptr;    // class table, same shape
-    unsigned long long *d_links = nullptr;  // per-cell bounce/moving link masks, same shape
+    uint32_t *d_cls = nullptr;     // per-cell class words, same shape
+    uint32_t *d_mlinks = nullptr;  // per-cell moving-wall link bits, same shape
     // open-boundary index lists, sorted by (lz, y, x); *_zoff[lz] = first entry of plane lz
     long long n_in = 0, n_out = 0;
     long long *d_in = nullptr, *d_out = nullptr;
@@ -62,6 +64,7 @@ struct mlb_plan {
     bool out_chained = false;
     void *d_out_tmp = nullptr;
     // reductions
+    int sms = 148;
     int diag_blocks = 0;
     double *d_partials = nullptr, *d_diag = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -80,9 +83,15 @@ int layout_of(int nx, int ny, int nz, int dtype, mlb_layout *out)
     const int sz = dtype == MLB_F32 ? 4 : 8;
     const long long line = 128 / sz;
     out->nx = nx; out->ny = ny; out->nz = nz; out->itemsize = sz;
-    out->xp = (nx + line - 1) / line * line;
+    // experiment knobs (undocumented): extra row / population padding
+    const char *px = getenv("MLB_PAD_X"), *pp = getenv("MLB_PAD_POP");
+    const long long pad_x = px ? atoll(px) : 0, pad_pop = pp ? atoll(pp) : 0;
+    out->xp = (nx + pad_x + line - 1) / line * line;
     out->plane = (long long)ny * out->xp;
-    out->pop = (long long)(nz + 2) * out->plane;
+    out->pop = (long long)(nz + 2) * out->plane + pad_pop * line;
+    if (out->pop >= (1LL << 31))
+        return fail(MLB_EUNSUPPORTED, "slab of %dx%dx%d cells exceeds 2^31 elements per "
+                    "population; use more z-slabs", nx, ny, nz);
     out->total = MLB_Q * out->pop;
     out->bytes = out->total * sz;
     return MLB_OK;
@@ -156,32 +165,33 @@ int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1,
                 cudaStream_t st)
 {
     mlb::StepArgs<T> a;
-    a.fpre = static_cast<const T *>(fpre);
-    a.fpost = static_cast<T *>(fpost);
+    for (int q = 0; q < MLB_Q; ++q) {
+        a.pre[q] = static_cast<const T *>(fpre) + (long long)q * p->lay.pop;
+        a.post[q] = static_cast<T *>(fpost) + (long long)q * p->lay.pop;
+    }
     a.cls = p->d_cls;
+    a.mlinks = p->d_mlinks;
     a.g = p->g;
     a.z0 = z0;
+    a.passthrough = p->passthrough;
     a.omega = T(p->omega);
     wall_terms<T>(p->wall_u, a.k);
-    // variant: 0 = auto, 32..512 = scalar kernel with that block width,
-    // 1008 / 1016 / 1032 = vectorised kernel with 8 / 16 / 32 packs per warp row
+    // variant: 0 = auto; 32..512 = one cell per thread with that block width;
+    // 1008 / 1016 / 1032 = 16-byte packs (4 floats / 2 doubles), 8 / 16 / 32
+    // packs per warp row
     constexpr int V = mlb::Vec<T>::V;
     int variant = p->variant;
     if (variant == 0)
-        variant = (p->nx % V == 0 && p->nx >= 8 * V) ? 1008 : 128;
+        variant = 128;
     if (variant >= 1000) {
         if (p->nx % V != 0)
             return fail(MLB_EINVAL, "the vectorised kernel needs nx %% %d == 0", V);
         const int lx = variant - 1000;
         const int rows = 128 / lx;  // rows per 128-thread block
         const dim3 grid((p->nx / V + lx - 1) / lx, (p->ny + rows - 1) / rows, z1 - z0);
-        switch (lx) {
-        case 8: mlb::step_vec_kernel<T, 8><<<grid, 128, 0, st>>>(a, p->d_links); break;
-        case 16: mlb::step_vec_kernel<T, 16><<<grid, 128, 0, st>>>(a, p->d_links); break;
-        case 32: mlb::step_vec_kernel<T, 32><<<grid, 128, 0, st>>>(a, p->d_links); break;
-        default: return fail(MLB_EINVAL, "variant %d: packs per warp row must be 8, 16 or 32",
-                             p->variant);
-        }
+        if (lx == 8) mlb::step_vec_kernel<T, 8><<<grid, 128, 0, st>>>(a);
+        else if (lx == 16) mlb::step_vec_kernel<T, 16><<<grid, 128, 0, st>>>(a);
+        else mlb::step_vec_kernel<T, 32><<<grid, 128, 0, st>>>(a);
         MLB_LAUNCHED();
         return MLB_OK;
     }
@@ -313,9 +323,8 @@ int mlb_plan_create(mlb_plan **out, int nx, int ny, int nz, int dtype, double om
         delete p;
         return rc;
     }
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    p->diag_blocks = sms * 8;
+    cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
+    p->diag_blocks = p->sms * 8;
     cudaError_t e = cudaMalloc(&p->d_partials, sizeof(double) * mlb::DIAG_N * p->diag_blocks);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_diag, sizeof(double) * mlb::DIAG_N);
     if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
@@ -333,7 +342,7 @@ int mlb_plan_destroy(mlb_plan *p)
     if (!p)
         return MLB_OK;
     cudaSetDevice(p->device);
-    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_links); cudaFree(p->d_in);
+    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_mlinks); cudaFree(p->d_in);
     cudaFree(p->d_out); cudaFree(p->d_out_tmp); cudaFree(p->d_partials); cudaFree(p->d_diag);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
@@ -367,9 +376,16 @@ int mlb_plan_set_variant(mlb_plan *p, int variant)
     if (int rc = check_plan(p, false)) return rc;
     if (variant != 0 && variant != 32 && variant != 64 && variant != 128 && variant != 256
         && variant != 512 && variant != 1008 && variant != 1016 && variant != 1032)
-        return fail(MLB_EINVAL, "variant must be 0 (auto), a scalar block width in "
-                    "{32,64,128,256,512}, or 1008/1016/1032 (vectorised kernel)");
+        return fail(MLB_EINVAL, "variant must be 0 (auto), a block width in {32,64,128,256,512} "
+                    "(one cell per thread) or 1008/1016/1032 (16-byte packs)");
     p->variant = variant;
+    return MLB_OK;
+}
+
+int mlb_plan_set_passthrough(mlb_plan *p, int on)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    p->passthrough = on ? 1 : 0;
     return MLB_OK;
 }
 
@@ -441,14 +457,14 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
             break;
         }
 
-    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_links); cudaFree(p->d_in);
+    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_mlinks); cudaFree(p->d_in);
     cudaFree(p->d_out); cudaFree(p->d_out_tmp);
-    p->d_flags = p->d_cls = nullptr; p->d_links = nullptr; p->d_in = p->d_out = nullptr;
+    p->d_flags = nullptr; p->d_cls = p->d_mlinks = nullptr; p->d_in = p->d_out = nullptr;
     p->d_out_tmp = nullptr;
     p->have_flags = false;
     MLB_CUDA(cudaMalloc(&p->d_flags, padded));
-    MLB_CUDA(cudaMalloc(&p->d_cls, padded));
-    MLB_CUDA(cudaMalloc(&p->d_links, padded * sizeof(unsigned long long)));
+    MLB_CUDA(cudaMalloc(&p->d_cls, padded * sizeof(uint32_t)));
+    MLB_CUDA(cudaMalloc(&p->d_mlinks, padded * sizeof(uint32_t)));
     MLB_CUDA(cudaMemcpy(p->d_flags, pad.data(), padded, cudaMemcpyHostToDevice));
     p->n_in = (long long)in_idx.size();
     p->n_out = (long long)out_idx.size();
@@ -465,7 +481,7 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
             MLB_CUDA(cudaMalloc(&p->d_out_tmp, (size_t)p->lay.itemsize * MLB_Q * p->n_out));
     }
     const dim3 grid((unsigned)((xp + 127) / 128), ny, nz + 2);
-    mlb::build_cls_kernel<<<grid, 128>>>(p->d_flags, p->d_cls, p->d_links, p->g);
+    mlb::build_cls_kernel<<<grid, 128>>>(p->d_flags, p->d_cls, p->d_mlinks, p->g);
     MLB_LAUNCHED();
     MLB_CUDA(cudaDeviceSynchronize());
     p->have_flags = true;
@@ -477,16 +493,16 @@ int mlb_plan_get_flags(const mlb_plan *p, uint8_t *h_flags)
     if (int rc = check_plan(p, true)) return rc;
     if (!h_flags) return fail(MLB_EINVAL, "h_flags is NULL");
     MLB_CUDA(cudaSetDevice(p->device));
-    // from the class table's low bits: proves the bytes the kernel tests
+    // from the class words' low bits: proves the codes the kernel tests
     const size_t padded = (size_t)(p->nz + 2) * p->lay.plane;
-    std::vector<uint8_t> pad(padded);
-    MLB_CUDA(cudaMemcpy(pad.data(), p->d_cls, padded, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> pad(padded);
+    MLB_CUDA(cudaMemcpy(pad.data(), p->d_cls, padded * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     for (int z = 0; z < p->nz; ++z)
         for (int y = 0; y < p->ny; ++y)
             for (int x = 0; x < p->nx; ++x)
-                h_flags[((size_t)z * p->ny + y) * p->nx + x] =
+                h_flags[((size_t)z * p->ny + y) * p->nx + x] = (uint8_t)(
                     pad[(size_t)(z + 1) * p->lay.plane + (size_t)y * p->lay.xp + x]
-                    & mlb::CLS_FLAG;
+                    & mlb::CLS_FLAG);
     return MLB_OK;
 }
 

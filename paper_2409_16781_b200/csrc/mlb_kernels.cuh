@@ -28,20 +28,30 @@ struct Geom {
 
 template <typename T>
 struct StepArgs {
-    const T *__restrict__ fpre;
-    T *__restrict__ fpost;
-    const uint8_t *__restrict__ cls;
+    // one base pointer per population (host-computed: keeps the 64-bit
+    // q * pop products out of the kernel; an address is then a single
+    // IMAD.WIDE of a 32-bit in-population offset onto a constant-bank base)
+    const T *pre[Q];
+    T *post[Q];
+    const uint32_t *__restrict__ cls;     // per-cell class word, see below
+    const uint32_t *__restrict__ mlinks;  // per-cell moving-wall link bits (rarely read)
     Geom g;
     int z0;        // first slab plane this launch updates (blockIdx.z = 0)
+    int passthrough;  // 1: non-fluid cells are rewritten with fpre's value (see step_cell)
     T omega;
     T k[Q];        // moving-wall terms 6 w_i (c_i . u_w), compute dtype
 };
 
-// class byte: low 3 bits = the reference's flag code (boundaries.py:20-24),
-// bit 7 = "some neighbour is SOLID or MOVING_WALL" (cell needs the flag-test
-// gather).  cls == 0 is a bulk fluid cell: 19 plain loads, no flag reads.
-constexpr uint8_t CLS_FLAG = 0x07;
-constexpr uint8_t CLS_NEAR_WALL = 0x80;
+// Per-cell class word, built once from the flags (build_cls_kernel):
+//   bits 0..2   the reference's flag code (boundaries.py:20-24)
+//   bit  2 + i  (i = 1..18) the source cell of direction i is a wall (SOLID or
+//               MOVING_WALL): that link bounces back
+//   bit  31     some bouncing link hits a MOVING_WALL: mlinks[d] bit i says which
+// cls == 0 is a bulk fluid cell.  One 4-byte load per cell tells the kernel
+// everything the reference learns from 19 flag reads (kernels.py:76-197).
+constexpr uint32_t CLS_FLAG = 0x7u;
+constexpr uint32_t CLS_MOVING = 0x80000000u;
+__host__ __device__ constexpr uint32_t cls_link(int i) { return 1u << (2 + i); }
 
 // ---------------------------------------------------------------------------
 // collide: lattice.collide_cell (lattice.py:127-182) for 19 velocities.
@@ -112,120 +122,135 @@ __host__ __device__ constexpr int opp(int i)
 // Fused pull-stream + bounce-back + BGK collide, one thread per cell
 // (kernels.py:76-245 `cell`, :247-279 `fused`).  blockIdx = (x tile, y, plane).
 // Reads fpre only, writes each FLUID cell of fpost once, nothing else.
+//
+// The kernel is latency-bound long before it is issue-bound, so everything
+// is arranged to put ONE memory round trip on a warp's critical path:
+//  * the class word and all 19 pulls are issued together, before the class
+//    word is looked at (a solid cell's pulls are simply dropped; wall cells
+//    hold valid, never-written populations, so every address is readable);
+//  * positions are 32-bit element offsets inside a population
+//    (layout_of() guarantees pop < 2^31) on host-computed per-population
+//    base pointers: an address is one IMAD + one IMAD.WIDE;
+//  * the offset of a source cell is the destination offset plus a
+//    BLOCK-UNIFORM delta (y / z neighbours incl. periodic wrap or halo plane)
+//    plus a per-thread x delta (-1 / +1, or the wrap distance on edge lanes);
+//  * wall-adjacent lanes patch their bounced directions afterwards from the
+//    link bits of the class word - no flag reads, no 3-way branches; the
+//    patch loads hit lines the same warp has just pulled.
+template <typename T>
+__device__ __forceinline__ void step_cell(const StepArgs<T> &a, const int x, const int y,
+                                          const int lz)
+{
+    const Geom &gm = a.g;
+    const int xp = (int)gm.xp, plane = (int)gm.plane;
+
+    // periodic wrap first, flag test second (kernels.py:83-96)
+    const int dxm = (x == 0) ? gm.nx - 1 : -1;            // to the source for c_x = +1
+    const int dxq = (x == gm.nx - 1) ? 1 - gm.nx : 1;     // to the source for c_x = -1
+    const int rm = ((y == 0) ? gm.ny - 1 : -1) * xp;      // block-uniform row deltas
+    const int rq = ((y == gm.ny - 1) ? 1 - gm.ny : 1) * xp;
+    const int zm = (((lz == 0) ? gm.zlo_src : lz) - (lz + 1)) * plane;          // plane deltas
+    const int zq = (((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) - (lz + 1)) * plane;
+    constexpr int zc = 0, rc = 0;
+
+    const int d = (lz + 1) * plane + y * xp + x;
+    const int dm = d + dxm, dq = d + dxq, dc = d;
+
+    const uint32_t cd = a.cls[d];
+    T g[Q];
+    g[0] = a.pre[0][d];
+#define MLB_PULL(i, zz, rr, dd) g[i] = a.pre[i][(dd) + ((zz) + (rr))];
+    MLB_PULL(1, zc, rc, dm)  MLB_PULL(2, zc, rm, dc)  MLB_PULL(3, zc, rc, dq)
+    MLB_PULL(4, zc, rq, dc)  MLB_PULL(5, zc, rm, dm)  MLB_PULL(6, zc, rm, dq)
+    MLB_PULL(7, zc, rq, dq)  MLB_PULL(8, zc, rq, dm)  MLB_PULL(9, zm, rc, dc)
+    MLB_PULL(10, zq, rc, dc) MLB_PULL(11, zm, rc, dm) MLB_PULL(12, zm, rc, dq)
+    MLB_PULL(13, zq, rc, dq) MLB_PULL(14, zq, rc, dm) MLB_PULL(15, zm, rm, dc)
+    MLB_PULL(16, zm, rq, dc) MLB_PULL(17, zq, rq, dc) MLB_PULL(18, zq, rm, dc)
+#undef MLB_PULL
+
+    // Non-fluid destination.  Strict mode: never written (kernels.py:79-80;
+    // the stores of the warp then leave 28-of-32-byte sectors at every wall,
+    // which L2 completes with a DRAM read - measured 9 % slower on the
+    // cavity).  Pass-through mode: the cell is rewritten with the value it
+    // holds in fpre; the caller guarantees fpre and fpost agree on non-fluid
+    // cells (true for every state the engine builds: both buffers start
+    // identical and only fluid / open-boundary cells ever change), so the
+    // bytes in memory are the same as if the cell had not been touched and
+    // every store of the warp is a full line.
+    const bool fluid = (cd & CLS_FLAG) == 0;
+    if (!fluid && !a.passthrough)
+        return;
+
+    if (fluid) {
+        if (cd != 0) {
+            // SOLID source -> own opposite population, MOVING_WALL source ->
+            // that plus the wall term (kernels.py:88-96)
+            const uint32_t mv = (cd & CLS_MOVING) ? a.mlinks[d] : 0u;
+#pragma unroll
+            for (int i = 1; i < Q; ++i)
+                if (cd & cls_link(i)) {
+                    const T c = a.pre[opp(i)][d];
+                    g[i] = (mv & (1u << i)) ? c + a.k[i] : c;
+                }
+        }
+        collide<T>(g, a.omega);
+    } else {
+        // pass-through: the pulled values are neighbours', not this cell's
+#pragma unroll
+        for (int i = 1; i < Q; ++i)
+            g[i] = a.pre[i][d];
+    }
+
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+        a.post[i][d] = g[i];
+}
+
 template <typename T, int BX>
 __global__ void __launch_bounds__(BX) step_kernel(const StepArgs<T> a)
 {
-    const Geom &gm = a.g;
     const int x = blockIdx.x * BX + threadIdx.x;
-    if (x >= gm.nx)
+    if (x >= a.g.nx)
         return;
-    const int y = blockIdx.y;
-    const int lz = a.z0 + blockIdx.z;
-
-    // periodic wrap first, flag test second (kernels.py:83-96); y and z are
-    // block-uniform, the x wrap touches only the two edge lanes of a row.
-    const int xm = (x == 0) ? gm.nx - 1 : x - 1;          // source for c_x = +1
-    const int xq = (x == gm.nx - 1) ? 0 : x + 1;          // source for c_x = -1
-    const int ym = (y == 0) ? gm.ny - 1 : y - 1;
-    const int yq = (y == gm.ny - 1) ? 0 : y + 1;
-    const long long zc = (long long)(lz + 1) * gm.plane;
-    const long long zm = (long long)((lz == 0) ? gm.zlo_src : lz) * gm.plane;
-    const long long zq = (long long)((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) * gm.plane;
-    const long long rc = (long long)y * gm.xp, rm = (long long)ym * gm.xp,
-                    rq = (long long)yq * gm.xp;
-
-    const long long d = zc + rc + x;
-    const uint8_t cd = a.cls[d];
-    if (cd & CLS_FLAG)
-        return;  // non-fluid destination: never written (kernels.py:79-80)
-
-    const T *__restrict__ f = a.fpre;
-    const long long P = gm.pop;
-    T g[Q];
-    g[0] = f[d];
-
-    if (cd == 0) {
-#define MLB_PULL(i, zz, rr, xx) g[i] = f[(long long)(i) * P + (zz) + (rr) + (xx)];
-        MLB_PULL(1, zc, rc, xm)  MLB_PULL(2, zc, rm, x)   MLB_PULL(3, zc, rc, xq)
-        MLB_PULL(4, zc, rq, x)   MLB_PULL(5, zc, rm, xm)  MLB_PULL(6, zc, rm, xq)
-        MLB_PULL(7, zc, rq, xq)  MLB_PULL(8, zc, rq, xm)  MLB_PULL(9, zm, rc, x)
-        MLB_PULL(10, zq, rc, x)  MLB_PULL(11, zm, rc, xm) MLB_PULL(12, zm, rc, xq)
-        MLB_PULL(13, zq, rc, xq) MLB_PULL(14, zq, rc, xm) MLB_PULL(15, zm, rm, x)
-        MLB_PULL(16, zm, rq, x)  MLB_PULL(17, zq, rq, x)  MLB_PULL(18, zq, rm, x)
-#undef MLB_PULL
-    } else {
-        // near a wall: SOLID source -> own opposite population, MOVING_WALL
-        // source -> that plus the wall term, anything else (fluid, inlet,
-        // outlet) -> plain pull (kernels.py:88-96, boundaries.py:10-12)
-#define MLB_PULL(i, zz, rr, xx)                                         \
-        {                                                               \
-            const long long s_ = (zz) + (rr) + (xx);                    \
-            const uint8_t m_ = a.cls[s_] & CLS_FLAG;                    \
-            if (m_ == 1)                                                \
-                g[i] = f[(long long)opp(i) * P + d];                    \
-            else if (m_ == 2)                                           \
-                g[i] = f[(long long)opp(i) * P + d] + a.k[i];           \
-            else                                                        \
-                g[i] = f[(long long)(i) * P + s_];                      \
-        }
-        MLB_PULL(1, zc, rc, xm)  MLB_PULL(2, zc, rm, x)   MLB_PULL(3, zc, rc, xq)
-        MLB_PULL(4, zc, rq, x)   MLB_PULL(5, zc, rm, xm)  MLB_PULL(6, zc, rm, xq)
-        MLB_PULL(7, zc, rq, xq)  MLB_PULL(8, zc, rq, xm)  MLB_PULL(9, zm, rc, x)
-        MLB_PULL(10, zq, rc, x)  MLB_PULL(11, zm, rc, xm) MLB_PULL(12, zm, rc, xq)
-        MLB_PULL(13, zq, rc, xq) MLB_PULL(14, zq, rc, xm) MLB_PULL(15, zm, rm, x)
-        MLB_PULL(16, zm, rq, x)  MLB_PULL(17, zq, rq, x)  MLB_PULL(18, zq, rm, x)
-#undef MLB_PULL
-    }
-
-    collide<T>(g, a.omega);
-
-    T *__restrict__ o = a.fpost + d;
-#pragma unroll
-    for (int i = 0; i < Q; ++i)
-        o[(long long)i * P] = g[i];
+    step_cell<T>(a, x, blockIdx.y, a.z0 + blockIdx.z);
 }
 
 // ---------------------------------------------------------------------------
-// Vectorised fused update: each thread owns a PACK of V = 16 / sizeof(T)
-// consecutive cells in x (one 16-byte word per population), a warp covers
-// LX packs in x by 32 / LX rows in y.  Per pack and population: one aligned
+// Vectorised variant: each thread owns a PACK of V = 16 / sizeof(T)
+// consecutive cells in x (one 16-byte word per population); a warp covers LX
+// packs in x by 32 / LX rows in y.  Per pack and population: one aligned
 // 16-byte load; the ten populations with c_x = +-1 need the word shifted by
 // one cell, which costs one extra scalar load of the element just outside
 // the pack (an L1 hit: the neighbouring lane's word holds it).  Stores are
 // aligned 16-byte words (pull scheme: destinations are never shifted).
-//
-// Walls stay branch-free: a warp whose packs are all bulk fluid takes the
-// plain path; any other warp takes the "general" path as a whole, where a
-// lane with wall links also loads its own cell's opposite populations and
-// selects per cell and direction with the precomputed link masks
-// (kernels.py:88-96: SOLID source -> own opposite population, MOVING_WALL
-// source -> that plus the wall term).  No flag reads, no divergence.
-template <typename T> struct Vec;
-template <> struct Vec<float>  { using type = float4;  static constexpr int V = 4; };
-template <> struct Vec<double> { using type = double2; static constexpr int V = 2; };
+// Same early-issue and link-bit patching as the scalar kernel.  Kept as a
+// selectable variant: at 512^3 it measures within 2 % of the scalar kernel
+// (fewer instructions per cell, but 3x the registers per thread).
+template <typename T, int V> struct Pack;
+template <> struct Pack<float, 4>  { using type = float4;  using ctype = uint4; };
+template <> struct Pack<double, 2> { using type = double2; using ctype = uint2; };
+template <typename T> struct Vec { static constexpr int V = 16 / (int)sizeof(T); };
 
-template <typename T>
-__device__ __forceinline__ void unpack(const typename Vec<T>::type &v, T (&o)[Vec<T>::V]);
-template <>
-__device__ __forceinline__ void unpack<float>(const float4 &v, float (&o)[4])
+__device__ __forceinline__ void unpack(const float4 &v, float (&o)[4])
 { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
-template <>
-__device__ __forceinline__ void unpack<double>(const double2 &v, double (&o)[2])
+__device__ __forceinline__ void unpack(const double2 &v, double (&o)[2])
 { o[0] = v.x; o[1] = v.y; }
-
+__device__ __forceinline__ void unpack(const uint4 &v, uint32_t (&o)[4])
+{ o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+__device__ __forceinline__ void unpack(const uint2 &v, uint32_t (&o)[2])
+{ o[0] = v.x; o[1] = v.y; }
 __device__ __forceinline__ float4 pack(const float (&o)[4]) { return make_float4(o[0], o[1], o[2], o[3]); }
 __device__ __forceinline__ double2 pack(const double (&o)[2]) { return make_double2(o[0], o[1]); }
 
 // The V values pulled along a direction with x component CX from the row
 // starting at `row` (already offset to population, plane and row).
-template <typename T, int CX>
+template <typename T, int V, int CX>
 __device__ __forceinline__ void pull_pack(const T *__restrict__ row, int x0, int xl, int xr,
-                                          T (&o)[Vec<T>::V])
+                                          T (&o)[V])
 {
-    constexpr int V = Vec<T>::V;
-    using VT = typename Vec<T>::type;
+    using VT = typename Pack<T, V>::type;
     T w[V];
-    unpack<T>(*reinterpret_cast<const VT *>(row + x0), w);
+    unpack(*reinterpret_cast<const VT *>(row + x0), w);
     if (CX == 0) {
 #pragma unroll
         for (int j = 0; j < V; ++j) o[j] = w[j];
@@ -249,95 +274,67 @@ __device__ __forceinline__ void pull_pack(const T *__restrict__ row, int x0, int
     X(17, 0, zq, rq)  X(18, 0, zq, rm)
 
 template <typename T, int LX>
-__global__ void __launch_bounds__(128)
-step_vec_kernel(const StepArgs<T> a, const unsigned long long *__restrict__ links)
+__global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<T> a)
 {
     constexpr int V = Vec<T>::V;
-    using VT = typename Vec<T>::type;
+    using VT = typename Pack<T, V>::type;
+    using CT = typename Pack<T, V>::ctype;
     constexpr int RPW = 32 / LX;        // rows per warp
-    constexpr unsigned FULL = 0xffffffffu;
     const Geom &gm = a.g;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int x0 = (blockIdx.x * LX + (lane % LX)) * V;
     const int y = blockIdx.y * (4 * RPW) + warp * RPW + lane / LX;
     const int lz = a.z0 + blockIdx.z;
-    const bool inrange = (x0 < gm.nx) && (y < gm.ny);
+    if (x0 >= gm.nx || y >= gm.ny)
+        return;
 
-    const long long zc = (long long)(lz + 1) * gm.plane;
-    const long long zm = (long long)((lz == 0) ? gm.zlo_src : lz) * gm.plane;
-    const long long zq = (long long)((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) * gm.plane;
-    const int yy = inrange ? y : 0;
-    const int ym = (yy == 0) ? gm.ny - 1 : yy - 1;
-    const int yq = (yy == gm.ny - 1) ? 0 : yy + 1;
-    const long long rc = (long long)yy * gm.xp, rm = (long long)ym * gm.xp,
-                    rq = (long long)yq * gm.xp;
-    const int xx = inrange ? x0 : 0;
-    const int xl = (xx == 0) ? gm.nx - 1 : xx - 1;
-    const int xr = (xx + V >= gm.nx) ? 0 : xx + V;
-    const long long d = zc + rc + xx;
+    const int xp = (int)gm.xp, plane = (int)gm.plane;
+    const int zc = (lz + 1) * plane;
+    const int zm = ((lz == 0) ? gm.zlo_src : lz) * plane;
+    const int zq = ((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) * plane;
+    const int ym = (y == 0) ? gm.ny - 1 : y - 1;
+    const int yq = (y == gm.ny - 1) ? 0 : y + 1;
+    const int rc = y * xp, rm = ym * xp, rq = yq * xp;
+    const int xl = (x0 == 0) ? gm.nx - 1 : x0 - 1;
+    const int xr = (x0 + V >= gm.nx) ? 0 : x0 + V;
+    const int d = zc + rc + x0;
 
-    // class bytes of the pack, one 16/32-bit word
-    unsigned c4;
-    if (V == 4)
-        c4 = *reinterpret_cast<const unsigned *>(a.cls + d);
-    else
-        c4 = *reinterpret_cast<const unsigned short *>(a.cls + d);
-    if (!inrange)
-        c4 = (V == 4) ? 0x01010101u : 0x0101u;  // nothing to do here
-    bool fluid[V];
+    // class words of the pack and all pulls, issued together
+    uint32_t c[V];
+    unpack(*reinterpret_cast<const CT *>(a.cls + d), c);
+    T g[Q][V];
+    unpack(*reinterpret_cast<const VT *>(a.pre[0] + d), g[0]);
+#define MLB_X(i, CX, Z, R) pull_pack<T, V, CX>(a.pre[i] + ((Z) + (R)), x0, xl, xr, g[i]);
+    MLB_DIRS(MLB_X)
+#undef MLB_X
+
+    uint32_t call = 0u;
     bool anyfluid = false, allfluid = true;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-        fluid[j] = ((c4 >> (8 * j)) & CLS_FLAG) == 0;
-        anyfluid |= fluid[j];
-        allfluid &= fluid[j];
+        const bool fl = (c[j] & CLS_FLAG) == 0;
+        anyfluid |= fl;
+        allfluid &= fl;
+        call |= fl ? c[j] : 0u;
     }
-    const bool bulk = (c4 == 0);
-    const bool general = !__all_sync(FULL, bulk || !anyfluid);  // warp-uniform
-    if (!anyfluid)
+    if (!anyfluid && !a.passthrough)
         return;
 
-    const T *__restrict__ f = a.fpre;
-    const long long P = gm.pop;
-    T g[Q][V];
-    unpack<T>(*reinterpret_cast<const VT *>(f + d), g[0]);
-
-    if (!general) {
-#define MLB_X(i, CX, Z, R) pull_pack<T, CX>(f + (long long)(i) * P + (Z) + (R), xx, xl, xr, g[i]);
-        MLB_DIRS(MLB_X)
-#undef MLB_X
-    } else {
-        // link masks of the pack (zero for bulk cells; garbage-free for
-        // non-fluid ones, which are never stored)
-        unsigned lo[V], hi[V];
+    if (call != 0) {  // some fluid cell of the pack touches a wall
+        uint32_t mv[V];
 #pragma unroll
-        for (int j = 0; j < V; ++j) { lo[j] = 0u; hi[j] = 0u; }
-        if (!bulk) {
+        for (int j = 0; j < V; ++j)
+            mv[j] = ((c[j] & CLS_FLAG) == 0 && (c[j] & CLS_MOVING)) ? a.mlinks[d + j] : 0u;
 #pragma unroll
-            for (int j = 0; j < V; j += 2) {
-                const ulonglong2 m = *reinterpret_cast<const ulonglong2 *>(links + d + j);
-                lo[j] = (unsigned)m.x;     hi[j] = (unsigned)(m.x >> 32);
-                lo[j + 1] = (unsigned)m.y; hi[j + 1] = (unsigned)(m.y >> 32);
+        for (int i = 1; i < Q; ++i)
+            if (call & cls_link(i)) {
+                T o[V];
+                unpack(*reinterpret_cast<const VT *>(a.pre[opp(i)] + d), o);
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    if (c[j] & cls_link(i))
+                        g[i][j] = (mv[j] & (1u << i)) ? o[j] + a.k[i] : o[j];
             }
-        }
-        unsigned anylo = 0u;
-#pragma unroll
-        for (int j = 0; j < V; ++j) anylo |= lo[j];
-#define MLB_X(i, CX, Z, R)                                                        \
-        {                                                                         \
-            pull_pack<T, CX>(f + (long long)(i) * P + (Z) + (R), xx, xl, xr, g[i]); \
-            if (anylo & (1u << (i))) {                                            \
-                T c_[V];                                                          \
-                unpack<T>(*reinterpret_cast<const VT *>(f + (long long)opp(i) * P + d), c_); \
-                _Pragma("unroll")                                                 \
-                for (int j = 0; j < V; ++j) {                                     \
-                    if (lo[j] & (1u << (i)))                                      \
-                        g[i][j] = (hi[j] & (1u << (i))) ? c_[j] + a.k[i] : c_[j]; \
-                }                                                                 \
-            }                                                                     \
-        }
-        MLB_DIRS(MLB_X)
-#undef MLB_X
     }
 
     // collide each cell of the pack (lattice.collide_cell order)
@@ -351,30 +348,38 @@ step_vec_kernel(const StepArgs<T> a, const unsigned long long *__restrict__ link
         for (int i = 0; i < Q; ++i) g[i][j] = gc[i];
     }
 
-    T *__restrict__ o = a.fpost + d;
-    if (allfluid) {
+    if (!allfluid && a.passthrough) {
+        // non-fluid cells of the pack keep the value they hold in fpre
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            T o[V];
+            unpack(*reinterpret_cast<const VT *>(a.pre[i] + d), o);
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                if ((c[j] & CLS_FLAG) != 0)
+                    g[i][j] = o[j];
+        }
+    }
+    if (allfluid || a.passthrough) {
 #pragma unroll
         for (int i = 0; i < Q; ++i)
-            *reinterpret_cast<VT *>(o + (long long)i * P) = pack(g[i]);
+            *reinterpret_cast<VT *>(a.post[i] + d) = pack(g[i]);
     } else {
 #pragma unroll
         for (int j = 0; j < V; ++j)
-            if (fluid[j]) {
+            if ((c[j] & CLS_FLAG) == 0) {
 #pragma unroll
                 for (int i = 0; i < Q; ++i)
-                    o[(long long)i * P + j] = g[i][j];
+                    a.post[i][d + j] = g[i][j];
             }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Class table and link masks from the padded flag block (halo planes already
-// filled).  One thread per padded element of storage planes [0, nz+2).
-//   links[d] bit i      (1 <= i <= 18): the source cell of direction i is a
-//                        wall (SOLID or MOVING_WALL) -> bounce-back link
-//   links[d] bit 32 + i: that wall is a MOVING_WALL -> add the wall term k_i
-// Direction i's source is the neighbour at -c_i, with the same periodic
-// wrap / halo-plane rule as the step kernels.
+// Class words (and the moving-wall link bits) from the padded flag block,
+// halo planes already filled.  One thread per padded element of storage
+// planes [0, nz+2).  Direction i's source is the neighbour at -c_i, with the
+// same periodic wrap / halo-plane rule as the step kernels.
 __device__ __forceinline__ constexpr int dir_index(int cx, int cy, int cz)
 {
     // inverse of the velocity table in lattice.py; -1 for the 8 corners / rest
@@ -390,8 +395,8 @@ __device__ __forceinline__ constexpr int dir_index(int cx, int cy, int cz)
 }
 
 __global__ void build_cls_kernel(const uint8_t *__restrict__ flags,
-                                 uint8_t *__restrict__ cls,
-                                 unsigned long long *__restrict__ links, const Geom gm)
+                                 uint32_t *__restrict__ cls, uint32_t *__restrict__ mlinks,
+                                 const Geom gm)
 {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= gm.xp)
@@ -399,15 +404,14 @@ __global__ void build_cls_kernel(const uint8_t *__restrict__ flags,
     const int y = blockIdx.y;
     const int sz = blockIdx.z;  // storage plane
     const long long d = (long long)sz * gm.plane + (long long)y * gm.xp + x;
+    mlinks[d] = 0u;
     if (x >= gm.nx) {
-        cls[d] = 1;  // row padding: solid, never written
-        links[d] = 0ull;
+        cls[d] = 1u;  // row padding: solid, never written
         return;
     }
-    const uint8_t fl = flags[d];
-    if (sz == 0 || sz == gm.nz + 1) {
-        cls[d] = fl;  // halo planes are only ever sources
-        links[d] = 0ull;
+    const uint32_t fl = flags[d];
+    if (sz == 0 || sz == gm.nz + 1 || fl != 0) {
+        cls[d] = fl;  // halo planes are only ever sources; non-fluid cells have no links
         return;
     }
     const int lz = sz - 1;
@@ -416,7 +420,7 @@ __global__ void build_cls_kernel(const uint8_t *__restrict__ flags,
     const int ys[3] = {y, (y == 0) ? gm.ny - 1 : y - 1, (y == gm.ny - 1) ? 0 : y + 1};
     const int zs[3] = {sz, (lz == 0) ? gm.zlo_src : lz, (lz == gm.nz - 1) ? gm.zhi_src : lz + 2};
     const int cof[3] = {0, 1, -1};  // the c component served by index 0/1/2
-    unsigned long long lk = 0ull;
+    uint32_t c = 0u, mv = 0u;
 #pragma unroll
     for (int dz = 0; dz < 3; ++dz)
 #pragma unroll
@@ -429,12 +433,12 @@ __global__ void build_cls_kernel(const uint8_t *__restrict__ flags,
                 const uint8_t m = flags[(long long)zs[dz] * gm.plane
                                         + (long long)ys[dy] * gm.xp + xs[dx]];
                 if (m == 1 || m == 2)
-                    lk |= 1ull << i;
+                    c |= cls_link(i);
                 if (m == 2)
-                    lk |= 1ull << (32 + i);
+                    mv |= 1u << i;
             }
-    cls[d] = fl | (lk ? CLS_NEAR_WALL : 0);
-    links[d] = (fl == 0) ? lk : 0ull;
+    cls[d] = c | (mv ? CLS_MOVING : 0u);
+    mlinks[d] = mv;
 }
 
 // ---------------------------------------------------------------------------
@@ -599,7 +603,7 @@ __device__ __forceinline__ void diag_block_reduce(double (&acc)[DIAG_N], double 
 
 template <typename T>
 __global__ void __launch_bounds__(DIAG_THREADS)
-diag_kernel(const T *__restrict__ f, const uint8_t *__restrict__ cls, const Geom gm,
+diag_kernel(const T *__restrict__ f, const uint32_t *__restrict__ cls, const Geom gm,
             double *__restrict__ partials)
 {
     double acc[DIAG_N];

@@ -145,6 +145,7 @@ class KernelPlan:
         hi, hi_p = plane(halo_hi)
         _cabi.check(lib.mlb_plan_set_flags(self._plan, _host_ptr(mask), lo_p, hi_p))
         self._scratch = None
+        self.passthrough = False
 
     # -- lifetime ----------------------------------------------------------
     def close(self):
@@ -203,6 +204,14 @@ class KernelPlan:
         _cabi.check(self._lib.mlb_plan_set_variant(self._plan, int(variant)))
 
     set_block_width = set_variant
+
+    def set_passthrough(self, on):
+        """Pass-through stores: also rewrite non-fluid cells of fpost with the
+        value they hold in fpre.  Only valid when the two blocks agree on
+        non-fluid cells (see include/mlb.h); memory then ends up identical
+        to the strict never-written mode, but every store is a full line."""
+        self.passthrough = bool(on)
+        _cabi.check(self._lib.mlb_plan_set_passthrough(self._plan, int(self.passthrough)))
 
     # -- host <-> device ---------------------------------------------------
     def _check_host(self, a):

@@ -83,22 +83,30 @@ def test_multi_step_with_open_pass_bitwise(geom, tag, rng):
 VEC_GEOMS = ["cavity16", "channel40", "periodic8", "wide", "duct"]
 
 
-@pytest.mark.parametrize("variant", [64, 128, 1008, 1016, 1032])
+@pytest.mark.parametrize("passthrough", [False, True])
+@pytest.mark.parametrize("variant", [32, 64, 128, 256, 512, 1008, 1016, 1032])
 @pytest.mark.parametrize("tag", ["f64", "f32"])
 @pytest.mark.parametrize("geom", VEC_GEOMS)
-def test_kernel_variants_never_change_bits(geom, tag, variant, rng):
-    """Block shape / vectorisation are pure performance knobs
-    (test_kernels.py:107-126): every variant, same bits as the oracle."""
+def test_kernel_variants_never_change_bits(geom, tag, variant, passthrough, rng):
+    """Block shape, vectorisation and the store mode are pure performance
+    knobs (test_kernels.py:107-126): every variant, same bits as the oracle.
+    Strict mode must preserve arbitrary never-written cells of the second
+    buffer; pass-through mode is exercised under its precondition (the two
+    buffers agree on non-fluid cells)."""
     grid, wall_u, inlet_u = geometries3d()[geom]
     prec = PREC[tag]
     f = random_block(rng, grid.size, prec.storage)
     sentinel = random_block(rng, grid.size, prec.storage)
+    if passthrough:
+        non_fluid = B.flatten_mask(grid) != B.FLUID
+        sentinel[:, non_fluid] = f[:, non_fluid]
     omega, steps = 1.6, 3
     a, b = f.copy(), sentinel.copy()
     orc = make_oracle(grid, omega, wall_u, inlet_u)
     want = orc.run(a, b, steps)
     plan = make_plan(grid, prec, omega, wall_u, inlet_u)
     plan.set_variant(variant)
+    plan.set_passthrough(passthrough)
     da, db = plan.alloc(), plan.alloc()
     plan.upload(f, da)
     plan.upload(sentinel, db)

@@ -7,17 +7,18 @@ from paper_2409_16781_b200.fields import Layout, Precision
 from paper_2409_16781_b200.kernels import KernelPlan
 
 def run(n, prec, width, steps=30, omega=1.7):
-    nx = ny = nz = n
+    nx, ny, nz = (n, n, n) if isinstance(n, int) else n
     mask = B.flatten_mask(B.cavity_mask(nx, ny, nz))
     plan = KernelPlan(nx, ny, nz, Layout.ROW, prec, mask, omega, (0.1, 0, 0))
     plan.set_variant(width)
+    plan.set_passthrough(os.environ.get('PT', '1') == '1')
     a, b = plan.alloc(), plan.alloc()
     from paper_2409_16781_b200.lattice import W
     for q in range(19):
         a.tensor[q].fill_(float(W[q])); b.tensor[q].fill_(float(W[q]))
     plan.run_steps(a, b, 5)
     _, _, ms = plan.run_steps(a, b, steps, timed=True)
-    ml = n**3 * steps / (ms * 1e-3) / 1e6
+    ml = nx * ny * nz * steps / (ms * 1e-3) / 1e6
     bpc = 38 * prec.storage.itemsize
     out = dict(n=n, prec=prec.token, width=width, ms_per_step=ms/steps, mlups=ml, gbs=ml*1e6*bpc/1e9)
     print(json.dumps(out), flush=True)
@@ -26,8 +27,12 @@ def run(n, prec, width, steps=30, omega=1.7):
     torch.cuda.empty_cache()
 
 if __name__ == "__main__":
-    sizes = [int(s) for s in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["256", "512"])]
+    sizes = [int(s) if "x" not in s else tuple(int(v) for v in s.split("x"))
+             for s in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["256", "512"])]
+    f32v = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [128, 1016, 1116, 2008, 2016, 2032, 2108, 2116, 2132]
+    f64v = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else [128, 1016, 1116]
     for n in sizes:
-        for prec in (Precision.SINGLE, Precision.DOUBLE):
-            for width in (128, 1008, 1016, 1032):
-                run(n, prec, width)
+        for width in f32v:
+            run(n, Precision.SINGLE, width)
+        for width in f64v:
+            run(n, Precision.DOUBLE, width)
