@@ -259,6 +259,7 @@ def main():
             host[q].fill(W[q])
     if args.variant:
         plan.set_variant(args.variant)
+    kernel_name = plan.kernel_name
     a, b = plan.alloc(), plan.alloc()
     plan.upload(host, a)
     b.tensor.copy_(a.tensor)
@@ -367,7 +368,7 @@ def main():
         traffic = json.load(open(tpath)).get(key)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "kernel": "mlb::step_kernel", "algorithmic_bytes_per_update": bytes_per_update,
+                "kernel": kernel_name, "algorithmic_bytes_per_update": bytes_per_update,
                 "updates_per_launch": cells_rank, "kernel_ms": kernel_ms}
 
     cpu_base = None

@@ -11,7 +11,7 @@
  * Memory model.  The CALLER owns every population buffer (in the Python
  * host: torch tensors; only data_ptr() crosses) - mirroring the reference,
  * where KernelPlan keeps no population copies (kernels.py:398-443).  The
- * plan owns only what it derives from the flags (a per-cell class byte, the
+ * plan owns only what it derives from the flags (a per-cell class word, the
  * inlet/outlet index lists), reduction scratch and two timing events.
  *
  * Host layout (what the reference passes): dense C-contiguous
@@ -78,6 +78,8 @@ int mlb_plan_set_physics(mlb_plan *plan, double omega, const double wall_u[3],
  * default, 32..512 = one cell per thread with that block width, 1008 / 1016 /
  * 1032 = 16-byte packs with 8 / 16 / 32 packs per warp row */
 int mlb_plan_set_variant(mlb_plan *plan, int variant);
+/* name of the fused kernel mlb_step will launch for this plan (for reports) */
+const char *mlb_plan_kernel_name(const mlb_plan *plan);
 /* Pass-through stores (default off = the reference's contract, non-fluid
  * cells of fpost are never written).  When on, mlb_step also stores every
  * non-fluid cell, with the value it holds in d_fpre.  The caller asserts

@@ -160,6 +160,16 @@ void inlet_values(double u_in, T *e)
     e[0] = wr0 * um;
 }
 
+// the kernel `variant` resolves to for this plan (0 = auto)
+int resolve_variant(const mlb_plan *p)
+{
+    const int V = p->dtype == MLB_F32 ? 4 : 2;
+    if (p->variant != 0)
+        return p->variant;
+    // measured on B200 (tools/sweep.py): packs win in fp32, not in fp64
+    return (p->dtype == MLB_F32 && p->nx % V == 0 && p->nx >= 128) ? 1016 : 128;
+}
+
 template <typename T>
 int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1,
                 cudaStream_t st)
@@ -180,9 +190,7 @@ int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1,
     // 1008 / 1016 / 1032 = 16-byte packs (4 floats / 2 doubles), 8 / 16 / 32
     // packs per warp row
     constexpr int V = mlb::Vec<T>::V;
-    int variant = p->variant;
-    if (variant == 0)
-        variant = 128;
+    const int variant = resolve_variant(p);
     if (variant >= 1000) {
         if (p->nx % V != 0)
             return fail(MLB_EINVAL, "the vectorised kernel needs nx %% %d == 0", V);
@@ -380,6 +388,19 @@ int mlb_plan_set_variant(mlb_plan *p, int variant)
                     "(one cell per thread) or 1008/1016/1032 (16-byte packs)");
     p->variant = variant;
     return MLB_OK;
+}
+
+const char *mlb_plan_kernel_name(const mlb_plan *p)
+{
+    static thread_local char name[64];
+    if (!p) return "";
+    const int v = resolve_variant(p);
+    const char *t = p->dtype == MLB_F32 ? "float" : "double";
+    if (v >= 1000)
+        snprintf(name, sizeof(name), "mlb::step_vec_kernel<%s, %d>", t, v - 1000);
+    else
+        snprintf(name, sizeof(name), "mlb::step_kernel<%s, %d>", t, v);
+    return name;
 }
 
 int mlb_plan_set_passthrough(mlb_plan *p, int on)

@@ -205,6 +205,10 @@ class KernelPlan:
 
     set_block_width = set_variant
 
+    @property
+    def kernel_name(self):
+        return self._lib.mlb_plan_kernel_name(self._plan).decode()
+
     def set_passthrough(self, on):
         """Pass-through stores: also rewrite non-fluid cells of fpost with the
         value they hold in fpre.  Only valid when the two blocks agree on
