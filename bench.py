@@ -53,13 +53,15 @@ METRIC = "MLUPS (D3Q19 BGK)"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=0, help="override the edge length (debug)")
     ap.add_argument("--precision", default="single", choices=["single", "double"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-slab", action="store_true",
+                    help="run the z-slab driver (halo planes, boundary-first overlap) even on 1 GPU")
     ap.add_argument("--variant", type=int, default=0, help="kernel variant (tuning; see mlb_plan_set_variant)")
     return ap.parse_args()
 
@@ -168,7 +170,7 @@ def cpu_arm(n, prec, steps, warmup, budget_s):
     t0 = time.perf_counter(); orc.step(b, a); dt = time.perf_counter() - t0
     rate = n * n * 8 / dt
     nz = int(rate * budget_s / ((steps + warmup) * n * n))
-    nz = max(8, min(n, nz))
+    nz = max(32, min(n, nz))
     orc, a, b = make(nz)
     for _ in range(warmup):
         orc.step(a, b); a, b = b, a
@@ -196,7 +198,7 @@ def main():
             return 0
         from paper_2409_16781_b200.lattice import omega_from_reynolds
         omega = omega_from_reynolds(RE, U0, n).omega
-        base, ms = cpu_arm(n, prec_tok, args.steps, args.warmup, budget_s=90.0)
+        base, ms = cpu_arm(n, prec_tok, args.steps, args.warmup, budget_s=120.0)
         line = {
             "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "MLUPS",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -240,7 +242,8 @@ def main():
         torch.cuda.synchronize()
 
     # ---- host state (pinned) and the plan ----------------------------------
-    if world == 1:
+    slab_mode = world > 1 or args.force_slab
+    if not slab_mode:
         spec = cases.CaseSpec("ldc", n, n, n, re=RE, u0=U0)
         state = cases.init(spec, prec)
         mask_flat = state.mask
@@ -265,7 +268,7 @@ def main():
     b.tensor.copy_(a.tensor)
     plan.set_passthrough(True)   # both blocks identical: what engine.Session establishes
     runner = None
-    if world > 1:
+    if slab_mode:
         runner = slab.DistSlab(slab.CudaStepper(plan), n, rank, world)
         for r in runner.exchange(a):
             r.wait()
@@ -306,7 +309,7 @@ def main():
         del a, b
         plan.close()
         torch.cuda.empty_cache()
-        if world == 1:
+        if not slab_mode:
             cfg = engine.RunConfig(steps=args.steps, precision=prec, device=local)
             warm = engine.RunConfig(steps=max(1, args.warmup), precision=prec, device=local)
             engine.run(state, warm)              # allocator / page-lock warm-up, untimed
@@ -344,8 +347,9 @@ def main():
                "d2h_bytes_per_step": d2h * world / args.steps,
                "seconds": dt,
                "call": "engine.run(host state, RunConfig(steps=K)): upload, K steps, download"
-                       if world == 1 else
+                       if not slab_mode else
                        "per rank: KernelPlan + upload, DistSlab.run(K), download"}
+
 
     if rank != 0:
         if world > 1:

@@ -22,6 +22,7 @@ Diagnostics (`macro`, `diagnostics`, `check_finite`, the per-step probe)
 execute on the device too; there is no CPU compute path in this package.
 """
 
+import struct
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -32,6 +33,12 @@ from .fields import (Layout, PopulationField, Precision, convert_precision,
                      flatten_xyz)
 from .kernels import BACKEND, DeviceField, KernelPlan, pinned_empty  # noqa: F401
 from .lattice import Q, RelaxationParams, equilibrium
+
+
+MAGIC = b"MLB2"
+VERSION = 2
+# magic, version, nx, ny, nz, precision code, layout code, Q, reserved, timestep
+_HEADER = struct.Struct("<4sIIIIBBBBQ")
 
 
 class DivergenceError(RuntimeError):
@@ -379,3 +386,70 @@ def run(state, config, on_output=None, on_checkpoint=None, probe=None):
                     nz=state.nz, mlups=mlups,
                     probe_series=(rec[:, 2].copy() if rec is not None else None),
                     probe_samples=rec)
+
+
+def checkpoint(state, path):
+    """Write the state in the binary checkpoint format, version 2.
+
+    The reference's MLB1 format (engine.py:9-13, :278-287) with the third
+    dimension added: little-endian header `<4sIIIIBBBBQ` = magic "MLB2", u32
+    version 2, u32 nx, ny, nz, u8 precision code, u8 layout code, u8 Q (19),
+    u8 reserved, u64 timestep (32 bytes), then the nineteen pre-buffer planes
+    in cell order, then the mask, one byte per cell.  Physics parameters
+    are not serialised.  A GPU-resident state is synchronised first.
+    """
+    if state.session is not None:
+        state.session.sync_host()
+    le_storage = state.precision.storage.newbyteorder("<")
+    planes = np.ascontiguousarray(state.f_pre.data, dtype=le_storage)
+    header = _HEADER.pack(MAGIC, VERSION, state.nx, state.ny, state.nz,
+                          state.precision.code, state.layout.code, Q, 0, state.t)
+    with open(path, "wb") as fh:
+        fh.write(header)
+        fh.write(planes.tobytes())
+        fh.write(np.ascontiguousarray(state.mask, dtype=np.uint8).tobytes())
+
+
+def restore(path):
+    """Read a checkpoint back into a host state (engine.py:290-330).
+
+    The returned state carries params=None; callers re-attach physics with
+    `cases.attach_params`.  Header and payload sizes are validated and
+    errors name the offending byte offset.
+    """
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if len(blob) < _HEADER.size:
+        raise ValueError(
+            f"truncated checkpoint: {len(blob)} bytes is shorter than the "
+            f"{_HEADER.size}-byte header")
+    magic, version, nx, ny, nz, pcode, lcode, q, _, t = _HEADER.unpack_from(blob, 0)
+    if magic != MAGIC:
+        raise ValueError(f"not a checkpoint file (magic {magic!r} at offset 0)")
+    if version != VERSION:
+        raise ValueError(f"unsupported checkpoint version {version} "
+                         f"(offset 4), expected {VERSION}")
+    precision = Precision.from_code(pcode)
+    layout = Layout.from_code(lcode)
+    if q != Q:
+        raise ValueError(f"checkpoint holds {q} populations per cell "
+                         f"(offset 22), expected {Q}")
+    n = nx * ny * nz
+    le_storage = precision.storage.newbyteorder("<")
+    plane_bytes = Q * n * le_storage.itemsize
+    expected = _HEADER.size + plane_bytes + n
+    if len(blob) != expected:
+        raise ValueError(
+            f"checkpoint payload mismatch for declared {nx}x{ny}x{nz} grid: "
+            f"expected {expected} bytes, found {len(blob)} "
+            f"(payload starts at offset {_HEADER.size})")
+    planes = np.frombuffer(blob, dtype=le_storage, count=Q * n, offset=_HEADER.size)
+    data = pinned_empty((Q, n), precision.storage)
+    data[:] = planes.reshape(Q, n)
+    mask = np.frombuffer(blob, dtype=np.uint8, count=n,
+                         offset=_HEADER.size + plane_bytes).copy()
+    if mask.max(initial=0) > boundaries.OUTLET:
+        raise ValueError("checkpoint mask holds unknown cell codes")
+    f_pre = PopulationField(data, nx, ny, nz, layout)
+    return SimState(f_pre=f_pre, f_post_=None, mask=mask, nx=nx, ny=ny, nz=nz,
+                    layout=layout, precision=precision, t=t)

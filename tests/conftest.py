@@ -14,6 +14,14 @@ GOLDEN = os.path.join(ROOT, "tests", "golden", "lb2d_golden.npz")
 def pytest_configure(config):
     config.addinivalue_line(
         "markers", "gpu: needs a CUDA device (run on the B200 box with -m gpu)")
+    # the built libraries travel with the tree; if a checkout lacks them,
+    # build them once (nvcc cross-compiles without a GPU)
+    import shutil
+    import subprocess
+    lib = os.path.join(ROOT, "paper_2409_16781_b200", "libmlb_d3q19.so")
+    if not os.path.exists(lib) and (shutil.which("nvcc") or os.path.exists("/usr/local/cuda/bin/nvcc")):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "paper_2409_16781_b200", "csrc")],
+                       check=False, capture_output=True)
 
 
 @pytest.fixture
