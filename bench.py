@@ -48,6 +48,9 @@ sys.path.insert(0, ROOT)
 NX = NY = NZ_PER_GPU = 512
 RE, U0 = 1000.0, 0.1
 METRIC = "MLUPS (D3Q19 BGK)"
+PREC_NAME = {"single": "fp32", "double": "fp64", "mixed1": "fp16 storage / fp32 compute"}
+PREC_BYTES = {"single": 4, "double": 8, "mixed1": 2}
+PREC_DTYPE = {"single": "f32", "double": "f64", "mixed1": "f16 storage, f32 compute"}
 
 
 def parse():
@@ -57,7 +60,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=0, help="override the edge length (debug)")
-    ap.add_argument("--precision", default="single", choices=["single", "double"])
+    ap.add_argument("--precision", default="single", choices=["single", "double", "mixed1"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-slab", action="store_true",
@@ -69,13 +72,13 @@ def parse():
 def workload_config(n, nz_global, world, prec, omega):
     size = f"{n}^3" if world == 1 else f"{n}x{n}x{nz_global}"
     return {
-        "workload": f"D3Q19 BGK lid-driven cavity {size} {'fp32' if prec == 'single' else 'fp64'}"
+        "workload": f"D3Q19 BGK lid-driven cavity {size} {PREC_NAME[prec]}"
                     f" (BASELINE.json configs[2]{', z-slab weak scaling' if world > 1 else ''})",
         "nx": n, "ny": n, "nz_per_gpu": n, "nz_global": nz_global,
         "re": RE, "u0": U0, "omega": omega,
         "decomposition": f"{world} z-slab(s), 5-population halos over NCCL" if world > 1 else "single GPU",
         "l2_policy": "inputs exceed L2: two population blocks of "
-                     f"{19 * n ** 3 * (4 if prec == 'single' else 8) / 1e9:.1f} GB per GPU vs 126 MB L2",
+                     f"{19 * n ** 3 * PREC_BYTES[prec] / 1e9:.1f} GB per GPU vs 126 MB L2",
     }
 
 
@@ -154,7 +157,7 @@ def cpu_arm(n, prec, steps, warmup, budget_s):
     from paper_2409_16781_b200 import boundaries as B
     from paper_2409_16781_b200.lattice import W, omega_from_reynolds
     cores = os.cpu_count() or 1
-    dtype = np.float32 if prec == "single" else np.float64
+    dtype = {"single": np.float32, "double": np.float64, "mixed1": np.float16}[prec]
     omega = omega_from_reynolds(RE, U0, n).omega
 
     def make(nz):
@@ -181,7 +184,7 @@ def cpu_arm(n, prec, steps, warmup, budget_s):
     mlups = n * n * nz * steps / dt / 1e6
     return {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": "port",
             "sample": f"{n}x{n}x{nz} z-slice of the cavity, {steps} steps after {warmup} warm-up, "
-                      f"{'fp32' if prec == 'single' else 'fp64'}, C/OpenMP port of the reference "
+                      f"{PREC_NAME[prec]}, C/OpenMP port of the reference "
                       f"algorithm (oracle/d3q19_oracle.c), {cores} threads"}, dt / steps * 1e3
 
 
@@ -203,7 +206,7 @@ def main():
             "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "MLUPS",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32" if prec_tok == "single" else "f64", "data": "synthetic",
+            "dtype": PREC_DTYPE[prec_tok], "data": "synthetic",
             "config": workload_config(n, n * max(1, args.gpus), max(1, args.gpus), prec_tok, omega),
             "cpu_baseline": base,
             "e2e": {"value": base["value"], "unit": "MLUPS", "h2d_bytes_per_step": 0,
@@ -368,7 +371,7 @@ def main():
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        key = f"step_kernel_{'f32' if prec_tok == 'single' else 'f64'}_{n}"
+        key = f"step_kernel_{ {'single': 'f32', 'double': 'f64', 'mixed1': 'f16'}[prec_tok] }_{n}"
         traffic = json.load(open(tpath)).get(key)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -383,7 +386,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32" if prec_tok == "single" else "f64", "data": "synthetic",
+        "dtype": PREC_DTYPE[prec_tok], "data": "synthetic",
         "config": workload_config(n, nz_global, world, prec_tok, params.omega),
         "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(nl.item()),
         "roofline": roofline, "cpu_baseline": cpu_base,

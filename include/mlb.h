@@ -35,8 +35,11 @@ extern "C" {
 #define MLB_ABI_VERSION 1
 #define MLB_Q 19
 
-/* dtype codes = the reference's Precision wire codes (fields.py:22-23) */
-enum { MLB_F32 = 0, MLB_F64 = 1 };
+/* dtype codes = the reference's Precision wire codes (fields.py:22-24):
+ * single, double, and mixed1 = populations STORED as IEEE binary16 and
+ * computed in float (exact upcast on load, round-to-nearest-even on store,
+ * kernels.py:435-455).  The reference's mixed2 (code 3) is not built. */
+enum { MLB_F32 = 0, MLB_F64 = 1, MLB_F16 = 2 };
 /* how the pulls across the slab's z faces are served */
 enum { MLB_Z_PERIODIC = 0, /* whole domain on this GPU: wrap in-kernel      */
        MLB_Z_HALO = 1 };   /* z-slab: read the halo planes (filled by the
@@ -48,7 +51,7 @@ typedef struct mlb_plan mlb_plan;
 
 typedef struct {
     int32_t nx, ny, nz;   /* slab cells                                    */
-    int32_t itemsize;     /* 4 or 8                                        */
+    int32_t itemsize;     /* 4, 8 or 2 (storage dtype)                     */
     int64_t xp;           /* row pitch, elements                           */
     int64_t plane;        /* elements per z-plane = ny*xp                  */
     int64_t pop;          /* elements per population = (nz+2)*plane        */
@@ -75,8 +78,9 @@ int mlb_plan_get_layout(const mlb_plan *plan, mlb_layout *out);
 int mlb_plan_set_physics(mlb_plan *plan, double omega, const double wall_u[3],
                          double inlet_u);
 /* kernel variant used by mlb_step (tuning knob, never changes bits): 0 =
- * default, 32..512 = one cell per thread with that block width, 1008 / 1016 /
- * 1032 = 16-byte packs with 8 / 16 / 32 packs per warp row */
+ * default; 32..512 = one cell per thread with that block width; W*1000 + LX
+ * = packs of consecutive cells, LX = 8 / 16 / 32 packs per warp row, W = 1:
+ * 16-byte packs (fp32 / fp64), W = 2 / 3: 8- / 4-byte packs (fp16 storage) */
 int mlb_plan_set_variant(mlb_plan *plan, int variant);
 /* name of the fused kernel mlb_step will launch for this plan (for reports) */
 const char *mlb_plan_kernel_name(const mlb_plan *plan);

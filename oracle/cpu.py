@@ -46,7 +46,7 @@ def lib():
     global _lib
     if _lib is None:
         _lib = ctypes.CDLL(build())
-        for suf, real in (("f32", ctypes.c_float), ("f64", ctypes.c_double)):
+        for suf in ("f32", "f64", "h32"):
             fn = getattr(_lib, f"orc_step_{suf}")
             fn.restype = ctypes.c_int
             fn.argtypes = [ctypes.POINTER(Geom), ctypes.c_void_p, ctypes.c_void_p,
@@ -75,7 +75,9 @@ def _suffix(dtype):
         return "f32"
     if dtype == np.float64:
         return "f64"
-    raise ValueError(f"oracle handles float32/float64, got {dtype}")
+    if dtype == np.float16:
+        return "h32"  # half storage, single compute (the reference's MIXED1)
+    raise ValueError(f"oracle handles float16/float32/float64 storage, got {dtype}")
 
 
 def _ptr(a):
@@ -175,7 +177,10 @@ class SlabOracle(_Base):
 
 
 def equilibrium(rho, ux, uy, uz, dtype):
-    out = np.empty(19, dtype=dtype)
+    """Equilibrium in the COMPUTE dtype of a storage dtype (float32 for
+    float16 storage)."""
+    cdtype = np.float32 if np.dtype(dtype) == np.float16 else dtype
+    out = np.empty(19, dtype=cdtype)
     getattr(lib(), f"orc_equilibrium_{_suffix(dtype)}")(
         float(rho), float(ux), float(uy), float(uz), _ptr(out))
     return out

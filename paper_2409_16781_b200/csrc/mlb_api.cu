@@ -76,11 +76,12 @@ int layout_of(int nx, int ny, int nz, int dtype, mlb_layout *out)
 {
     if (nx < 1 || ny < 1 || nz < 1)
         return fail(MLB_EINVAL, "grid %dx%dx%d is empty", nx, ny, nz);
-    if (dtype != MLB_F32 && dtype != MLB_F64)
-        return fail(MLB_EINVAL, "unknown dtype code %d (0 = f32, 1 = f64)", dtype);
+    if (dtype != MLB_F32 && dtype != MLB_F64 && dtype != MLB_F16)
+        return fail(MLB_EINVAL, "unknown dtype code %d (0 = f32, 1 = f64, 2 = f16 storage / "
+                    "f32 compute)", dtype);
     if (ny > 65535 || nz > 65535)
         return fail(MLB_EUNSUPPORTED, "ny and nz are limited to 65535 per slab");
-    const int sz = dtype == MLB_F32 ? 4 : 8;
+    const int sz = dtype == MLB_F32 ? 4 : dtype == MLB_F64 ? 8 : 2;
     const long long line = 128 / sz;
     out->nx = nx; out->ny = ny; out->nz = nz; out->itemsize = sz;
     // experiment knobs (undocumented): extra row / population padding
@@ -160,24 +161,50 @@ void inlet_values(double u_in, T *e)
     e[0] = wr0 * um;
 }
 
-// the kernel `variant` resolves to for this plan (0 = auto)
-int resolve_variant(const mlb_plan *p)
+// Kernel variants (mlb_plan_set_variant).  0 = auto; 32..512 = one cell per
+// thread with that block width; W * 1000 + LX = packs of (16 >> (W - 1)) bytes
+// (W = 1: 16 B = 4 floats / 2 doubles; W = 2: 8 B = 4 halves; W = 3: 4 B =
+// 2 halves) with LX = 8 / 16 / 32 packs per warp row.
+int pack_cells(int dtype, int variant)
 {
-    const int V = p->dtype == MLB_F32 ? 4 : 2;
-    if (p->variant != 0)
-        return p->variant;
-    // measured on B200 (tools/sweep.py): packs win in fp32, not in fp64
-    return (p->dtype == MLB_F32 && p->nx % V == 0 && p->nx >= 128) ? 1016 : 128;
+    const int bytes = 16 >> (variant / 1000 - 1);
+    const int sz = dtype == MLB_F32 ? 4 : dtype == MLB_F64 ? 8 : 2;
+    return bytes / sz;
 }
 
-template <typename T>
-int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1,
-                cudaStream_t st)
+bool variant_exists(int dtype, int variant)
 {
-    mlb::StepArgs<T> a;
+    if (variant == 0 || variant == 32 || variant == 64 || variant == 128 || variant == 256
+        || variant == 512)
+        return true;
+    const int w = variant / 1000, lx = variant % 1000;
+    if (lx != 8 && lx != 16 && lx != 32)
+        return false;
+    if (dtype == MLB_F16)
+        return w == 2 || w == 3;
+    return w == 1;
+}
+
+// the kernel `variant` resolves to for this plan (0 = auto); measured on B200
+// with tools/sweep.py: packs win in fp32 and fp16 storage, not in fp64
+int resolve_variant(const mlb_plan *p)
+{
+    if (p->variant != 0)
+        return p->variant;
+    if (p->dtype == MLB_F32 && p->nx % 4 == 0 && p->nx >= 128)
+        return 1016;
+    if (p->dtype == MLB_F16 && p->nx % 4 == 0 && p->nx >= 128)
+        return 2008;
+    return 128;
+}
+
+template <typename TS>
+void fill_args(mlb_plan *p, const void *fpre, void *fpost, int z0, mlb::StepArgs<TS> &a)
+{
+    using T = typename mlb::Store<TS>::C;
     for (int q = 0; q < MLB_Q; ++q) {
-        a.pre[q] = static_cast<const T *>(fpre) + (long long)q * p->lay.pop;
-        a.post[q] = static_cast<T *>(fpost) + (long long)q * p->lay.pop;
+        a.pre[q] = static_cast<const TS *>(fpre) + (long long)q * p->lay.pop;
+        a.post[q] = static_cast<TS *>(fpost) + (long long)q * p->lay.pop;
     }
     a.cls = p->d_cls;
     a.mlinks = p->d_mlinks;
@@ -186,47 +213,78 @@ int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1,
     a.passthrough = p->passthrough;
     a.omega = T(p->omega);
     wall_terms<T>(p->wall_u, a.k);
-    // variant: 0 = auto; 32..512 = one cell per thread with that block width;
-    // 1008 / 1016 / 1032 = 16-byte packs (4 floats / 2 doubles), 8 / 16 / 32
-    // packs per warp row
-    constexpr int V = mlb::Vec<T>::V;
-    const int variant = resolve_variant(p);
-    if (variant >= 1000) {
-        if (p->nx % V != 0)
-            return fail(MLB_EINVAL, "the vectorised kernel needs nx %% %d == 0", V);
-        const int lx = variant - 1000;
-        const int rows = 128 / lx;  // rows per 128-thread block
-        const dim3 grid((p->nx / V + lx - 1) / lx, (p->ny + rows - 1) / rows, z1 - z0);
-        if (lx == 8) mlb::step_vec_kernel<T, 8><<<grid, 128, 0, st>>>(a);
-        else if (lx == 16) mlb::step_vec_kernel<T, 16><<<grid, 128, 0, st>>>(a);
-        else mlb::step_vec_kernel<T, 32><<<grid, 128, 0, st>>>(a);
-        MLB_LAUNCHED();
-        return MLB_OK;
-    }
-    int bx = variant;
+}
+
+template <typename TS, int V>
+int launch_vec(mlb_plan *p, const mlb::StepArgs<TS> &a, int lx, int nplanes, cudaStream_t st)
+{
+    if (p->nx % V != 0)
+        return fail(MLB_EINVAL, "this vectorised kernel needs nx %% %d == 0", V);
+    const int rows = 128 / lx;  // rows per 128-thread block
+    const dim3 grid((p->nx / V + lx - 1) / lx, (p->ny + rows - 1) / rows, nplanes);
+    if (lx == 8) mlb::step_vec_kernel<TS, V, 8><<<grid, 128, 0, st>>>(a);
+    else if (lx == 16) mlb::step_vec_kernel<TS, V, 16><<<grid, 128, 0, st>>>(a);
+    else mlb::step_vec_kernel<TS, V, 32><<<grid, 128, 0, st>>>(a);
+    MLB_LAUNCHED();
+    return MLB_OK;
+}
+
+template <typename TS>
+int launch_scalar(mlb_plan *p, const mlb::StepArgs<TS> &a, int bx, int nplanes, cudaStream_t st)
+{
     while (bx > 32 && bx / 2 >= p->nx)
         bx /= 2;
-    const dim3 grid((p->nx + bx - 1) / bx, p->ny, z1 - z0);
+    const dim3 grid((p->nx + bx - 1) / bx, p->ny, nplanes);
     switch (bx) {
-    case 32: mlb::step_kernel<T, 32><<<grid, 32, 0, st>>>(a); break;
-    case 64: mlb::step_kernel<T, 64><<<grid, 64, 0, st>>>(a); break;
-    case 128: mlb::step_kernel<T, 128><<<grid, 128, 0, st>>>(a); break;
-    case 256: mlb::step_kernel<T, 256><<<grid, 256, 0, st>>>(a); break;
-    case 512: mlb::step_kernel<T, 512><<<grid, 512, 0, st>>>(a); break;
-    default: return fail(MLB_EINVAL, "variant %d is not a block width", p->variant);
+    case 32: mlb::step_kernel<TS, 32><<<grid, 32, 0, st>>>(a); break;
+    case 64: mlb::step_kernel<TS, 64><<<grid, 64, 0, st>>>(a); break;
+    case 128: mlb::step_kernel<TS, 128><<<grid, 128, 0, st>>>(a); break;
+    case 256: mlb::step_kernel<TS, 256><<<grid, 256, 0, st>>>(a); break;
+    default: mlb::step_kernel<TS, 512><<<grid, 512, 0, st>>>(a); break;
     }
     MLB_LAUNCHED();
     return MLB_OK;
 }
 
+int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cudaStream_t st)
+{
+    const int variant = resolve_variant(p);
+    if (!variant_exists(p->dtype, variant))
+        return fail(MLB_EINVAL, "kernel variant %d does not exist for dtype code %d", variant,
+                    p->dtype);
+    const int lx = variant % 1000, n = z1 - z0;
+    if (p->dtype == MLB_F32) {
+        mlb::StepArgs<float> a;
+        fill_args<float>(p, fpre, fpost, z0, a);
+        return variant >= 1000 ? launch_vec<float, 4>(p, a, lx, n, st)
+                               : launch_scalar<float>(p, a, variant, n, st);
+    }
+    if (p->dtype == MLB_F64) {
+        mlb::StepArgs<double> a;
+        fill_args<double>(p, fpre, fpost, z0, a);
+        return variant >= 1000 ? launch_vec<double, 2>(p, a, lx, n, st)
+                               : launch_scalar<double>(p, a, variant, n, st);
+    }
+    mlb::StepArgs<__half> a;
+    fill_args<__half>(p, fpre, fpost, z0, a);
+    if (variant >= 3000) return launch_vec<__half, 2>(p, a, lx, n, st);
+    if (variant >= 2000) return launch_vec<__half, 4>(p, a, lx, n, st);
+    return launch_scalar<__half>(p, a, variant, n, st);
+}
+
 template <typename T>
 int launch_open(mlb_plan *p, void *fpost, int z0, int z1, cudaStream_t st)
 {
+    using C = typename mlb::Store<T>::C;
     T *f = static_cast<T *>(fpost);
     const long long i0 = p->in_zoff[z0], i1 = p->in_zoff[z1];
     if (i1 > i0) {
+        // computed in compute dtype, stored in storage dtype (engine.py:167-171)
+        C cv[MLB_Q];
+        inlet_values<C>(p->inlet_u, cv);
         mlb::InletVals<T> v;
-        inlet_values<T>(p->inlet_u, v.v);
+        for (int q = 0; q < MLB_Q; ++q)
+            v.v[q] = mlb::Store<T>::down(cv[q]);
         const long long n = i1 - i0;
         mlb::inlet_kernel<T><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
             f, p->d_in + i0, n, p->lay.pop, v);
@@ -382,10 +440,10 @@ int mlb_plan_set_physics(mlb_plan *p, double omega, const double wall_u[3], doub
 int mlb_plan_set_variant(mlb_plan *p, int variant)
 {
     if (int rc = check_plan(p, false)) return rc;
-    if (variant != 0 && variant != 32 && variant != 64 && variant != 128 && variant != 256
-        && variant != 512 && variant != 1008 && variant != 1016 && variant != 1032)
-        return fail(MLB_EINVAL, "variant must be 0 (auto), a block width in {32,64,128,256,512} "
-                    "(one cell per thread) or 1008/1016/1032 (16-byte packs)");
+    if (!variant_exists(p->dtype, variant))
+        return fail(MLB_EINVAL, "variant %d: must be 0 (auto), a block width in {32,64,128,256,"
+                    "512} (one cell per thread), or W*1000 + {8,16,32} with W = 1 (16-byte packs, "
+                    "fp32/fp64), 2 or 3 (8- / 4-byte packs, fp16 storage)", variant);
     p->variant = variant;
     return MLB_OK;
 }
@@ -395,9 +453,10 @@ const char *mlb_plan_kernel_name(const mlb_plan *p)
     static thread_local char name[64];
     if (!p) return "";
     const int v = resolve_variant(p);
-    const char *t = p->dtype == MLB_F32 ? "float" : "double";
+    const char *t = p->dtype == MLB_F32 ? "float" : p->dtype == MLB_F64 ? "double" : "__half";
     if (v >= 1000)
-        snprintf(name, sizeof(name), "mlb::step_vec_kernel<%s, %d>", t, v - 1000);
+        snprintf(name, sizeof(name), "mlb::step_vec_kernel<%s, %d, %d>", t,
+                 pack_cells(p->dtype, v), v % 1000);
     else
         snprintf(name, sizeof(name), "mlb::step_kernel<%s, %d>", t, v);
     return name;
@@ -554,8 +613,7 @@ int mlb_step_range(mlb_plan *p, const void *d_fpre, void *d_fpost, int z0, int z
         return fail(MLB_EINVAL, "plane range [%d, %d) outside [0, %d)", z0, z1, p->nz);
     if (z0 == z1) return MLB_OK;
     MLB_CUDA(cudaSetDevice(p->device));
-    return p->dtype == MLB_F32 ? launch_step<float>(p, d_fpre, d_fpost, z0, z1, S(stream))
-                               : launch_step<double>(p, d_fpre, d_fpost, z0, z1, S(stream));
+    return launch_step(p, d_fpre, d_fpost, z0, z1, S(stream));
 }
 
 int mlb_step(mlb_plan *p, const void *d_fpre, void *d_fpost, void *stream)
@@ -572,8 +630,9 @@ int mlb_open_pass_range(mlb_plan *p, void *d_fpost, int z0, int z1, void *stream
         return fail(MLB_EINVAL, "plane range [%d, %d) outside [0, %d)", z0, z1, p->nz);
     if (p->n_in == 0 && p->n_out == 0) return MLB_OK;
     MLB_CUDA(cudaSetDevice(p->device));
-    return p->dtype == MLB_F32 ? launch_open<float>(p, d_fpost, z0, z1, S(stream))
-                               : launch_open<double>(p, d_fpost, z0, z1, S(stream));
+    if (p->dtype == MLB_F32) return launch_open<float>(p, d_fpost, z0, z1, S(stream));
+    if (p->dtype == MLB_F64) return launch_open<double>(p, d_fpost, z0, z1, S(stream));
+    return launch_open<__half>(p, d_fpost, z0, z1, S(stream));
 }
 
 int mlb_open_pass(mlb_plan *p, void *d_fpost, void *stream)
@@ -640,9 +699,12 @@ int mlb_macro(const mlb_plan *p, const void *d_f, double *d_rho, double *d_ux, d
     if (p->dtype == MLB_F32)
         mlb::macro_kernel<float><<<grid, 128, 0, S(stream)>>>(
             static_cast<const float *>(d_f), p->g, d_rho, d_ux, d_uy, d_uz);
-    else
+    else if (p->dtype == MLB_F64)
         mlb::macro_kernel<double><<<grid, 128, 0, S(stream)>>>(
             static_cast<const double *>(d_f), p->g, d_rho, d_ux, d_uy, d_uz);
+    else
+        mlb::macro_kernel<__half><<<grid, 128, 0, S(stream)>>>(
+            static_cast<const __half *>(d_f), p->g, d_rho, d_ux, d_uy, d_uz);
     MLB_LAUNCHED();
     return MLB_OK;
 }
@@ -655,9 +717,12 @@ int mlb_diagnostics(mlb_plan *p, const void *d_f, double h_out[8], void *stream)
     if (p->dtype == MLB_F32)
         mlb::diag_kernel<float><<<p->diag_blocks, mlb::DIAG_THREADS, 0, S(stream)>>>(
             static_cast<const float *>(d_f), p->d_cls, p->g, p->d_partials);
-    else
+    else if (p->dtype == MLB_F64)
         mlb::diag_kernel<double><<<p->diag_blocks, mlb::DIAG_THREADS, 0, S(stream)>>>(
             static_cast<const double *>(d_f), p->d_cls, p->g, p->d_partials);
+    else
+        mlb::diag_kernel<__half><<<p->diag_blocks, mlb::DIAG_THREADS, 0, S(stream)>>>(
+            static_cast<const __half *>(d_f), p->d_cls, p->g, p->d_partials);
     MLB_LAUNCHED();
     mlb::diag_final_kernel<<<1, mlb::DIAG_THREADS, 0, S(stream)>>>(p->d_partials,
                                                                   p->diag_blocks, p->d_diag);
@@ -679,8 +744,11 @@ int mlb_probe(const mlb_plan *p, const void *d_f, int x, int y, int lz, double *
     if (p->dtype == MLB_F32)
         mlb::probe_kernel<float><<<1, 1, 0, S(stream)>>>(static_cast<const float *>(d_f),
                                                          p->g, x, y, lz, d_out4);
-    else
+    else if (p->dtype == MLB_F64)
         mlb::probe_kernel<double><<<1, 1, 0, S(stream)>>>(static_cast<const double *>(d_f),
+                                                          p->g, x, y, lz, d_out4);
+    else
+        mlb::probe_kernel<__half><<<1, 1, 0, S(stream)>>>(static_cast<const __half *>(d_f),
                                                           p->g, x, y, lz, d_out4);
     MLB_LAUNCHED();
     return MLB_OK;

@@ -14,11 +14,33 @@
 // 11..14 = (+x+z),(-x+z),(-x-z),(+x-z); 15..18 = (+y+z),(-y+z),(-y-z),(+y-z).
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace mlb {
 
 constexpr int Q = 19;
+
+// Storage type TS -> compute type and the two conversions.  float and double
+// compute in their own type; __half is the reference's MIXED1 mode
+// (fields.py:24): stored as binary16, upcast exactly on load, computed in
+// float, rounded to nearest even on store (kernels.py:435-455).
+template <typename TS> struct Store;
+template <> struct Store<float> {
+    using C = float;
+    static __host__ __device__ __forceinline__ float up(float v) { return v; }
+    static __host__ __device__ __forceinline__ float down(float v) { return v; }
+};
+template <> struct Store<double> {
+    using C = double;
+    static __host__ __device__ __forceinline__ double up(double v) { return v; }
+    static __host__ __device__ __forceinline__ double down(double v) { return v; }
+};
+template <> struct Store<__half> {
+    using C = float;
+    static __host__ __device__ __forceinline__ float up(__half v) { return __half2float(v); }
+    static __host__ __device__ __forceinline__ __half down(float v) { return __float2half_rn(v); }
+};
 
 struct Geom {
     int nx, ny, nz;          // slab cells
@@ -26,13 +48,14 @@ struct Geom {
     long long xp, plane, pop;  // row pitch, z-plane, population strides (elements)
 };
 
-template <typename T>
+template <typename TS>
 struct StepArgs {
+    using T = typename Store<TS>::C;  // compute type
     // one base pointer per population (host-computed: keeps the 64-bit
     // q * pop products out of the kernel; an address is then a single
     // IMAD.WIDE of a 32-bit in-population offset onto a constant-bank base)
-    const T *pre[Q];
-    T *post[Q];
+    const TS *pre[Q];
+    TS *post[Q];
     const uint32_t *__restrict__ cls;     // per-cell class word, see below
     const uint32_t *__restrict__ mlinks;  // per-cell moving-wall link bits (rarely read)
     Geom g;
@@ -137,10 +160,11 @@ __host__ __device__ constexpr int opp(int i)
 //  * wall-adjacent lanes patch their bounced directions afterwards from the
 //    link bits of the class word - no flag reads, no 3-way branches; the
 //    patch loads hit lines the same warp has just pulled.
-template <typename T>
-__device__ __forceinline__ void step_cell(const StepArgs<T> &a, const int x, const int y,
+template <typename TS>
+__device__ __forceinline__ void step_cell(const StepArgs<TS> &a, const int x, const int y,
                                           const int lz)
 {
+    using T = typename Store<TS>::C;
     const Geom &gm = a.g;
     const int xp = (int)gm.xp, plane = (int)gm.plane;
 
@@ -158,8 +182,8 @@ __device__ __forceinline__ void step_cell(const StepArgs<T> &a, const int x, con
 
     const uint32_t cd = a.cls[d];
     T g[Q];
-    g[0] = a.pre[0][d];
-#define MLB_PULL(i, zz, rr, dd) g[i] = a.pre[i][(dd) + ((zz) + (rr))];
+    g[0] = Store<TS>::up(a.pre[0][d]);
+#define MLB_PULL(i, zz, rr, dd) g[i] = Store<TS>::up(a.pre[i][(dd) + ((zz) + (rr))]);
     MLB_PULL(1, zc, rc, dm)  MLB_PULL(2, zc, rm, dc)  MLB_PULL(3, zc, rc, dq)
     MLB_PULL(4, zc, rq, dc)  MLB_PULL(5, zc, rm, dm)  MLB_PULL(6, zc, rm, dq)
     MLB_PULL(7, zc, rq, dq)  MLB_PULL(8, zc, rq, dm)  MLB_PULL(9, zm, rc, dc)
@@ -189,35 +213,37 @@ __device__ __forceinline__ void step_cell(const StepArgs<T> &a, const int x, con
 #pragma unroll
             for (int i = 1; i < Q; ++i)
                 if (cd & cls_link(i)) {
-                    const T c = a.pre[opp(i)][d];
+                    const T c = Store<TS>::up(a.pre[opp(i)][d]);
                     g[i] = (mv & (1u << i)) ? c + a.k[i] : c;
                 }
         }
         collide<T>(g, a.omega);
     } else {
         // pass-through: the pulled values are neighbours', not this cell's
+        // (storage -> compute -> storage is exact in every mode)
 #pragma unroll
         for (int i = 1; i < Q; ++i)
-            g[i] = a.pre[i][d];
+            g[i] = Store<TS>::up(a.pre[i][d]);
     }
 
 #pragma unroll
     for (int i = 0; i < Q; ++i)
-        a.post[i][d] = g[i];
+        a.post[i][d] = Store<TS>::down(g[i]);
 }
 
-template <typename T, int BX>
-__global__ void __launch_bounds__(BX) step_kernel(const StepArgs<T> a)
+template <typename TS, int BX>
+__global__ void __launch_bounds__(BX) step_kernel(const StepArgs<TS> a)
 {
     const int x = blockIdx.x * BX + threadIdx.x;
     if (x >= a.g.nx)
         return;
-    step_cell<T>(a, x, blockIdx.y, a.z0 + blockIdx.z);
+    step_cell<TS>(a, x, blockIdx.y, a.z0 + blockIdx.z);
 }
 
 // ---------------------------------------------------------------------------
-// Vectorised variant: each thread owns a PACK of V = 16 / sizeof(T)
-// consecutive cells in x (one 16-byte word per population); a warp covers LX
+// Vectorised variant: each thread owns a PACK of V consecutive cells in x
+// (one 16-byte word per population in fp32 / fp64, 8 or 4 bytes in fp16
+// storage); a warp covers LX
 // packs in x by 32 / LX rows in y.  Per pack and population: one aligned
 // 16-byte load; the ten populations with c_x = +-1 need the word shifted by
 // one cell, which costs one extra scalar load of the element just outside
@@ -226,42 +252,73 @@ __global__ void __launch_bounds__(BX) step_kernel(const StepArgs<T> a)
 // Same early-issue and link-bit patching as the scalar kernel.  Kept as a
 // selectable variant: at 512^3 it measures within 2 % of the scalar kernel
 // (fewer instructions per cell, but 3x the registers per thread).
-template <typename T, int V> struct Pack;
-template <> struct Pack<float, 4>  { using type = float4;  using ctype = uint4; };
-template <> struct Pack<double, 2> { using type = double2; using ctype = uint2; };
-template <typename T> struct Vec { static constexpr int V = 16 / (int)sizeof(T); };
-
-__device__ __forceinline__ void unpack(const float4 &v, float (&o)[4])
-{ o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
-__device__ __forceinline__ void unpack(const double2 &v, double (&o)[2])
-{ o[0] = v.x; o[1] = v.y; }
-__device__ __forceinline__ void unpack(const uint4 &v, uint32_t (&o)[4])
-{ o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
-__device__ __forceinline__ void unpack(const uint2 &v, uint32_t (&o)[2])
-{ o[0] = v.x; o[1] = v.y; }
-__device__ __forceinline__ float4 pack(const float (&o)[4]) { return make_float4(o[0], o[1], o[2], o[3]); }
-__device__ __forceinline__ double2 pack(const double (&o)[2]) { return make_double2(o[0], o[1]); }
+// pack loads / stores: V consecutive storage elements <-> V compute values
+template <typename TS, int V> struct PackIO;
+template <> struct PackIO<float, 4> {
+    static __device__ __forceinline__ void load(const float *p, float (&o)[4])
+    { const float4 v = *reinterpret_cast<const float4 *>(p); o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+    static __device__ __forceinline__ void store(float *p, const float (&o)[4])
+    { *reinterpret_cast<float4 *>(p) = make_float4(o[0], o[1], o[2], o[3]); }
+};
+template <> struct PackIO<double, 2> {
+    static __device__ __forceinline__ void load(const double *p, double (&o)[2])
+    { const double2 v = *reinterpret_cast<const double2 *>(p); o[0] = v.x; o[1] = v.y; }
+    static __device__ __forceinline__ void store(double *p, const double (&o)[2])
+    { *reinterpret_cast<double2 *>(p) = make_double2(o[0], o[1]); }
+};
+template <> struct PackIO<__half, 2> {
+    static __device__ __forceinline__ void load(const __half *p, float (&o)[2])
+    { const __half2 v = *reinterpret_cast<const __half2 *>(p); o[0] = __low2float(v); o[1] = __high2float(v); }
+    static __device__ __forceinline__ void store(__half *p, const float (&o)[2])
+    { *reinterpret_cast<__half2 *>(p) = __floats2half2_rn(o[0], o[1]); }
+};
+template <> struct PackIO<__half, 4> {
+    static __device__ __forceinline__ void load(const __half *p, float (&o)[4])
+    {
+        const uint2 u = *reinterpret_cast<const uint2 *>(p);
+        const __half2 a = *reinterpret_cast<const __half2 *>(&u.x);
+        const __half2 b = *reinterpret_cast<const __half2 *>(&u.y);
+        o[0] = __low2float(a); o[1] = __high2float(a); o[2] = __low2float(b); o[3] = __high2float(b);
+    }
+    static __device__ __forceinline__ void store(__half *p, const float (&o)[4])
+    {
+        const __half2 a = __floats2half2_rn(o[0], o[1]), b = __floats2half2_rn(o[2], o[3]);
+        uint2 u;
+        u.x = *reinterpret_cast<const unsigned *>(&a);
+        u.y = *reinterpret_cast<const unsigned *>(&b);
+        *reinterpret_cast<uint2 *>(p) = u;
+    }
+};
+// the class words of a pack
+template <int V> struct ClsIO;
+template <> struct ClsIO<2> {
+    static __device__ __forceinline__ void load(const uint32_t *p, uint32_t (&o)[2])
+    { const uint2 v = *reinterpret_cast<const uint2 *>(p); o[0] = v.x; o[1] = v.y; }
+};
+template <> struct ClsIO<4> {
+    static __device__ __forceinline__ void load(const uint32_t *p, uint32_t (&o)[4])
+    { const uint4 v = *reinterpret_cast<const uint4 *>(p); o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+};
 
 // The V values pulled along a direction with x component CX from the row
 // starting at `row` (already offset to population, plane and row).
-template <typename T, int V, int CX>
-__device__ __forceinline__ void pull_pack(const T *__restrict__ row, int x0, int xl, int xr,
-                                          T (&o)[V])
+template <typename TS, int V, int CX>
+__device__ __forceinline__ void pull_pack(const TS *__restrict__ row, int x0, int xl, int xr,
+                                          typename Store<TS>::C (&o)[V])
 {
-    using VT = typename Pack<T, V>::type;
-    T w[V];
-    unpack(*reinterpret_cast<const VT *>(row + x0), w);
+    typename Store<TS>::C w[V];
+    PackIO<TS, V>::load(row + x0, w);
     if (CX == 0) {
 #pragma unroll
         for (int j = 0; j < V; ++j) o[j] = w[j];
     } else if (CX > 0) {  // source x - 1
-        o[0] = row[xl];
+        o[0] = Store<TS>::up(row[xl]);
 #pragma unroll
         for (int j = 1; j < V; ++j) o[j] = w[j - 1];
     } else {              // source x + 1
 #pragma unroll
         for (int j = 0; j < V - 1; ++j) o[j] = w[j + 1];
-        o[V - 1] = row[xr];
+        o[V - 1] = Store<TS>::up(row[xr]);
     }
 }
 
@@ -273,12 +330,10 @@ __device__ __forceinline__ void pull_pack(const T *__restrict__ row, int x0, int
     X(13, -1, zq, rc) X(14, 1, zq, rc)  X(15, 0, zm, rm)  X(16, 0, zm, rq)       \
     X(17, 0, zq, rq)  X(18, 0, zq, rm)
 
-template <typename T, int LX>
-__global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<T> a)
+template <typename TS, int V, int LX>
+__global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a)
 {
-    constexpr int V = Vec<T>::V;
-    using VT = typename Pack<T, V>::type;
-    using CT = typename Pack<T, V>::ctype;
+    using T = typename Store<TS>::C;
     constexpr int RPW = 32 / LX;        // rows per warp
     const Geom &gm = a.g;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -301,10 +356,10 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<T> a)
 
     // class words of the pack and all pulls, issued together
     uint32_t c[V];
-    unpack(*reinterpret_cast<const CT *>(a.cls + d), c);
+    ClsIO<V>::load(a.cls + d, c);
     T g[Q][V];
-    unpack(*reinterpret_cast<const VT *>(a.pre[0] + d), g[0]);
-#define MLB_X(i, CX, Z, R) pull_pack<T, V, CX>(a.pre[i] + ((Z) + (R)), x0, xl, xr, g[i]);
+    PackIO<TS, V>::load(a.pre[0] + d, g[0]);
+#define MLB_X(i, CX, Z, R) pull_pack<TS, V, CX>(a.pre[i] + ((Z) + (R)), x0, xl, xr, g[i]);
     MLB_DIRS(MLB_X)
 #undef MLB_X
 
@@ -329,7 +384,7 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<T> a)
         for (int i = 1; i < Q; ++i)
             if (call & cls_link(i)) {
                 T o[V];
-                unpack(*reinterpret_cast<const VT *>(a.pre[opp(i)] + d), o);
+                PackIO<TS, V>::load(a.pre[opp(i)] + d, o);
 #pragma unroll
                 for (int j = 0; j < V; ++j)
                     if (c[j] & cls_link(i))
@@ -353,7 +408,7 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<T> a)
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
             T o[V];
-            unpack(*reinterpret_cast<const VT *>(a.pre[i] + d), o);
+            PackIO<TS, V>::load(a.pre[i] + d, o);
 #pragma unroll
             for (int j = 0; j < V; ++j)
                 if ((c[j] & CLS_FLAG) != 0)
@@ -363,14 +418,14 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<T> a)
     if (allfluid || a.passthrough) {
 #pragma unroll
         for (int i = 0; i < Q; ++i)
-            *reinterpret_cast<VT *>(a.post[i] + d) = pack(g[i]);
+            PackIO<TS, V>::store(a.post[i] + d, g[i]);
     } else {
 #pragma unroll
         for (int j = 0; j < V; ++j)
             if ((c[j] & CLS_FLAG) == 0) {
 #pragma unroll
                 for (int i = 0; i < Q; ++i)
-                    a.post[i][d + j] = g[i][j];
+                    a.post[i][d + j] = Store<TS>::down(g[i][j]);
             }
     }
 }
@@ -512,7 +567,7 @@ __device__ __forceinline__ void cell_moments(const T *__restrict__ f, long long 
     double v[Q];
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
-        v[i] = (double)f[(long long)i * pop + d];
+        v[i] = (double)Store<T>::up(f[(long long)i * pop + d]);
         if (bad && !isfinite(v[i]))
             ++*bad;
     }

@@ -199,8 +199,10 @@ class KernelPlan:
 
     def set_variant(self, variant):
         """Kernel variant (tuning knob, never changes bits): 0 = auto,
-        32..512 = one cell per thread with that block width, 1008 / 1016 /
-        1032 = vectorised kernel with 8 / 16 / 32 packs per warp row."""
+        32..512 = one cell per thread with that block width, W*1000 + LX =
+        packs of cells (W = 1: 16-byte packs for fp32/fp64, W = 2 / 3: 8- /
+        4-byte packs for fp16 storage) with LX = 8 / 16 / 32 packs per warp
+        row (include/mlb.h)."""
         _cabi.check(self._lib.mlb_plan_set_variant(self._plan, int(variant)))
 
     set_block_width = set_variant
@@ -315,7 +317,8 @@ class KernelPlan:
 
 
 def _torch_dtype(precision):
-    return torch.float32 if precision is Precision.SINGLE else torch.float64
+    return {Precision.SINGLE: torch.float32, Precision.DOUBLE: torch.float64,
+            Precision.MIXED1: torch.float16}[precision]
 
 
 def pinned_empty(shape, dtype):
@@ -325,6 +328,7 @@ def pinned_empty(shape, dtype):
     if torch.cuda.is_available():
         tdt = {np.dtype(np.float32): torch.float32,
                np.dtype(np.float64): torch.float64,
+               np.dtype(np.float16): torch.float16,
                np.dtype(np.uint8): torch.uint8}[dtype]
         return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
     return np.empty(shape, dtype=dtype)

@@ -39,7 +39,7 @@ def flops_per_cell(precision=None):
 
 def bytes_per_cell(precision):
     """Ideal memory traffic per cell update: 19 planes read + 19 written in
-    storage precision (152 B in fp32, 304 B in fp64)."""
+    storage precision (152 B in fp32, 304 B in fp64, 76 B in mixed1)."""
     if not isinstance(precision, Precision):
         precision = Precision.from_token(precision)
     return 2 * Q * precision.storage.itemsize

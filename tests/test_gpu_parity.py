@@ -17,7 +17,10 @@ from .helpers import (extrude_mask, from_xyzq, geometries3d, lift_2d,
 
 pytestmark = pytest.mark.gpu
 
-PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE}
+PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED1}
+VARIANTS = {"f32": [32, 64, 128, 256, 512, 1008, 1016, 1032],
+            "f64": [32, 64, 128, 256, 512, 1008, 1016, 1032],
+            "f16": [32, 128, 512, 2008, 2016, 2032, 3008, 3016, 3032]}
 
 
 def make_plan(grid, prec, omega, wall_u, inlet_u=0.0, **kw):
@@ -32,7 +35,7 @@ def make_oracle(grid, omega, wall_u, inlet_u=0.0):
     return CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u, inlet_u)
 
 
-@pytest.mark.parametrize("tag", ["f64", "f32"])
+@pytest.mark.parametrize("tag", ["f64", "f32", "f16"])
 @pytest.mark.parametrize("geom", list(geometries3d()))
 def test_one_step_bitwise(geom, tag, rng):
     grid, wall_u, inlet_u = geometries3d()[geom]
@@ -61,7 +64,7 @@ def test_one_step_matches_naive_oracle(geom, rng):
     np.testing.assert_allclose(to_xyzq(got, nx, ny, nz), want, rtol=1e-12, atol=1e-15)
 
 
-@pytest.mark.parametrize("tag", ["f64", "f32"])
+@pytest.mark.parametrize("tag", ["f64", "f32", "f16"])
 @pytest.mark.parametrize("geom", list(geometries3d()))
 def test_multi_step_with_open_pass_bitwise(geom, tag, rng):
     grid, wall_u, inlet_u = geometries3d()[geom]
@@ -84,8 +87,7 @@ VEC_GEOMS = ["cavity16", "channel40", "periodic8", "wide", "duct"]
 
 
 @pytest.mark.parametrize("passthrough", [False, True])
-@pytest.mark.parametrize("variant", [32, 64, 128, 256, 512, 1008, 1016, 1032])
-@pytest.mark.parametrize("tag", ["f64", "f32"])
+@pytest.mark.parametrize("tag,variant", [(t, v) for t in VARIANTS for v in VARIANTS[t]])
 @pytest.mark.parametrize("geom", VEC_GEOMS)
 def test_kernel_variants_never_change_bits(geom, tag, variant, passthrough, rng):
     """Block shape, vectorisation and the store mode are pure performance
@@ -156,7 +158,7 @@ def test_flags_byte_identical(rng):
         np.testing.assert_array_equal(plan.device_flags(), B.flatten_mask(grid))
 
 
-@pytest.mark.parametrize("tag", ["f64", "f32"])
+@pytest.mark.parametrize("tag", ["f64", "f32", "f16"])
 def test_macro_bitwise_and_diagnostics(tag, rng):
     grid, wall_u, inlet_u = geometries3d()["channel"]
     prec = PREC[tag]
@@ -174,7 +176,7 @@ def test_macro_bitwise_and_diagnostics(tag, rng):
         assert gd[key] == pytest.approx(wd[key], rel=1e-12, abs=1e-12), key
     assert gd["fluid_cells"] == np.count_nonzero(grid == 0)
     f[3, 17] = np.nan
-    f[11, 5] = np.inf
+    f[11, 5] = np.inf  # (both representable in every storage dtype)
     plan.upload(f, d)
     assert plan.diagnostics(d)["nonfinite"] == 2
 

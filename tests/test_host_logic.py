@@ -19,7 +19,9 @@ class TestFields:
         assert (Precision.SINGLE.code, Precision.DOUBLE.code) == (0, 1)
         assert Precision.from_token("double") is Precision.DOUBLE
         assert Precision.from_code(0) is Precision.SINGLE
-        for bad in ("mixed1", "half"):
+        assert Precision.MIXED1.storage == np.float16 and Precision.MIXED1.compute == np.float32
+        assert Precision.from_code(2) is Precision.MIXED1  # the reference's wire code
+        for bad in ("mixed2", "half"):
             with pytest.raises(ValueError, match="precision"):
                 Precision.from_token(bad)
 
@@ -152,6 +154,7 @@ class TestPerfport:
     def test_cost_model(self):
         assert perfport.bytes_per_cell(Precision.SINGLE) == 152
         assert perfport.bytes_per_cell("double") == 304
+        assert perfport.bytes_per_cell(Precision.MIXED1) == 76
         assert perfport.arithmetic_intensity(195, 152) == pytest.approx(1.2829, rel=1e-4)
         assert perfport.mlups(512, 512, 512, 10, 0.5) == pytest.approx(2684.35456)
         with pytest.raises(ValueError):

@@ -174,6 +174,35 @@ class TestInvariants:
         assert d["max_u"] == pytest.approx((np.sqrt((m ** 2).sum(0)) / rho)[fluid].max(), rel=1e-13)
 
 
+class TestMixed1Storage:
+    @pytest.mark.parametrize("geom", ["cavity_oblique_lid", "channel40", "periodic8"])
+    def test_half_storage_is_the_float_kernel_between_two_casts(self, geom, rng):
+        """The reference defines MIXED1 through float32 bridge planes
+        (kernels.py:447-455): f16 -> f32 is exact, the float kernel runs,
+        f32 -> f16 rounds to nearest.  The half-storage oracle must equal
+        exactly that, step after step, never-written cells included."""
+        grid, wall_u, inlet_u = geometries3d()[geom]
+        orc = oracle_for(grid, 1.3, wall_u, inlet_u)
+        f16 = random_block(rng, grid.size, np.float16)
+        a, b = f16.copy(), random_block(rng, grid.size, np.float16)
+        a32, b32 = a.astype(np.float32), b.astype(np.float32)
+        for _ in range(4):
+            orc.step(a, b)
+            orc.open_pass(b)
+            orc.step(a32, b32)
+            orc.open_pass(b32)
+            b32 = b32.astype(np.float16).astype(np.float32)  # the bridge's store + reload
+            np.testing.assert_array_equal(b, b32.astype(np.float16))
+            a, b, a32, b32 = b, a, b32, a32
+
+    def test_macro_upcasts_exactly(self, rng):
+        grid, wall_u, inlet_u = geometries3d()["periodic8"]
+        orc = oracle_for(grid, 1.0, wall_u)
+        f16 = random_block(rng, grid.size, np.float16)
+        for got, want in zip(orc.macro(f16), orc.macro(f16.astype(np.float64))):
+            np.testing.assert_array_equal(got, want)
+
+
 # ---- 3. the independent naive oracle on 3-D geometries ----------------------
 class TestAgainstNaiveOracle:
     @pytest.mark.parametrize("geom", list(geometries3d()))
