@@ -135,6 +135,20 @@ int mlb_open_pass_range(mlb_plan *plan, void *d_fpost, int z0, int z1,
 int mlb_run_steps(mlb_plan *plan, void *d_a, void *d_b, int nsteps,
                   void *stream, float *ms);
 
+/* ---- in-place update ("AA pattern"): one population block instead of two ---
+ * Same arithmetic and the same 2 x 19 x itemsize bytes per update as
+ * mlb_run_steps, half the footprint (1024^3 fp32 = 82 GB fits one B200).
+ * The block alternates between the normal representation (*repr == 0: what
+ * mlb_upload writes and mlb_download / mlb_macro / mlb_diagnostics expect)
+ * and a shifted one (*repr == 1) after an odd number of steps;
+ * mlb_inplace_normalize brings it back to 0 without stepping.  *repr is
+ * updated by both calls.  Walls only: plans whose flags contain INLET /
+ * OUTLET cells, and MLB_Z_HALO plans, are rejected (MLB_EUNSUPPORTED).
+ * Non-fluid cells are never modified. */
+int mlb_run_steps_inplace(mlb_plan *plan, void *d_f, int nsteps, int *repr,
+                          void *stream, float *ms);
+int mlb_inplace_normalize(mlb_plan *plan, void *d_f, int *repr, void *stream);
+
 /* ---- z-slab halo exchange ----------------------------------
  * Copies the 5 crossing populations of one boundary plane of d_src (a
  * population block of a slab with the same nx, ny, dtype; possibly on a

@@ -27,6 +27,7 @@ SYMBOLS = (
     "mlb_plan_kernel_name", "mlb_plan_set_flags",
     "mlb_plan_get_flags", "mlb_upload", "mlb_download", "mlb_step",
     "mlb_step_range", "mlb_open_pass", "mlb_open_pass_range", "mlb_run_steps",
+    "mlb_run_steps_inplace", "mlb_inplace_normalize",
     "mlb_halo_copy", "mlb_macro", "mlb_diagnostics", "mlb_probe",
     "mlb_step_host",
 )
@@ -76,6 +77,9 @@ def lib():
         "mlb_open_pass": (i, [vp, vp, vp]),
         "mlb_open_pass_range": (i, [vp, vp, i, i, vp]),
         "mlb_run_steps": (i, [vp, vp, vp, i, vp, ctypes.POINTER(ctypes.c_float)]),
+        "mlb_run_steps_inplace": (i, [vp, vp, i, ctypes.POINTER(ctypes.c_int), vp,
+                                      ctypes.POINTER(ctypes.c_float)]),
+        "mlb_inplace_normalize": (i, [vp, vp, ctypes.POINTER(ctypes.c_int), vp]),
         "mlb_halo_copy": (i, [vp, vp, vp, i, i, vp]),
         "mlb_macro": (i, [vp, vp, vp, vp, vp, vp, vp]),
         "mlb_diagnostics": (i, [vp, vp, dp3, vp]),

@@ -272,6 +272,35 @@ int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cuda
     return launch_scalar<__half>(p, a, variant, n, st);
 }
 
+// in-place (AA pattern) launches: kind 0 = R0 -> R1 step, 1 = R1 -> R0 step, 2 = swap
+template <typename TS>
+int launch_aa(mlb_plan *p, void *f, int kind, cudaStream_t st)
+{
+    using T = typename mlb::Store<TS>::C;
+    mlb::AAArgs<TS> a;
+    for (int q = 0; q < MLB_Q; ++q)
+        a.f[q] = static_cast<TS *>(f) + (long long)q * p->lay.pop;
+    a.cls = p->d_cls;
+    a.mlinks = p->d_mlinks;
+    a.g = p->g;
+    a.omega = T(p->omega);
+    wall_terms<T>(p->wall_u, a.k);
+    constexpr int BX = 128;
+    const dim3 grid((p->nx + BX - 1) / BX, p->ny, p->nz);
+    if (kind == 0) mlb::aa_pull_kernel<TS, BX><<<grid, BX, 0, st>>>(a);
+    else if (kind == 1) mlb::aa_local_kernel<TS, BX><<<grid, BX, 0, st>>>(a);
+    else mlb::aa_swap_kernel<TS, BX><<<grid, BX, 0, st>>>(a);
+    MLB_LAUNCHED();
+    return MLB_OK;
+}
+
+int launch_aa_any(mlb_plan *p, void *f, int kind, cudaStream_t st)
+{
+    if (p->dtype == MLB_F32) return launch_aa<float>(p, f, kind, st);
+    if (p->dtype == MLB_F64) return launch_aa<double>(p, f, kind, st);
+    return launch_aa<__half>(p, f, kind, st);
+}
+
 template <typename T>
 int launch_open(mlb_plan *p, void *fpost, int z0, int z1, cudaStream_t st)
 {
@@ -661,6 +690,50 @@ int mlb_run_steps(mlb_plan *p, void *d_a, void *d_b, int nsteps, void *stream, f
         MLB_CUDA(cudaEventSynchronize(p->ev1));
         MLB_CUDA(cudaEventElapsedTime(ms, p->ev0, p->ev1));
     }
+    return MLB_OK;
+}
+
+static int check_inplace(const mlb_plan *p, const void *d_f, const int *repr)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (!d_f || !repr) return fail(MLB_EINVAL, "NULL argument");
+    if (*repr != 0 && *repr != 1)
+        return fail(MLB_EINVAL, "representation must be 0 (normal) or 1 (shifted), got %d", *repr);
+    if (p->z_mode != MLB_Z_PERIODIC)
+        return fail(MLB_EUNSUPPORTED, "the in-place update needs an MLB_Z_PERIODIC plan "
+                    "(whole domain on one GPU)");
+    if (p->n_in || p->n_out)
+        return fail(MLB_EUNSUPPORTED, "the in-place update handles walls only; this geometry "
+                    "has %lld inlet and %lld outlet cells - use the two-buffer path",
+                    p->n_in, p->n_out);
+    return MLB_OK;
+}
+
+int mlb_run_steps_inplace(mlb_plan *p, void *d_f, int nsteps, int *repr, void *stream, float *ms)
+{
+    if (int rc = check_inplace(p, d_f, repr)) return rc;
+    if (nsteps < 0) return fail(MLB_EINVAL, "nsteps < 0");
+    MLB_CUDA(cudaSetDevice(p->device));
+    if (ms) MLB_CUDA(cudaEventRecord(p->ev0, S(stream)));
+    for (int t = 0; t < nsteps; ++t) {
+        if (int rc = launch_aa_any(p, d_f, *repr, S(stream))) return rc;
+        *repr ^= 1;
+    }
+    if (ms) {
+        MLB_CUDA(cudaEventRecord(p->ev1, S(stream)));
+        MLB_CUDA(cudaEventSynchronize(p->ev1));
+        MLB_CUDA(cudaEventElapsedTime(ms, p->ev0, p->ev1));
+    }
+    return MLB_OK;
+}
+
+int mlb_inplace_normalize(mlb_plan *p, void *d_f, int *repr, void *stream)
+{
+    if (int rc = check_inplace(p, d_f, repr)) return rc;
+    if (*repr == 0) return MLB_OK;
+    MLB_CUDA(cudaSetDevice(p->device));
+    if (int rc = launch_aa_any(p, d_f, 2, S(stream))) return rc;
+    *repr = 0;
     return MLB_OK;
 }
 

@@ -241,6 +241,166 @@ __global__ void __launch_bounds__(BX) step_kernel(const StepArgs<TS> a)
 }
 
 // ---------------------------------------------------------------------------
+// In-place ("AA pattern") update: ONE population block instead of two, same
+// 2 x 19 x sizeof(TS) bytes of traffic per update.  The block alternates
+// between two representations of the same post-collision state F:
+//   R0 (normal):   A[i][x] = F[i][x]
+//   R1 (shifted):  for a fluid cell x and direction i,  F[opp(i)][x] lives at
+//                  A[i][x - c_i]   if the cell x - c_i is not a wall,
+//                  A[opp(i)][x]    if it is (the link bounces back).
+// R0 -> R1 (`aa_pull_kernel`): a cell reads exactly the locations the A/B
+// kernel reads (kernels.py:83-197: A[i][x - c_i], or its own A[opp(i)][x]
+// (+ wall term) for a bouncing link), collides, and writes the result for
+// direction opp(i) back INTO THE LOCATION IT READ for direction i.  Every
+// location is read by exactly one cell, so nothing is clobbered.
+// R1 -> R0 (`aa_local_kernel`): what a cell needs for direction i is then
+// always in its own slot A[opp(i)][x] (the neighbour put it there, or it is
+// the cell's own bounced population, which still lacks the wall term - it is
+// added here, the same single addition the A/B kernel performs); collide;
+// write A[i][x].  Arithmetic and operands are those of the A/B kernel, so
+// the populations are bit-identical to it (and to the oracle) after any
+// number of steps.  `aa_swap_kernel` converts R1 <-> R0 without a step (for
+// diagnostics or a download in the middle of a pair).
+// Scope: walls only - flags FLUID / SOLID / MOVING_WALL (open boundaries
+// stay on the A/B path), whole domain on one GPU (MLB_Z_PERIODIC).
+template <typename TS>
+struct AAArgs {
+    using T = typename Store<TS>::C;
+    TS *f[Q];
+    const uint32_t *__restrict__ cls;
+    const uint32_t *__restrict__ mlinks;
+    Geom g;
+    T omega;
+    T k[Q];
+};
+
+template <typename TS>
+struct CellPos {
+    int d, off[Q];  // own offset, and the offset of the source cell per direction
+};
+
+template <typename TS>
+__device__ __forceinline__ void aa_offsets(const Geom &gm, int x, int y, int lz, int &d,
+                                           int (&off)[Q])
+{
+    const int xp = (int)gm.xp, plane = (int)gm.plane;
+    const int dxm = (x == 0) ? gm.nx - 1 : -1;
+    const int dxq = (x == gm.nx - 1) ? 1 - gm.nx : 1;
+    const int rm = ((y == 0) ? gm.ny - 1 : -1) * xp;
+    const int rq = ((y == gm.ny - 1) ? 1 - gm.ny : 1) * xp;
+    const int zm = (((lz == 0) ? gm.zlo_src : lz) - (lz + 1)) * plane;
+    const int zq = (((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) - (lz + 1)) * plane;
+    d = (lz + 1) * plane + y * xp + x;
+    off[0] = d;
+    off[1] = d + dxm;        off[2] = d + rm;         off[3] = d + dxq;        off[4] = d + rq;
+    off[5] = d + dxm + rm;   off[6] = d + dxq + rm;   off[7] = d + dxq + rq;   off[8] = d + dxm + rq;
+    off[9] = d + zm;         off[10] = d + zq;
+    off[11] = d + dxm + zm;  off[12] = d + dxq + zm;  off[13] = d + dxq + zq;  off[14] = d + dxm + zq;
+    off[15] = d + rm + zm;   off[16] = d + rq + zm;   off[17] = d + rq + zq;   off[18] = d + rm + zq;
+}
+
+template <typename TS, int BX>
+__global__ void __launch_bounds__(BX) aa_pull_kernel(const AAArgs<TS> a)
+{
+    using T = typename Store<TS>::C;
+    const int x = blockIdx.x * BX + threadIdx.x;
+    if (x >= a.g.nx)
+        return;
+    int d, off[Q];
+    aa_offsets<TS>(a.g, x, blockIdx.y, blockIdx.z, d, off);
+    const uint32_t cd = a.cls[d];
+    T g[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+        g[i] = Store<TS>::up(a.f[i][off[i]]);
+    if (cd & CLS_FLAG)
+        return;
+    if (cd != 0) {
+        const uint32_t mv = (cd & CLS_MOVING) ? a.mlinks[d] : 0u;
+#pragma unroll
+        for (int i = 1; i < Q; ++i)
+            if (cd & cls_link(i)) {
+                const T c = Store<TS>::up(a.f[opp(i)][d]);
+                g[i] = (mv & (1u << i)) ? c + a.k[i] : c;
+            }
+    }
+    collide<T>(g, a.omega);
+    a.f[0][d] = Store<TS>::down(g[0]);
+#pragma unroll
+    for (int i = 1; i < Q; ++i) {
+        const TS v = Store<TS>::down(g[opp(i)]);
+        if (cd & cls_link(i))
+            a.f[opp(i)][d] = v;     // bouncing link: stays in the cell, unswapped
+        else
+            a.f[i][off[i]] = v;     // into the location read for direction i
+    }
+}
+
+template <typename TS, int BX>
+__global__ void __launch_bounds__(BX) aa_local_kernel(const AAArgs<TS> a)
+{
+    using T = typename Store<TS>::C;
+    const int x = blockIdx.x * BX + threadIdx.x;
+    if (x >= a.g.nx)
+        return;
+    const int d = ((int)blockIdx.z + 1) * (int)a.g.plane + (int)blockIdx.y * (int)a.g.xp + x;
+    const uint32_t cd = a.cls[d];
+    T g[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+        g[i] = Store<TS>::up(a.f[opp(i)][d]);
+    if (cd & CLS_FLAG) {
+        // non-fluid cell: rewrite its own (untouched) values so that every
+        // store of the warp is a full line - in place this is always valid
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+            a.f[opp(i)][d] = Store<TS>::down(g[i]);
+        return;
+    }
+    if (cd & CLS_MOVING) {
+        const uint32_t mv = a.mlinks[d];
+#pragma unroll
+        for (int i = 1; i < Q; ++i)
+            if (mv & (1u << i))
+                g[i] = g[i] + a.k[i];
+    }
+    collide<T>(g, a.omega);
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+        a.f[i][d] = Store<TS>::down(g[i]);
+}
+
+// R1 <-> R0 without a step: swap each pair of locations {(q, x), (opp(q), x + c_q)}
+// whose link does not bounce; each pair is owned by the cell on the "positive"
+// side (q in {1,2,5,6,9,11,12,15,16}; x + c_q = the source cell of opp(q)).
+template <typename TS, int BX>
+__global__ void __launch_bounds__(BX) aa_swap_kernel(const AAArgs<TS> a)
+{
+    const int x = blockIdx.x * BX + threadIdx.x;
+    if (x >= a.g.nx)
+        return;
+    int d, off[Q];
+    aa_offsets<TS>(a.g, x, blockIdx.y, blockIdx.z, d, off);
+    const uint32_t cd = a.cls[d];
+    if (cd & CLS_FLAG)
+        return;
+#pragma unroll
+    for (int q = 1; q < Q; ++q) {
+        constexpr int dummy = 0; (void)dummy;
+        const bool positive = (q == 1 || q == 2 || q == 5 || q == 6 || q == 9 || q == 11
+                               || q == 12 || q == 15 || q == 16);
+        if (!positive)
+            continue;
+        const int o = opp(q);           // x + c_q is the source cell of direction o
+        if (cd & cls_link(o))
+            continue;                   // bouncing link: both representations agree
+        const TS u = a.f[q][d], v = a.f[o][off[o]];
+        a.f[q][d] = v;
+        a.f[o][off[o]] = u;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Vectorised variant: each thread owns a PACK of V consecutive cells in x
 // (one 16-byte word per population in fp32 / fp64, 8 or 4 bytes in fp16
 // storage); a warp covers LX

@@ -90,6 +90,7 @@ class RunConfig:
     checkpoint_every: int = 0
     out_dir: str = "out"
     device: int | None = None
+    inplace: bool = False  # one device block instead of two (AA pattern; walls only)
 
     def __post_init__(self):
         if self.steps < 1:
@@ -127,16 +128,19 @@ class SimState:
             post = PopulationField(
                 pinned_empty(self.f_pre.data.shape, self.f_pre.data.dtype),
                 self.nx, self.ny, self.nz, self.layout)
-            if self.session is not None and self.session.host_stale:
+            if (self.session is not None and self.session.host_stale
+                    and not self.session.inplace):
                 self.session.plan.download(self.session.post, post.data)
             else:
+                if self.session is not None:
+                    self.session.sync_host()
                 np.copyto(post.data, self.f_pre.data)
             self.f_post_ = post
         return self.f_post_
 
     def swap(self):
         self.f_pre, self.f_post_ = self.f_post, self.f_pre
-        if self.session is not None:
+        if self.session is not None and not self.session.inplace:
             self.session.pre, self.session.post = self.session.post, self.session.pre
 
     def _session_for_diagnostics(self):
@@ -152,6 +156,7 @@ class SimState:
         computed by the CUDA macro kernel."""
         sess, temp = self._session_for_diagnostics()
         try:
+            sess.normalize()
             out = tuple(t.cpu().numpy().transpose(2, 1, 0)
                         for t in sess.plan.macro(sess.pre))
         finally:
@@ -164,6 +169,7 @@ class SimState:
         fluid cells - deterministic device reductions."""
         sess, temp = self._session_for_diagnostics()
         try:
+            sess.normalize()
             return sess.plan.diagnostics(sess.pre)
         finally:
             if temp:
@@ -233,17 +239,31 @@ class Session:
     construction) and is not downloaded.
     """
 
-    def __init__(self, state, plan):
+    def __init__(self, state, plan, inplace=False):
         self.state = state
         self.plan = plan
+        self.inplace = bool(inplace)
+        if self.inplace and np.any(state.mask >= boundaries.INLET):
+            raise ValueError("the in-place update handles walls only; this "
+                             "geometry has inlet/outlet cells - use inplace=False")
         self.pre = plan.alloc()
-        self.post = plan.alloc()
+        self.post = None if self.inplace else plan.alloc()
         self.host_stale = False
         self.upload()
+
+    def normalize(self):
+        """In-place sessions: bring the block to the normal representation
+        (a no-op after an even number of steps)."""
+        if self.inplace:
+            self.plan.normalize(self.pre)
 
     def upload(self):
         st = self.state
         self.plan.upload(st.f_pre.data, self.pre)
+        if self.inplace:
+            self.pre.repr = 0
+            self.host_stale = False
+            return
         if st.f_post_ is None:
             self.post.tensor.copy_(self.pre.tensor)
             same = True
@@ -264,16 +284,22 @@ class Session:
         if not self.host_stale:
             return
         st = self.state
+        self.normalize()
         self.plan.download(self.pre, st.f_pre.data, sync=False)
-        if st.f_post_ is not None:
+        if st.f_post_ is not None and not self.inplace:
             self.plan.download(self.post, st.f_post_.data, sync=False)
         torch.cuda.current_stream(self.plan.device).synchronize()
+        if st.f_post_ is not None and self.inplace:
+            np.copyto(st.f_post_.data, st.f_pre.data)  # there is no second device block
         self.host_stale = False
 
     def advance(self, nsteps, timed=False):
         """`nsteps` x (fused update, open-boundary pass, swap)."""
-        newest, other, ms = self.plan.run_steps(self.pre, self.post, nsteps, timed)
-        self.pre, self.post = newest, other
+        if self.inplace:
+            ms = self.plan.run_steps_inplace(self.pre, nsteps, timed)
+        else:
+            newest, other, ms = self.plan.run_steps(self.pre, self.post, nsteps, timed)
+            self.pre, self.post = newest, other
         self.state.t += nsteps
         self.host_stale = True
         return ms
@@ -293,7 +319,7 @@ def open_session(state, config=None):
         return state.session
     config = config or RunConfig(steps=1, precision=state.precision,
                                  layout=state.layout)
-    state.session = Session(state, build_plan(state, config))
+    state.session = Session(state, build_plan(state, config), inplace=config.inplace)
     return state.session
 
 
@@ -362,6 +388,7 @@ def run(state, config, on_output=None, on_checkpoint=None, probe=None):
             events.append((e0, e1))
             done += chunk
             if samples is not None:
+                sess.normalize()
                 plan.probe(sess.pre, probe[0], probe[1], probe[2], samples[done - 1])
             if config.output_every and state.t % config.output_every == 0:
                 state.check_finite()

@@ -64,6 +64,7 @@ class DeviceField:
     def __init__(self, tensor, nx, ny, nz):
         self.tensor = tensor
         self.nx, self.ny, self.nz = nx, ny, nz
+        self.repr = 0  # in-place runs only: 0 = normal, 1 = shifted (include/mlb.h)
 
     @property
     def ptr(self):
@@ -282,6 +283,27 @@ class KernelPlan:
             ctypes.byref(ms) if timed else None))
         newest, other = (a, b) if nsteps % 2 == 0 else (b, a)
         return newest, other, (ms.value if timed else None)
+
+    def run_steps_inplace(self, f, nsteps, timed=False):
+        """`nsteps` steps on ONE block (the AA pattern): same arithmetic and
+        traffic as `run_steps`, half the memory.  Walls only.  `f.repr`
+        tracks the representation the block is left in; call `normalize`
+        before reading it back.  Returns the loop's device time in ms when
+        `timed`."""
+        ms = ctypes.c_float(0.0)
+        r = ctypes.c_int(f.repr)
+        _cabi.check(self._lib.mlb_run_steps_inplace(
+            self._plan, f.ptr, int(nsteps), ctypes.byref(r), _stream_ptr(self.device),
+            ctypes.byref(ms) if timed else None))
+        f.repr = r.value
+        return ms.value if timed else None
+
+    def normalize(self, f):
+        """Bring an in-place block back to the normal representation."""
+        r = ctypes.c_int(f.repr)
+        _cabi.check(self._lib.mlb_inplace_normalize(self._plan, f.ptr, ctypes.byref(r),
+                                                    _stream_ptr(self.device)))
+        f.repr = r.value
 
     def halo_copy(self, dst, src, face):
         """Fill one halo plane of `dst` from the matching boundary plane of

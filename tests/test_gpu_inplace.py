@@ -1,0 +1,142 @@
+"""The in-place (AA pattern) update: one population block, same bits.
+
+Arithmetic and operands are those of the two-buffer kernel, so after any
+number of steps - odd or even, through the shifted representation and back
+- the populations must equal the CPU oracle's bit for bit, and non-fluid
+cells must be untouched."""
+
+import numpy as np
+import pytest
+
+from oracle.cpu import CpuOracle
+from paper_2409_16781_b200 import boundaries as B
+from paper_2409_16781_b200 import lattice as L
+from paper_2409_16781_b200.fields import Layout, Precision
+
+from .helpers import geometries3d, random_block
+
+pytestmark = pytest.mark.gpu
+
+PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED1}
+WALL_GEOMS = ["cavity", "cavity_oblique_lid", "cavity16", "periodic", "periodic8", "wide"]
+
+
+def make(grid, prec, omega, wall_u):
+    from paper_2409_16781_b200.kernels import KernelPlan
+    nx, ny, nz = grid.shape
+    plan = KernelPlan(nx, ny, nz, Layout.ROW, prec, B.flatten_mask(grid), omega, wall_u)
+    orc = CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u)
+    return plan, orc
+
+
+@pytest.mark.parametrize("steps", [1, 2, 5, 8])
+@pytest.mark.parametrize("tag", ["f64", "f32", "f16"])
+@pytest.mark.parametrize("geom", WALL_GEOMS)
+def test_inplace_equals_oracle_bitwise(geom, tag, steps, rng):
+    grid, wall_u, _ = geometries3d()[geom]
+    prec = PREC[tag]
+    plan, orc = make(grid, prec, 1.45, wall_u)
+    f = random_block(rng, grid.size, prec.storage)
+    want = orc.run(f.copy(), f.copy(), steps)
+    d = plan.alloc()
+    plan.upload(f, d)
+    plan.run_steps_inplace(d, steps)
+    assert d.repr == steps % 2
+    plan.normalize(d)
+    assert d.repr == 0
+    got = np.empty_like(f)
+    plan.download(d, got)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_split_runs_and_normalize_in_the_middle(rng):
+    grid, wall_u, _ = geometries3d()["cavity16"]
+    plan, orc = make(grid, Precision.SINGLE, 1.7, wall_u)
+    f = random_block(rng, grid.size, np.float32)
+    want = orc.run(f.copy(), f.copy(), 9)
+    d = plan.alloc()
+    plan.upload(f, d)
+    plan.run_steps_inplace(d, 3)     # ends shifted
+    plan.normalize(d)                # back to normal without stepping
+    mid = np.empty_like(f)
+    plan.download(d, mid)
+    np.testing.assert_array_equal(mid, orc.run(f.copy(), f.copy(), 3))
+    plan.normalize(d)                # no-op in the normal representation
+    plan.run_steps_inplace(d, 1)
+    plan.run_steps_inplace(d, 5)     # continues from the shifted representation
+    plan.normalize(d)
+    got = np.empty_like(f)
+    plan.download(d, got)
+    np.testing.assert_array_equal(got, want)
+    # diagnostics on the normalised block equal the two-buffer path's
+    a, b = plan.alloc(), plan.alloc()
+    plan.upload(f, a)
+    plan.upload(f, b)
+    newest, _, _ = plan.run_steps(a, b, 9)
+    assert plan.diagnostics(d) == plan.diagnostics(newest)
+
+
+def test_open_boundaries_are_rejected(rng):
+    grid, wall_u, inlet_u = geometries3d()["channel40"]
+    from paper_2409_16781_b200.kernels import KernelPlan
+    nx, ny, nz = grid.shape
+    plan = KernelPlan(nx, ny, nz, Layout.ROW, Precision.SINGLE, B.flatten_mask(grid), 1.0,
+                      wall_u, inlet_u=inlet_u)
+    d = plan.alloc(zero=True)
+    with pytest.raises(ValueError, match="walls only"):
+        plan.run_steps_inplace(d, 1)
+    from paper_2409_16781_b200 import cases, engine
+    state = cases.init(cases.CaseSpec("vks", 48, 32, 8), Precision.SINGLE)
+    with pytest.raises(ValueError, match="walls only"):
+        engine.run(state, engine.RunConfig(steps=1, inplace=True))
+
+
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+def test_engine_run_inplace_equals_two_buffer_run(tag):
+    from paper_2409_16781_b200 import cases, engine
+    prec = PREC[tag]
+    spec = cases.CaseSpec("ldc", 40, 36, 28, re=100.0, u0=0.1)
+    a = cases.init(spec, prec)
+    b = cases.init(spec, prec)
+    seen = []
+    ra = engine.run(a, engine.RunConfig(steps=31, precision=prec, output_every=10),
+                    on_output=lambda st: seen.append(st.t), probe=(20, 30, 14))
+    rb = engine.run(b, engine.RunConfig(steps=31, precision=prec, output_every=10, inplace=True),
+                    probe=(20, 30, 14))
+    assert seen == [10, 20, 30] and a.t == b.t == 31
+    np.testing.assert_array_equal(a.f_pre.data, b.f_pre.data)
+    np.testing.assert_array_equal(ra.probe_samples, rb.probe_samples)
+    for x, y in zip(a.macro(), b.macro()):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_ldc_1024_cubed_fp32_on_one_gpu():
+    """BASELINE configs[3]'s grid on ONE B200: 1024^3 fp32 needs 81.7 GB per
+    block; two blocks plus tables would not leave room, one block does.
+    Properties at full size: mass conservation in the closed box, finite
+    fields, walls untouched, the lid drags fluid along +x."""
+    import torch
+    from paper_2409_16781_b200.kernels import KernelPlan
+    from paper_2409_16781_b200.lattice import omega_from_reynolds
+    n = 1024
+    free, _ = torch.cuda.mem_get_info()
+    if free < 100e9:
+        pytest.skip("needs ~95 GB of free device memory")
+    omega = omega_from_reynolds(1000.0, 0.1, n).omega
+    flags = B.flatten_mask(B.cavity_mask(n, n, n))
+    plan = KernelPlan(n, n, n, Layout.ROW, Precision.SINGLE, flags, omega, (0.1, 0.0, 0.0))
+    del flags
+    d = plan.alloc()
+    for q in range(19):
+        d.tensor[q].fill_(float(np.float32(L.W[q])))
+    d0 = plan.diagnostics(d)
+    assert d0["fluid_cells"] == (n - 2) ** 3
+    ms = plan.run_steps_inplace(d, 6, timed=True)
+    plan.normalize(d)
+    d1 = plan.diagnostics(d)
+    assert d1["nonfinite"] == 0
+    assert abs(d1["mass"] - d0["mass"]) <= 2e-6 * d0["mass"]
+    assert 0.0 < d1["max_u"] < 0.2 and d1["px"] > 0.0
+    wall = d.tensor[:, 1:-1, 0, :n]
+    assert all(bool((wall[q] == float(np.float32(L.W[q]))).all()) for q in range(19))
+    print(f"1024^3 fp32 in place: {n ** 3 * 6 / ms / 1e3:.0f} MLUPS")
