@@ -134,3 +134,81 @@ def test_omega_zero_roll_256_periodic():
         want = torch.roll(src, shifts=(int(L.C[q][2]), int(L.C[q][1]), int(L.C[q][0])),
                           dims=(0, 1, 2))
         assert torch.equal(b.tensor[q, 1:-1], want), q
+
+
+def test_channel_1024x512x512_fp32_flag_mask_path():
+    """configs[4] at full size on one GPU: channel along x with solid y/z
+    walls, equilibrium inlet, zero-gradient outlet and a bounce-back
+    cylinder (the reference's vks geometry, z-extruded).  (a) a thin window
+    of the same case, bit-exact against the oracle; (b) at full size:
+    inlet / outlet semantics (engine.py:156-180) hold exactly on the device
+    state, fields stay finite, solid cells untouched, and two z-slabs
+    reproduce the single domain bit for bit."""
+    import torch
+    from paper_2409_16781_b200 import cases, engine, slab
+    from paper_2409_16781_b200.kernels import KernelPlan
+
+    # (a) oracle window: same geometry builder, 256 x 128 x 24, 15 steps
+    spec = cases.CaseSpec("vks", 256, 128, 24, re=100.0, u0=0.08)
+    state = cases.init(spec, Precision.SINGLE)
+    f0 = state.f_pre.data.copy()
+    engine.run(state, engine.RunConfig(steps=15))
+    orc = CpuOracle(256, 128, 24, state.mask, state.params.omega, inlet_u=0.08, threads=16)
+    np.testing.assert_array_equal(state.f_pre.data, orc.run(f0.copy(), f0.copy(), 15))
+    del f0, state
+
+    # (b) full size
+    nx, ny, nz, steps = 1024, 512, 512, 12
+    spec = cases.CaseSpec("vks", nx, ny, nz, re=200.0, u0=0.08)
+    grid = spec.mask()
+    flags = B.flatten_mask(grid)
+    omega = spec.relaxation().omega
+    eq = L.equilibrium(1.0, 0.08, 0.0, 0.0).astype(np.float32)
+
+    def fresh(plan):
+        a = plan.alloc()
+        for q in range(19):
+            a.tensor[q].fill_(float(eq[q]))
+        b = plan.alloc()
+        b.tensor.copy_(a.tensor)
+        return a, b
+
+    plan = KernelPlan(nx, ny, nz, Layout.ROW, Precision.SINGLE, flags, omega, inlet_u=0.08)
+    plan.set_passthrough(True)
+    a, b = fresh(plan)
+    res, _, ms = plan.run_steps(a, b, steps, timed=True)
+    d = plan.diagnostics(res)
+    assert d["nonfinite"] == 0 and 0.0 < d["max_u"] < 0.3
+    assert d["fluid_cells"] == np.count_nonzero(flags == 0)
+    t = res.tensor[:, 1:-1]                                  # (19, nz, ny, nx)
+    m = torch.from_numpy(grid.transpose(2, 1, 0).copy()).cuda()   # [z][y][x]
+    inlet, outlet, solid = m == B.INLET, m == B.OUTLET, m == B.SOLID
+    for q in range(19):
+        assert bool((t[q][inlet] == float(eq[q])).all())
+        assert bool((t[q][..., -1][outlet[..., -1]] == t[q][..., -2][outlet[..., -1]]).all())
+        assert bool((t[q][solid] == float(eq[q])).all())     # never changed
+    ref = res.tensor[:, 1:-1].clone()
+    print(f"channel {nx}x{ny}x{nz} fp32: {nx * ny * nz * steps / ms / 1e3:.0f} MLUPS")
+    del a, b, res, t
+    plan.close()
+    torch.cuda.empty_cache()
+
+    f3 = flags.reshape(nz, ny, nx)
+    slabs = []
+    for (z0, z1) in slab.partition(nz, 2):
+        lo, hi = slab.slab_halo_flags(f3, nx, ny, z0, z1)
+        p = KernelPlan(nx, ny, z1 - z0, Layout.ROW, Precision.SINGLE, f3[z0:z1], omega,
+                       inlet_u=0.08, halo_lo=lo, halo_hi=hi, slab=True)
+        p.set_passthrough(True)
+        slabs.append((p, list(fresh(p))))
+    pre, post = 0, 1
+    for _ in range(steps):
+        for p, blocks in slabs:
+            p.step_range(blocks[pre], blocks[post], 0, p.nz)
+            p.open_pass_range(blocks[post], 0, p.nz)
+        for r, (p, blocks) in enumerate(slabs):
+            p.halo_copy(blocks[post], slabs[r - 1][1][post], face=0)
+            p.halo_copy(blocks[post], slabs[(r + 1) % 2][1][post], face=1)
+        pre, post = post, pre
+    assert torch.equal(slabs[0][1][pre].tensor[:, 1:-1], ref[:, :256])
+    assert torch.equal(slabs[1][1][pre].tensor[:, 1:-1], ref[:, 256:])
