@@ -9,11 +9,11 @@ lazily so that the host modules stay usable on a machine without a GPU.
 from . import boundaries, fields, lattice, perfport  # noqa: F401
 
 __all__ = ["boundaries", "fields", "lattice", "perfport", "kernels", "engine",
-           "cases", "slab"]
+           "cases", "slab", "io"]
 
 
 def __getattr__(name):
-    if name in ("kernels", "engine", "cases", "slab", "_cabi"):
+    if name in ("kernels", "engine", "cases", "slab", "io", "_cabi"):
         import importlib
         return importlib.import_module(f"{__name__}.{name}")
     raise AttributeError(name)

@@ -84,12 +84,9 @@ int layout_of(int nx, int ny, int nz, int dtype, mlb_layout *out)
     const int sz = dtype == MLB_F32 ? 4 : dtype == MLB_F64 ? 8 : 2;
     const long long line = 128 / sz;
     out->nx = nx; out->ny = ny; out->nz = nz; out->itemsize = sz;
-    // experiment knobs (undocumented): extra row / population padding
-    const char *px = getenv("MLB_PAD_X"), *pp = getenv("MLB_PAD_POP");
-    const long long pad_x = px ? atoll(px) : 0, pad_pop = pp ? atoll(pp) : 0;
-    out->xp = (nx + pad_x + line - 1) / line * line;
+    out->xp = (nx + line - 1) / line * line;
     out->plane = (long long)ny * out->xp;
-    out->pop = (long long)(nz + 2) * out->plane + pad_pop * line;
+    out->pop = (long long)(nz + 2) * out->plane;
     if (out->pop >= (1LL << 31))
         return fail(MLB_EUNSUPPORTED, "slab of %dx%dx%d cells exceeds 2^31 elements per "
                     "population; use more z-slabs", nx, ny, nz);

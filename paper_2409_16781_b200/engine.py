@@ -29,9 +29,8 @@ import numpy as np
 import torch
 
 from . import boundaries
-from .fields import (Layout, PopulationField, Precision, convert_precision,
-                     flatten_xyz)
-from .kernels import BACKEND, DeviceField, KernelPlan, pinned_empty  # noqa: F401
+from .fields import Layout, PopulationField, Precision, convert_precision
+from .kernels import BACKEND, KernelPlan, pinned_empty  # noqa: F401  (BACKEND: API parity)
 from .lattice import Q, RelaxationParams, equilibrium
 
 

@@ -101,7 +101,6 @@ class DistSlab:
         self.below, self.above = ring_neighbours(rank, world)
         self.cuda = isinstance(stepper, CudaStepper)
         self.overlap = bool(overlap) and self.cuda and self.nz >= 3
-        self._main_done = None
 
     # -- halo exchange -----------------------------------------------------
     def _ops(self, t):
@@ -194,16 +193,6 @@ def exchange_flag_halos(flags_slab, rank, world, group=None, device=None):
     if dev != "cpu":
         torch.cuda.synchronize()
     return lo.cpu().numpy(), hi.cpu().numpy()
-
-
-def fill_block_from_dense(tensor, dense, nx):
-    """Copy a dense (19, nz, ny, nx) array into the interior planes of a
-    (19, nz+2, ny, xp) block tensor (CPU helper for tests)."""
-    tensor[:, 1:-1, :, :nx] = torch.as_tensor(dense)
-
-
-def gather_dense(tensor, nx):
-    return tensor[:, 1:-1, :, :nx].contiguous()
 
 
 __all__ = ["partition", "ring_neighbours", "slab_halo_flags", "CudaStepper",

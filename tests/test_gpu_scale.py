@@ -163,7 +163,8 @@ def test_channel_1024x512x512_fp32_flag_mask_path():
     grid = spec.mask()
     flags = B.flatten_mask(grid)
     omega = spec.relaxation().omega
-    eq = L.equilibrium(1.0, 0.08, 0.0, 0.0).astype(np.float32)
+    eq = L.equilibrium(1.0, 0.08, 0.0, 0.0).astype(np.float32)          # initial fill: f64 -> f32
+    eq_in = L.equilibrium(1.0, 0.08, 0.0, 0.0, dtype=np.float32)        # inlet: compute dtype
 
     def fresh(plan):
         a = plan.alloc()
@@ -184,7 +185,7 @@ def test_channel_1024x512x512_fp32_flag_mask_path():
     m = torch.from_numpy(grid.transpose(2, 1, 0).copy()).cuda()   # [z][y][x]
     inlet, outlet, solid = m == B.INLET, m == B.OUTLET, m == B.SOLID
     for q in range(19):
-        assert bool((t[q][inlet] == float(eq[q])).all())
+        assert bool((t[q][inlet] == float(eq_in[q])).all())
         assert bool((t[q][..., -1][outlet[..., -1]] == t[q][..., -2][outlet[..., -1]]).all())
         assert bool((t[q][solid] == float(eq[q])).all())     # never changed
     ref = res.tensor[:, 1:-1].clone()
