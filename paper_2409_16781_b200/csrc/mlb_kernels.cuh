@@ -299,20 +299,41 @@ __device__ __forceinline__ void aa_offsets(const Geom &gm, int x, int y, int lz,
     off[15] = d + rm + zm;   off[16] = d + rq + zm;   off[17] = d + rq + zq;   off[18] = d + rm + zq;
 }
 
+// direction table for the scalar in-place kernels: X(i, plane delta, row delta, x-shifted base)
+#define MLB_AA_DIRS(X)                                                              \
+    X(1, zc, rc, dm)   X(2, zc, rm, dc)   X(3, zc, rc, dq)   X(4, zc, rq, dc)       \
+    X(5, zc, rm, dm)   X(6, zc, rm, dq)   X(7, zc, rq, dq)   X(8, zc, rq, dm)       \
+    X(9, zm, rc, dc)   X(10, zq, rc, dc)  X(11, zm, rc, dm)  X(12, zm, rc, dq)      \
+    X(13, zq, rc, dq)  X(14, zq, rc, dm)  X(15, zm, rm, dc)  X(16, zm, rq, dc)      \
+    X(17, zq, rq, dc)  X(18, zq, rm, dc)
+
 template <typename TS, int BX>
 __global__ void __launch_bounds__(BX) aa_pull_kernel(const AAArgs<TS> a)
 {
     using T = typename Store<TS>::C;
+    const Geom &gm = a.g;
     const int x = blockIdx.x * BX + threadIdx.x;
-    if (x >= a.g.nx)
+    if (x >= gm.nx)
         return;
-    int d, off[Q];
-    aa_offsets<TS>(a.g, x, blockIdx.y, blockIdx.z, d, off);
+    const int y = blockIdx.y, lz = blockIdx.z;
+    const int xp = (int)gm.xp, plane = (int)gm.plane;
+    // same index arithmetic as step_cell
+    const int dxm = (x == 0) ? gm.nx - 1 : -1;
+    const int dxq = (x == gm.nx - 1) ? 1 - gm.nx : 1;
+    const int rm = ((y == 0) ? gm.ny - 1 : -1) * xp;
+    const int rq = ((y == gm.ny - 1) ? 1 - gm.ny : 1) * xp;
+    const int zm = (((lz == 0) ? gm.zlo_src : lz) - (lz + 1)) * plane;
+    const int zq = (((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) - (lz + 1)) * plane;
+    constexpr int zc = 0, rc = 0;
+    const int d = (lz + 1) * plane + y * xp + x;
+    const int dm = d + dxm, dq = d + dxq, dc = d;
+
     const uint32_t cd = a.cls[d];
     T g[Q];
-#pragma unroll
-    for (int i = 0; i < Q; ++i)
-        g[i] = Store<TS>::up(a.f[i][off[i]]);
+    g[0] = Store<TS>::up(a.f[0][d]);
+#define MLB_X(i, zz, rr, dd) g[i] = Store<TS>::up(a.f[i][(dd) + ((zz) + (rr))]);
+    MLB_AA_DIRS(MLB_X)
+#undef MLB_X
     if (cd & CLS_FLAG)
         return;
     if (cd != 0) {
@@ -326,13 +347,19 @@ __global__ void __launch_bounds__(BX) aa_pull_kernel(const AAArgs<TS> a)
     }
     collide<T>(g, a.omega);
     a.f[0][d] = Store<TS>::down(g[0]);
-#pragma unroll
-    for (int i = 1; i < Q; ++i) {
-        const TS v = Store<TS>::down(g[opp(i)]);
-        if (cd & cls_link(i))
-            a.f[opp(i)][d] = v;     // bouncing link: stays in the cell, unswapped
-        else
-            a.f[i][off[i]] = v;     // into the location read for direction i
+    if (cd == 0) {
+        // bulk cell: every result goes into the location read for its opposite
+#define MLB_X(i, zz, rr, dd) a.f[i][(dd) + ((zz) + (rr))] = Store<TS>::down(g[opp(i)]);
+        MLB_AA_DIRS(MLB_X)
+#undef MLB_X
+    } else {
+#define MLB_X(i, zz, rr, dd)                                                         \
+        if (cd & cls_link(i))                                                        \
+            a.f[opp(i)][d] = Store<TS>::down(g[opp(i)]); /* bounces: stays, unswapped */ \
+        else                                                                         \
+            a.f[i][(dd) + ((zz) + (rr))] = Store<TS>::down(g[opp(i)]);
+        MLB_AA_DIRS(MLB_X)
+#undef MLB_X
     }
 }
 

@@ -1,0 +1,12 @@
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2409_16781_b200 import boundaries as B
+from paper_2409_16781_b200.fields import Layout, Precision
+from paper_2409_16781_b200.kernels import KernelPlan
+from paper_2409_16781_b200.lattice import W
+n = 512
+plan = KernelPlan(n, n, n, Layout.ROW, Precision.SINGLE, B.flatten_mask(B.cavity_mask(n, n, n)), 1.7, (0.1, 0, 0))
+a = plan.alloc()
+for q in range(19):
+    a.tensor[q].fill_(float(W[q]))
+plan.run_steps_inplace(a, 8)
