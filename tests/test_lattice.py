@@ -159,3 +159,15 @@ class TestRelaxation:
             RelaxationParams.from_omega(1.0, source=np.zeros(9))
         assert RelaxationParams.from_omega(1.0, source=np.full(19, 1e-8)).has_source
         assert not RelaxationParams.from_omega(1.0).has_source
+
+
+def test_c01_equilibrium_moment_exactness(rng):
+    # acceptance criterion 1 (test_acceptance.py:49-63) with a third component
+    rho = rng.uniform(0.5, 2.0, size=1000)
+    u = rng.normal(size=(3, 1000))
+    u *= rng.uniform(0.0, 0.2, size=1000) / np.linalg.norm(u, axis=0)
+    got = moments(equilibrium(rho, *u))
+    scale = np.maximum(1.0, np.linalg.norm(u, axis=0))
+    worst = max(np.max(np.abs(got[0] - rho) / rho),
+                *(np.max(np.abs(g - w) / scale) for g, w in zip(got[1:], u)))
+    assert worst <= 1e-13
