@@ -90,7 +90,10 @@ const char *mlb_plan_kernel_name(const mlb_plan *plan);
  * that d_fpre and d_fpost agree on non-fluid cells - true for any pair of
  * buffers that started identical (engine.py:148) - so memory ends up
  * byte-identical to the strict mode, while every warp store is a full
- * 128-byte line instead of leaving partial sectors at each wall. */
+ * 128-byte line instead of leaving partial sectors at each wall.  Rejected
+ * (MLB_EUNSUPPORTED) for geometries in which an outlet cell's x-1 neighbour
+ * is itself an outlet cell: there the reference's result depends on the
+ * stale content of the never-written cell. */
 int mlb_plan_set_passthrough(mlb_plan *plan, int on);
 
 /* Flags: the reference's `mask` argument (kernels.py:408, a (N,) uint8 array
@@ -121,6 +124,13 @@ int mlb_download(const mlb_plan *plan, const void *d_f, void *h_dense, void *str
 int mlb_step(mlb_plan *plan, const void *d_fpre, void *d_fpost, void *stream);
 int mlb_step_range(mlb_plan *plan, const void *d_fpre, void *d_fpost,
                    int z0, int z1, void *stream);
+/* The fused update followed by the open-boundary pass on the same planes -
+ * one time step's work for planes [z0, z1).  Equivalent to mlb_step_range +
+ * mlb_open_pass_range; with pass-through stores and a pack kernel the pass is
+ * applied inside the fused kernel (no extra launches, no strided column
+ * writes) whenever every outlet cell's x-1 neighbour lies in the same pack. */
+int mlb_step_open_range(mlb_plan *plan, const void *d_fpre, void *d_fpost,
+                        int z0, int z1, void *stream);
 /* _OpenBoundaryPass.apply (engine.py:176-180) on d_fpost: inlet cells <-
  * equilibrium(1, inlet_u, 0, 0) in compute dtype; outlet cells <- the fresh
  * populations of their x-1 neighbour, all sources read before any write. */

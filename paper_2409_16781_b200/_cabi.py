@@ -26,7 +26,8 @@ SYMBOLS = (
     "mlb_plan_set_physics", "mlb_plan_set_variant", "mlb_plan_set_passthrough",
     "mlb_plan_kernel_name", "mlb_plan_set_flags",
     "mlb_plan_get_flags", "mlb_upload", "mlb_download", "mlb_step",
-    "mlb_step_range", "mlb_open_pass", "mlb_open_pass_range", "mlb_run_steps",
+    "mlb_step_range", "mlb_step_open_range", "mlb_open_pass", "mlb_open_pass_range",
+    "mlb_run_steps",
     "mlb_run_steps_inplace", "mlb_inplace_normalize",
     "mlb_halo_copy", "mlb_macro", "mlb_diagnostics", "mlb_probe",
     "mlb_step_host",
@@ -74,6 +75,7 @@ def lib():
         "mlb_download": (i, [vp, vp, vp, vp]),
         "mlb_step": (i, [vp, vp, vp, vp]),
         "mlb_step_range": (i, [vp, vp, vp, i, i, vp]),
+        "mlb_step_open_range": (i, [vp, vp, vp, i, i, vp]),
         "mlb_open_pass": (i, [vp, vp, vp]),
         "mlb_open_pass_range": (i, [vp, vp, i, i, vp]),
         "mlb_run_steps": (i, [vp, vp, vp, i, vp, ctypes.POINTER(ctypes.c_float)]),

@@ -62,6 +62,7 @@ struct mlb_plan {
     long long *d_in = nullptr, *d_out = nullptr;
     std::vector<long long> in_zoff, out_zoff;
     bool out_chained = false;
+    unsigned out_xmod8 = 0;  // bit r set: some outlet cell has x % 8 == r
     void *d_out_tmp = nullptr;
     // reductions
     int sms = 148;
@@ -192,11 +193,33 @@ int resolve_variant(const mlb_plan *p)
         return 1016;
     if (p->dtype == MLB_F16 && p->nx % 4 == 0 && p->nx >= 128)
         return 2008;
+    // fp64: the scalar kernel is ~2 % faster, unless there are open-boundary
+    // cells, which only a pack kernel can handle inside the fused pass (~7 %)
+    if (p->dtype == MLB_F64 && (p->n_in || p->n_out) && p->nx % 2 == 0 && p->nx >= 128)
+        return 1016;
     return 128;
 }
 
+template <typename T>
+void inlet_values(double u_in, T *e);
+
+// can the open-boundary pass ride along in the pack kernel?  Needs pass-through
+// stores (the kernel then writes inlet / outlet cells anyway) and every outlet
+// cell's x-1 neighbour inside the same pack of V cells.
+bool can_fuse_open(const mlb_plan *p, int variant)
+{
+    if (!p->passthrough || variant < 1000 || (p->n_in == 0 && p->n_out == 0))
+        return false;
+    const int V = pack_cells(p->dtype, variant);
+    for (int r = 0; r < 8; r += V)
+        if (p->out_xmod8 & (1u << r))
+            return false;
+    return true;
+}
+
 template <typename TS>
-void fill_args(mlb_plan *p, const void *fpre, void *fpost, int z0, mlb::StepArgs<TS> &a)
+void fill_args(mlb_plan *p, const void *fpre, void *fpost, int z0, bool fuse_open,
+               mlb::StepArgs<TS> &a)
 {
     using T = typename mlb::Store<TS>::C;
     for (int q = 0; q < MLB_Q; ++q) {
@@ -208,6 +231,11 @@ void fill_args(mlb_plan *p, const void *fpre, void *fpost, int z0, mlb::StepArgs
     a.g = p->g;
     a.z0 = z0;
     a.passthrough = p->passthrough;
+    a.fuse_open = fuse_open ? 1 : 0;
+    T cv[MLB_Q];
+    inlet_values<T>(p->inlet_u, cv);  // compute dtype, then storage dtype (engine.py:167-171)
+    for (int q = 0; q < MLB_Q; ++q)
+        a.inlet[q] = mlb::Store<TS>::down(cv[q]);
     a.omega = T(p->omega);
     wall_terms<T>(p->wall_u, a.k);
 }
@@ -243,7 +271,8 @@ int launch_scalar(mlb_plan *p, const mlb::StepArgs<TS> &a, int bx, int nplanes, 
     return MLB_OK;
 }
 
-int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cudaStream_t st)
+int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cudaStream_t st,
+                bool fuse_open = false)
 {
     const int variant = resolve_variant(p);
     if (!variant_exists(p->dtype, variant))
@@ -252,18 +281,18 @@ int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cuda
     const int lx = variant % 1000, n = z1 - z0;
     if (p->dtype == MLB_F32) {
         mlb::StepArgs<float> a;
-        fill_args<float>(p, fpre, fpost, z0, a);
+        fill_args<float>(p, fpre, fpost, z0, fuse_open, a);
         return variant >= 1000 ? launch_vec<float, 4>(p, a, lx, n, st)
                                : launch_scalar<float>(p, a, variant, n, st);
     }
     if (p->dtype == MLB_F64) {
         mlb::StepArgs<double> a;
-        fill_args<double>(p, fpre, fpost, z0, a);
+        fill_args<double>(p, fpre, fpost, z0, fuse_open, a);
         return variant >= 1000 ? launch_vec<double, 2>(p, a, lx, n, st)
                                : launch_scalar<double>(p, a, variant, n, st);
     }
     mlb::StepArgs<__half> a;
-    fill_args<__half>(p, fpre, fpost, z0, a);
+    fill_args<__half>(p, fpre, fpost, z0, fuse_open, a);
     if (variant >= 3000) return launch_vec<__half, 2>(p, a, lx, n, st);
     if (variant >= 2000) return launch_vec<__half, 4>(p, a, lx, n, st);
     return launch_scalar<__half>(p, a, variant, n, st);
@@ -491,6 +520,11 @@ const char *mlb_plan_kernel_name(const mlb_plan *p)
 int mlb_plan_set_passthrough(mlb_plan *p, int on)
 {
     if (int rc = check_plan(p, false)) return rc;
+    if (on && p->out_chained)
+        return fail(MLB_EUNSUPPORTED, "pass-through stores are not valid for this geometry: an "
+                    "outlet cell copies from another outlet cell, and the reference then reads "
+                    "that cell's STALE value in fpost (numpy evaluates the right-hand side "
+                    "first, engine.py:179-180), which pass-through would refresh");
     p->passthrough = on ? 1 : 0;
     return MLB_OK;
 }
@@ -509,6 +543,7 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     std::vector<long long> in_idx, out_idx;
     p->in_zoff.assign(nz + 1, 0);
     p->out_zoff.assign(nz + 1, 0);
+    p->out_xmod8 = 0;
     const size_t dense_plane = (size_t)nx * ny;
     for (int sz = 0; sz < nz + 2; ++sz) {
         const uint8_t *src;
@@ -544,6 +579,8 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
                 if (m == 3)
                     in_idx.push_back(d0 + x);
                 else if (m == 4) {
+                    if (interior)
+                        p->out_xmod8 |= 1u << (x & 7);
                     if (x == 0)
                         return fail(MLB_EUNSUPPORTED, "outlet cell at x = 0 (y=%d, z=%d): "
                                     "its source would be the previous row's last cell", y, sz - 1);
@@ -562,6 +599,8 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
             p->out_chained = true;
             break;
         }
+    if (p->out_chained)
+        p->passthrough = 0;  // see mlb_plan_set_passthrough
 
     cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_mlinks); cudaFree(p->d_in);
     cudaFree(p->d_out); cudaFree(p->d_out_tmp);
@@ -661,6 +700,24 @@ int mlb_open_pass_range(mlb_plan *p, void *d_fpost, int z0, int z1, void *stream
     return launch_open<__half>(p, d_fpost, z0, z1, S(stream));
 }
 
+int mlb_step_open_range(mlb_plan *p, const void *d_fpre, void *d_fpost, int z0, int z1,
+                        void *stream)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (can_fuse_open(p, resolve_variant(p))) {
+        if (!d_fpre || !d_fpost) return fail(MLB_EINVAL, "NULL population block");
+        if (d_fpre == d_fpost)
+            return fail(MLB_EINVAL, "fpre and fpost must be distinct blocks");
+        if (z0 < 0 || z1 > p->nz || z0 > z1)
+            return fail(MLB_EINVAL, "plane range [%d, %d) outside [0, %d)", z0, z1, p->nz);
+        if (z0 == z1) return MLB_OK;
+        MLB_CUDA(cudaSetDevice(p->device));
+        return launch_step(p, d_fpre, d_fpost, z0, z1, S(stream), true);
+    }
+    if (int rc = mlb_step_range(p, d_fpre, d_fpost, z0, z1, stream)) return rc;
+    return mlb_open_pass_range(p, d_fpost, z0, z1, stream);
+}
+
 int mlb_open_pass(mlb_plan *p, void *d_fpost, void *stream)
 {
     if (int rc = check_plan(p, true)) return rc;
@@ -678,8 +735,7 @@ int mlb_run_steps(mlb_plan *p, void *d_a, void *d_b, int nsteps, void *stream, f
     if (ms) MLB_CUDA(cudaEventRecord(p->ev0, S(stream)));
     void *pre = d_a, *post = d_b;
     for (int t = 0; t < nsteps; ++t) {
-        if (int rc = mlb_step_range(p, pre, post, 0, p->nz, stream)) return rc;
-        if (int rc = mlb_open_pass_range(p, post, 0, p->nz, stream)) return rc;
+        if (int rc = mlb_step_open_range(p, pre, post, 0, p->nz, stream)) return rc;
         void *tmp = pre; pre = post; post = tmp;
     }
     if (ms) {

@@ -61,6 +61,9 @@ struct StepArgs {
     Geom g;
     int z0;        // first slab plane this launch updates (blockIdx.z = 0)
     int passthrough;  // 1: non-fluid cells are rewritten with fpre's value (see step_cell)
+    int fuse_open;    // 1 (pack kernels, pass-through only): apply the open-boundary pass
+                      // (engine.py:156-180) to the cells of the pack before storing
+    TS inlet[Q];      // equilibrium(1, u_in, 0, 0), storage dtype
     T omega;
     T k[Q];        // moving-wall terms 6 w_i (c_i . u_w), compute dtype
 };
@@ -600,6 +603,28 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a)
             for (int j = 0; j < V; ++j)
                 if ((c[j] & CLS_FLAG) != 0)
                     g[i][j] = o[j];
+        }
+        if (a.fuse_open) {
+            // _OpenBoundaryPass.apply fused into the store: inlet cells take the
+            // constant equilibrium; then outlet cells take the fresh value of
+            // their x-1 neighbour - a cell of the same pack (the host checked
+            // that no outlet cell starts a pack).  Descending j reads each left
+            // neighbour before it could itself be substituted, which is numpy's
+            // "right-hand side first" (engine.py:179-180).
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                if ((c[j] & CLS_FLAG) == 3) {
+#pragma unroll
+                    for (int i = 0; i < Q; ++i)
+                        g[i][j] = Store<TS>::up(a.inlet[i]);
+                }
+#pragma unroll
+            for (int j = V - 1; j >= 1; --j)
+                if ((c[j] & CLS_FLAG) == 4) {
+#pragma unroll
+                    for (int i = 0; i < Q; ++i)
+                        g[i][j] = g[i][j - 1];
+                }
         }
     }
     if (allfluid || a.passthrough) {

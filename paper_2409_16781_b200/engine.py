@@ -275,8 +275,13 @@ class Session:
         # the two buffers agree on non-fluid cells; identical buffers - what
         # every state built by this package starts from (engine.py:148 of the
         # reference) - are a sufficient condition that is cheap to establish.
-        # Otherwise the strict never-written mode is used.
-        self.plan.set_passthrough(same)
+        # Otherwise - or when the geometry chains outlet cells, where the
+        # reference's result depends on stale never-written values and the
+        # library refuses the mode - the strict never-written mode is used.
+        try:
+            self.plan.set_passthrough(same)
+        except ValueError:
+            self.plan.set_passthrough(False)
         self.host_stale = False
 
     def sync_host(self):

@@ -262,6 +262,13 @@ class KernelPlan:
                                              int(z0), int(z1),
                                              _stream_ptr(self.device)))
 
+    def step_open_range(self, fpre, fpost, z0, z1):
+        """One time step's work on planes [z0, z1): fused update + open-
+        boundary pass (fused into one kernel when possible, include/mlb.h)."""
+        _cabi.check(self._lib.mlb_step_open_range(self._plan, fpre.ptr, fpost.ptr,
+                                                  int(z0), int(z1),
+                                                  _stream_ptr(self.device)))
+
     def open_pass(self, fpost):
         _cabi.check(self._lib.mlb_open_pass(self._plan, fpost.ptr,
                                             _stream_ptr(self.device)))

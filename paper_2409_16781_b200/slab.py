@@ -80,8 +80,7 @@ class CudaStepper:
         return field.tensor
 
     def step_range(self, pre, post, z0, z1):
-        self.plan.step_range(pre, post, z0, z1)
-        self.plan.open_pass_range(post, z0, z1)
+        self.plan.step_open_range(pre, post, z0, z1)
 
 
 class DistSlab:

@@ -26,11 +26,25 @@ def geometries3d():
     periodic8[3, 2, 1] = B.SOLID
     periodic8[4, 2, 1] = B.MOVING_WALL
     wide = B.open_mask(72, 4, 3)
+    # open-boundary cells in arbitrary places (the reference's pass works on
+    # index lists, engine.py:161-174): an inlet column mid-domain, a CHAIN of
+    # outlet cells (each copying its west neighbour's pre-pass value), walls
+    open_chain = B.open_mask(16, 6, 4)
+    open_chain[5, 1:5, :] = B.INLET
+    open_chain[13:16, 2:4, 1:3] = B.OUTLET
+    open_chain[9, 3, 2] = B.SOLID
+    open_chain[:, 0, :] = B.SOLID
+    # an outlet cell that starts a 16-byte pack (x % 4 == 0): cannot ride in
+    # the pack kernel, must fall back to the list-driven pass
+    open_unfusable = open_chain.copy()
+    open_unfusable[8, 4, 1:3] = B.OUTLET
     return {"cavity": (cavity, (0.08, 0.0, 0.0), 0.0),
             "cavity16": (cavity16, (0.05, 0.0, -0.03), 0.0),
             "channel40": (channel40, (0.0, 0.0, 0.0), 0.06),
             "periodic8": (periodic8, (0.02, 0.03, -0.04), 0.0),
             "wide": (wide, (0.0, 0.0, 0.0), 0.0),
+            "open_chain": (open_chain, (0.0, 0.0, 0.0), 0.04),
+            "open_unfusable": (open_unfusable, (0.0, 0.0, 0.0), 0.04),
             "cavity_oblique_lid": (cavity, (0.05, 0.0, -0.03), 0.0),
             "channel": (channel, (0.0, 0.0, 0.0), 0.07),
             "duct": (duct, (0.0, 0.0, 0.0), 0.05),

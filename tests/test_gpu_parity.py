@@ -83,7 +83,7 @@ def test_multi_step_with_open_pass_bitwise(geom, tag, rng):
     np.testing.assert_array_equal(got, want)
 
 
-VEC_GEOMS = ["cavity16", "channel40", "periodic8", "wide", "duct"]
+VEC_GEOMS = ["cavity16", "channel40", "periodic8", "wide", "duct", "open_chain", "open_unfusable"]
 
 
 @pytest.mark.parametrize("passthrough", [False, True])
@@ -108,6 +108,12 @@ def test_kernel_variants_never_change_bits(geom, tag, variant, passthrough, rng)
     want = orc.run(a, b, steps)
     plan = make_plan(grid, prec, omega, wall_u, inlet_u)
     plan.set_variant(variant)
+    if passthrough and geom.startswith("open_"):
+        # chained outlet cells: the reference's result depends on the stale
+        # content of a never-written cell, so pass-through must be refused
+        with pytest.raises(ValueError, match="outlet"):
+            plan.set_passthrough(True)
+        return
     plan.set_passthrough(passthrough)
     da, db = plan.alloc(), plan.alloc()
     plan.upload(f, da)
@@ -226,3 +232,23 @@ def test_z_projection_bridge_to_lb2d(case, tag, tol, golden):
     proj = project_2d(got, nz)
     scale = np.abs(want).max()
     assert np.abs(proj - want[None]).max() / scale <= tol
+
+
+@pytest.mark.parametrize("tag", ["f64", "f32", "f16"])
+def test_engine_run_on_chained_outlets_falls_back_to_strict_stores(tag, rng):
+    """engine.run must stay bit-exact on a geometry where pass-through is
+    invalid (chained outlet cells) by keeping the strict store mode."""
+    from paper_2409_16781_b200 import engine
+    from paper_2409_16781_b200.lattice import RelaxationParams
+    grid, wall_u, inlet_u = geometries3d()["open_chain"]
+    prec = PREC[tag]
+    nx, ny, nz = grid.shape
+    rho = rng.uniform(0.9, 1.1, size=grid.shape)
+    u = rng.uniform(-0.05, 0.05, size=(3,) + grid.shape)
+    state = engine.state_from_macroscopic(rho, u[0], u[1], u[2], grid, Layout.ROW, prec,
+                                          params=RelaxationParams.from_omega(1.2),
+                                          inlet_u=inlet_u)
+    f0 = state.f_pre.data.copy()
+    engine.run(state, engine.RunConfig(steps=9, precision=prec))
+    want = make_oracle(grid, 1.2, wall_u, inlet_u).run(f0.copy(), f0.copy(), 9)
+    np.testing.assert_array_equal(state.f_pre.data, want)
