@@ -59,12 +59,21 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=0, help="override the edge length (debug)")
+    ap.add_argument("--edge", "--n", dest="n", type=int, default=0,
+                    help="override the edge length (debug; use --edge under torchrun)")
     ap.add_argument("--precision", default="single", choices=["single", "double", "mixed1"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-slab", action="store_true",
                     help="run the z-slab driver (halo planes, boundary-first overlap) even on 1 GPU")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="halo exchange of the z-slab run: 'peer' = stores into the neighbours' halo "
+                         "planes from inside the fused kernel over CUDA-IPC-mapped peer memory "
+                         "(default; falls back to 'nccl' if the mapping cannot be set up), "
+                         "'nccl' = torch.distributed send/recv")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="debug, not a benchmark: all ranks use device 0 with a gloo control plane, so "
+                         "a one-GPU box can drive the N > 1 code path (peer ring across processes)")
     ap.add_argument("--variant", type=int, default=0, help="kernel variant (tuning; see mlb_plan_set_variant)")
     return ap.parse_args()
 
@@ -76,7 +85,7 @@ def workload_config(n, nz_global, world, prec, omega):
                     f" (BASELINE.json configs[2]{', z-slab weak scaling' if world > 1 else ''})",
         "nx": n, "ny": n, "nz_per_gpu": n, "nz_global": nz_global,
         "re": RE, "u0": U0, "omega": omega,
-        "decomposition": f"{world} z-slab(s), 5-population halos over NCCL" if world > 1 else "single GPU",
+        "decomposition": f"{world} z-slab(s), 5-population halos" if world > 1 else "single GPU",
         "l2_policy": "inputs exceed L2: two population blocks of "
                      f"{19 * n ** 3 * PREC_BYTES[prec] / 1e9:.1f} GB per GPU vs 126 MB L2",
     }
@@ -233,10 +242,15 @@ def main():
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N > 1 must be launched with torch.distributed.run "
                              "(one rank per GPU)")
+    if args.share_gpu:
+        local = 0
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
     prec = Precision.from_token(prec_tok)
     itemsize = prec.storage.itemsize
     nz_global = n * world
@@ -262,7 +276,7 @@ def main():
         m = slab_mask(n, rank, world)
         mask_flat = B.flatten_mask(m)
         lo, hi = slab.exchange_flag_halos(mask_flat.reshape(n, n, n), rank, world,
-                                          device=device)
+                                          device=None if args.share_gpu else device)
         plan = KernelPlan(n, n, n, Layout.ROW, prec, mask_flat, params.omega,
                           (U0, 0.0, 0.0), device=local, halo_lo=lo, halo_hi=hi, slab=True)
         host = pinned_empty((19, cells_rank), prec.storage)
@@ -276,10 +290,54 @@ def main():
     b.tensor.copy_(a.tensor)
     plan.set_passthrough(True)   # both blocks identical: what engine.Session establishes
     runner = None
-    if slab_mode:
-        runner = slab.DistSlab(slab.CudaStepper(plan), n, rank, world)
-        for r in runner.exchange(a):
+    transport = None
+
+    def agree(ok):
+        """Every rank takes the same branch: True only if all ranks say so."""
+        if world == 1:
+            return bool(ok)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        return bool(flag.item())
+
+    def halo_planes(blk):
+        t = blk.tensor
+        return torch.stack([t[q, 0] for q in slab.UP] + [t[q, n + 1] for q in slab.DOWN])
+
+    def make_runner(p, x, y):
+        """DistSlab over the peer ring when it can be set up and delivers the
+        very planes the send/recv exchange delivers, else over send/recv."""
+        why = None
+        if args.transport == "peer":
+            ring, err = None, None
+            try:
+                ring = slab.PeerRing(p, [x, y], rank, world)
+            except Exception as exc:  # cudaIpc* refused (allocator, no P2P, ...)
+                err = f"{type(exc).__name__}: {exc}"
+            if agree(ring is not None):
+                rr = slab.DistSlab(slab.CudaStepper(p), n, rank, world, ring=ring)
+                rr.exchange(x)
+                got = halo_planes(x).clone()
+                if world > 1 and not args.share_gpu:
+                    plain = slab.DistSlab(slab.CudaStepper(p), n, rank, world)
+                    for r in plain.exchange(x):
+                        r.wait()
+                    torch.cuda.synchronize()
+                if agree(torch.equal(got, halo_planes(x))):
+                    return rr, "peer"
+                why = "pre-flight mismatch against send/recv"
+                ring.close()
+            else:
+                why = err or "a peer rank could not map the ring"
+                if ring is not None:
+                    ring.close()
+        rr = slab.DistSlab(slab.CudaStepper(p), n, rank, world)
+        for r in rr.exchange(x):
             r.wait()
+        return rr, "nccl" if why is None else f"nccl (peer ring unavailable: {why})"
+
+    if slab_mode:
+        runner, transport = make_runner(plan, a, b)
 
     def advance(x, y, k):
         if runner is None:
@@ -289,13 +347,26 @@ def main():
 
     # ---- device-timed run: W warm-up, then exactly K steps -------------------
     a, b = advance(a, b, args.warmup)
+    if runner is not None:
+        runner.finish()
     barrier()
+    if runner is not None and runner.ring is not None and world > 1 and not args.share_gpu:
+        # the fused exchange against the plain one, on live data: the halos the
+        # kernels stored into this rank must be the planes send/recv delivers
+        got = halo_planes(a).clone()
+        for r in slab.DistSlab(slab.CudaStepper(plan), n, rank, world).exchange(a):
+            r.wait()
+        torch.cuda.synchronize()
+        if not agree(torch.equal(got, halo_planes(a))):
+            raise SystemExit("bench: fused peer-store halos differ from the send/recv exchange")
     launches0 = _cabi.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record()
         a, b = advance(a, b, args.steps)
         e1.record()
+        if runner is not None:
+            runner.finish()
         barrier()
     launches = _cabi.launch_count() - launches0
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
@@ -314,7 +385,9 @@ def main():
     if not args.no_e2e:
         h2d = 19 * cells_rank * itemsize + cells_rank      # populations + flags
         d2h = 19 * cells_rank * itemsize
-        del a, b
+        if runner is not None and runner.ring is not None:
+            runner.ring.close()
+        del a, b, runner
         plan.close()
         torch.cuda.empty_cache()
         if not slab_mode:
@@ -334,11 +407,12 @@ def main():
                 p.upload(host, x)
                 y.tensor.copy_(x.tensor)
                 p.set_passthrough(True)
-                rr = slab.DistSlab(slab.CudaStepper(p), n, rank, world)
-                for r in rr.exchange(x):
-                    r.wait()
+                rr, _ = make_runner(p, x, y)
                 x, y = rr.run(x, y, k)
+                rr.finish()
                 p.download(x, host)
+                if rr.ring is not None:
+                    rr.ring.close()
                 p.close()
             e2e_once(max(1, args.warmup))
             barrier()
@@ -356,7 +430,7 @@ def main():
                "seconds": dt,
                "call": "engine.run(host state, RunConfig(steps=K)): upload, K steps, download"
                        if not slab_mode else
-                       "per rank: KernelPlan + upload, DistSlab.run(K), download"}
+                       "per rank: KernelPlan + upload, halo transport setup, DistSlab.run(K), download"}
 
 
     if rank != 0:
@@ -392,7 +466,10 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": PREC_DTYPE[prec_tok], "data": "synthetic",
-        "config": workload_config(n, nz_global, world, prec_tok, params.omega),
+        "config": dict(workload_config(n, nz_global, world, prec_tok, params.omega),
+                       **({"halo_transport": transport,
+                           "signal_wait": {1: "stream memory operation", 2: "polling kernel"}[
+                               _cabi.lib().mlb_signal_wait_kind()]} if transport else {})),
         "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(nl.item()),
         "roofline": roofline, "cpu_baseline": cpu_base,
         "check": {"mass": diag["mass"], "max_u": diag["max_u"], "nonfinite": diag["nonfinite"]},

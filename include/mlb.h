@@ -170,6 +170,63 @@ int mlb_inplace_normalize(mlb_plan *plan, void *d_f, int *repr, void *stream);
 int mlb_halo_copy(const mlb_plan *plan, void *d_dst, const void *d_src,
                   int src_nz, int face, void *stream);
 
+/* The same exchange seen from the sender: the boundary plane of the LOCAL
+ * block d_src (a slab of this plan) is written into the halo plane of d_dst, a
+ * neighbour's block with dst_nz planes (peer memory: another GPU's block
+ * mapped with mlb_ipc_open or through peer access).
+ *   face 0: local plane lz = nz-1, c_z = +1 set -> d_dst's halo below (lz = -1)
+ *   face 1: local plane lz = 0,    c_z = -1 set -> d_dst's halo above (lz = dst_nz) */
+int mlb_halo_push(const mlb_plan *plan, const void *d_src, void *d_dst,
+                  int dst_nz, int face, void *stream);
+
+/* Fused update + exchange: mlb_step_open_range on planes [z0, z1) whose
+ * boundary planes ALSO store their 5 crossing populations into the ring
+ * neighbours' halo planes from inside the fused kernel (no pack buffer, no
+ * copy, no collective; the transfer rides on the kernel's own stores over
+ * NVLink).  d_below_post / d_above_post are the neighbours' post blocks with
+ * nz_below / nz_above planes (NULL = no neighbour on that side, or not this
+ * call's business); only a range that contains plane 0 pushes down, only one
+ * that contains plane nz-1 pushes up.  The halos end up byte-identical to
+ * mlb_step_open_range followed by mlb_halo_push.  (With a list-driven open-
+ * boundary pass on those planes that sequence is literally what runs.)
+ * Ordering against the neighbour's own kernels is the caller's job: see
+ * mlb_signal_post / mlb_signal_wait. */
+int mlb_step_push_range(mlb_plan *plan, const void *d_fpre, void *d_fpost,
+                        int z0, int z1, void *d_below_post, int nz_below,
+                        void *d_above_post, int nz_above, void *stream);
+
+/* ---- peer memory: CUDA IPC mapping + stream-ordered signals ---------------
+ * One process per GPU: a rank exports its population blocks and its signal
+ * words (mlb_ipc_export: handle of the enclosing cudaMalloc allocation + the
+ * byte offset of d_ptr inside it), ships the 64 handle bytes to its ring
+ * neighbours by any means (the Python host uses torch.distributed's object
+ * collectives), and the neighbours map them (mlb_ipc_open returns the mapped
+ * BASE; add the offset).  A handle can be opened once per process: callers
+ * cache by handle bytes.  Not for allocations of the same process. */
+#define MLB_IPC_HANDLE_BYTES 64
+#define MLB_SIGNAL_BYTES 256   /* 64 uint32 slots, zero-initialised */
+int mlb_ipc_export(const void *d_ptr, unsigned char handle[MLB_IPC_HANDLE_BYTES],
+                   int64_t *offset);
+int mlb_ipc_open(int device, const unsigned char handle[MLB_IPC_HANDLE_BYTES],
+                 void **d_base);
+int mlb_ipc_close(void *d_base);
+/* Signals: monotone uint32 step counters in device memory.  mlb_signal_post
+ * enqueues "everything earlier on `stream` is visible system-wide, then
+ * *d_slot = value" (d_slot is usually a slot of a NEIGHBOUR's signal block);
+ * mlb_signal_wait stalls `stream` until *d_slot >= value (wrap-around safe)
+ * without blocking the host.  mode 0 = a stream memory operation
+ * (cuStreamWaitValue32: no SM is occupied) when the driver offers it, else a
+ * one-thread polling kernel; 1 = memory operation or error; 2 = polling
+ * kernel. */
+int mlb_signal_create(int device, void **d_sig);
+int mlb_signal_destroy(void *d_sig);
+int mlb_signal_post(void *d_slot, uint32_t value, void *stream);
+int mlb_signal_wait(const void *d_slot, uint32_t value, int mode, void *stream);
+/* what mode 0 resolves to with this driver: 1 = stream memory operation,
+ * 2 = polling kernel */
+int mlb_signal_wait_kind(void);
+int mlb_signal_read(const void *d_slot, uint32_t *out);
+
 /* ---- diagnostics ---------------------------------------------------------
  * mlb_macro: SimState.macro (engine.py:104-118): rho, u in float64 for ALL
  * cells, true division, rho = 0 -> u = 0.  Outputs are dense [nz][ny][nx]

@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libmlb_d3q19.so")
 ABI_VERSION = 1
 
 MLB_F32, MLB_F64 = 0, 1
+IPC_HANDLE_BYTES = 64
 MLB_Z_PERIODIC, MLB_Z_HALO = 0, 1
 MLB_OK, MLB_EINVAL, MLB_ECUDA, MLB_ENOMEM, MLB_EUNSUPPORTED = 0, 1, 2, 3, 4
 
@@ -29,7 +30,10 @@ SYMBOLS = (
     "mlb_step_range", "mlb_step_open_range", "mlb_open_pass", "mlb_open_pass_range",
     "mlb_run_steps",
     "mlb_run_steps_inplace", "mlb_inplace_normalize",
-    "mlb_halo_copy", "mlb_macro", "mlb_diagnostics", "mlb_probe",
+    "mlb_halo_copy", "mlb_halo_push", "mlb_step_push_range",
+    "mlb_ipc_export", "mlb_ipc_open", "mlb_ipc_close",
+    "mlb_signal_create", "mlb_signal_destroy", "mlb_signal_post", "mlb_signal_wait",
+    "mlb_signal_wait_kind", "mlb_signal_read", "mlb_macro", "mlb_diagnostics", "mlb_probe",
     "mlb_step_host",
 )
 
@@ -83,6 +87,17 @@ def lib():
                                       ctypes.POINTER(ctypes.c_float)]),
         "mlb_inplace_normalize": (i, [vp, vp, ctypes.POINTER(ctypes.c_int), vp]),
         "mlb_halo_copy": (i, [vp, vp, vp, i, i, vp]),
+        "mlb_halo_push": (i, [vp, vp, vp, i, i, vp]),
+        "mlb_step_push_range": (i, [vp, vp, vp, i, i, vp, i, vp, i, vp]),
+        "mlb_ipc_export": (i, [vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)]),
+        "mlb_ipc_open": (i, [i, ctypes.c_char_p, ctypes.POINTER(vp)]),
+        "mlb_ipc_close": (i, [vp]),
+        "mlb_signal_create": (i, [i, ctypes.POINTER(vp)]),
+        "mlb_signal_destroy": (i, [vp]),
+        "mlb_signal_post": (i, [vp, ctypes.c_uint32, vp]),
+        "mlb_signal_wait": (i, [vp, ctypes.c_uint32, i, vp]),
+        "mlb_signal_wait_kind": (i, []),
+        "mlb_signal_read": (i, [vp, ctypes.POINTER(ctypes.c_uint32)]),
         "mlb_macro": (i, [vp, vp, vp, vp, vp, vp, vp]),
         "mlb_diagnostics": (i, [vp, vp, dp3, vp]),
         "mlb_probe": (i, [vp, vp, i, i, i, vp, vp]),

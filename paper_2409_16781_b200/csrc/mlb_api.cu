@@ -240,62 +240,94 @@ void fill_args(mlb_plan *p, const void *fpre, void *fpost, int z0, bool fuse_ope
     wall_terms<T>(p->wall_u, a.k);
 }
 
-template <typename TS, int V>
-int launch_vec(mlb_plan *p, const mlb::StepArgs<TS> &a, int lx, int nplanes, cudaStream_t st)
+// the neighbours' halo planes a launch also stores into (mlb_step_push_range)
+struct PushTarget {
+    void *below = nullptr, *above = nullptr;  // the neighbours' post blocks (peer memory)
+    int nz_below = 0, nz_above = 0;
+};
+
+template <typename TS>
+void fill_push(const mlb_plan *p, const PushTarget &t, mlb::PushArgs<TS> &ph)
+{
+    const long long plane = p->lay.plane;
+    for (int j = 0; j < 5; ++j) {
+        // slab below: its halo plane lz = nz (storage nz_below + 1) takes our plane 0, c_z = -1
+        ph.lo[j] = t.below ? static_cast<TS *>(t.below)
+                                 + ((long long)mlb::halo_down(j) * (t.nz_below + 2)
+                                    + (t.nz_below + 1)) * plane
+                           : nullptr;
+        // slab above: its halo plane lz = -1 (storage 0) takes our plane nz-1, c_z = +1
+        ph.hi[j] = t.above ? static_cast<TS *>(t.above)
+                                 + (long long)mlb::halo_up(j) * (t.nz_above + 2) * plane
+                           : nullptr;
+    }
+}
+
+template <typename TS, int V, bool PUSH>
+int launch_vec(mlb_plan *p, const mlb::StepArgs<TS> &a, const mlb::PushArgs<TS> &ph, int lx,
+               int nplanes, cudaStream_t st)
 {
     if (p->nx % V != 0)
         return fail(MLB_EINVAL, "this vectorised kernel needs nx %% %d == 0", V);
     const int rows = 128 / lx;  // rows per 128-thread block
     const dim3 grid((p->nx / V + lx - 1) / lx, (p->ny + rows - 1) / rows, nplanes);
-    if (lx == 8) mlb::step_vec_kernel<TS, V, 8><<<grid, 128, 0, st>>>(a);
-    else if (lx == 16) mlb::step_vec_kernel<TS, V, 16><<<grid, 128, 0, st>>>(a);
-    else mlb::step_vec_kernel<TS, V, 32><<<grid, 128, 0, st>>>(a);
+    if (lx == 8) mlb::step_vec_kernel<TS, V, 8, PUSH><<<grid, 128, 0, st>>>(a, ph);
+    else if (lx == 16) mlb::step_vec_kernel<TS, V, 16, PUSH><<<grid, 128, 0, st>>>(a, ph);
+    else mlb::step_vec_kernel<TS, V, 32, PUSH><<<grid, 128, 0, st>>>(a, ph);
     MLB_LAUNCHED();
     return MLB_OK;
 }
 
-template <typename TS>
-int launch_scalar(mlb_plan *p, const mlb::StepArgs<TS> &a, int bx, int nplanes, cudaStream_t st)
+template <typename TS, bool PUSH>
+int launch_scalar(mlb_plan *p, const mlb::StepArgs<TS> &a, const mlb::PushArgs<TS> &ph, int bx,
+                  int nplanes, cudaStream_t st)
 {
     while (bx > 32 && bx / 2 >= p->nx)
         bx /= 2;
     const dim3 grid((p->nx + bx - 1) / bx, p->ny, nplanes);
     switch (bx) {
-    case 32: mlb::step_kernel<TS, 32><<<grid, 32, 0, st>>>(a); break;
-    case 64: mlb::step_kernel<TS, 64><<<grid, 64, 0, st>>>(a); break;
-    case 128: mlb::step_kernel<TS, 128><<<grid, 128, 0, st>>>(a); break;
-    case 256: mlb::step_kernel<TS, 256><<<grid, 256, 0, st>>>(a); break;
-    default: mlb::step_kernel<TS, 512><<<grid, 512, 0, st>>>(a); break;
+    case 32: mlb::step_kernel<TS, 32, PUSH><<<grid, 32, 0, st>>>(a, ph); break;
+    case 64: mlb::step_kernel<TS, 64, PUSH><<<grid, 64, 0, st>>>(a, ph); break;
+    case 128: mlb::step_kernel<TS, 128, PUSH><<<grid, 128, 0, st>>>(a, ph); break;
+    case 256: mlb::step_kernel<TS, 256, PUSH><<<grid, 256, 0, st>>>(a, ph); break;
+    default: mlb::step_kernel<TS, 512, PUSH><<<grid, 512, 0, st>>>(a, ph); break;
     }
     MLB_LAUNCHED();
     return MLB_OK;
 }
 
+template <typename TS, int V1, int V2, bool PUSH>
+int launch_typed(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cudaStream_t st,
+                 bool fuse_open, int variant, const PushTarget *push)
+{
+    mlb::StepArgs<TS> a;
+    fill_args<TS>(p, fpre, fpost, z0, fuse_open, a);
+    mlb::PushArgs<TS> ph{};
+    if (PUSH)
+        fill_push<TS>(p, *push, ph);
+    const int lx = variant % 1000, n = z1 - z0;
+    if (variant >= 3000) return launch_vec<TS, V2, PUSH>(p, a, ph, lx, n, st);
+    if (variant >= 1000) return launch_vec<TS, V1, PUSH>(p, a, ph, lx, n, st);
+    return launch_scalar<TS, PUSH>(p, a, ph, variant, n, st);
+}
+
 int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cudaStream_t st,
-                bool fuse_open = false)
+                bool fuse_open = false, const PushTarget *push = nullptr)
 {
     const int variant = resolve_variant(p);
     if (!variant_exists(p->dtype, variant))
         return fail(MLB_EINVAL, "kernel variant %d does not exist for dtype code %d", variant,
                     p->dtype);
-    const int lx = variant % 1000, n = z1 - z0;
-    if (p->dtype == MLB_F32) {
-        mlb::StepArgs<float> a;
-        fill_args<float>(p, fpre, fpost, z0, fuse_open, a);
-        return variant >= 1000 ? launch_vec<float, 4>(p, a, lx, n, st)
-                               : launch_scalar<float>(p, a, variant, n, st);
-    }
-    if (p->dtype == MLB_F64) {
-        mlb::StepArgs<double> a;
-        fill_args<double>(p, fpre, fpost, z0, fuse_open, a);
-        return variant >= 1000 ? launch_vec<double, 2>(p, a, lx, n, st)
-                               : launch_scalar<double>(p, a, variant, n, st);
-    }
-    mlb::StepArgs<__half> a;
-    fill_args<__half>(p, fpre, fpost, z0, fuse_open, a);
-    if (variant >= 3000) return launch_vec<__half, 2>(p, a, lx, n, st);
-    if (variant >= 2000) return launch_vec<__half, 4>(p, a, lx, n, st);
-    return launch_scalar<__half>(p, a, variant, n, st);
+    // pack widths per dtype: W = 1 -> 16-byte packs (fp32 / fp64); fp16 storage
+    // has W = 2 (4 halves) and W = 3 (2 halves)
+    if (p->dtype == MLB_F32)
+        return push ? launch_typed<float, 4, 4, true>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push)
+                    : launch_typed<float, 4, 4, false>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push);
+    if (p->dtype == MLB_F64)
+        return push ? launch_typed<double, 2, 2, true>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push)
+                    : launch_typed<double, 2, 2, false>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push);
+    return push ? launch_typed<__half, 4, 2, true>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push)
+                : launch_typed<__half, 4, 2, false>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push);
 }
 
 // in-place (AA pattern) launches: kind 0 = R0 -> R1 step, 1 = R1 -> R0 step, 2 = swap
@@ -510,10 +542,10 @@ const char *mlb_plan_kernel_name(const mlb_plan *p)
     const int v = resolve_variant(p);
     const char *t = p->dtype == MLB_F32 ? "float" : p->dtype == MLB_F64 ? "double" : "__half";
     if (v >= 1000)
-        snprintf(name, sizeof(name), "mlb::step_vec_kernel<%s, %d, %d>", t,
+        snprintf(name, sizeof(name), "mlb::step_vec_kernel<%s, %d, %d, false>", t,
                  pack_cells(p->dtype, v), v % 1000);
     else
-        snprintf(name, sizeof(name), "mlb::step_kernel<%s, %d>", t, v);
+        snprintf(name, sizeof(name), "mlb::step_kernel<%s, %d, false>", t, v);
     return name;
 }
 
@@ -790,6 +822,27 @@ int mlb_inplace_normalize(mlb_plan *p, void *d_f, int *repr, void *stream)
     return MLB_OK;
 }
 
+// 5 crossing populations of one boundary plane of a slab with src_nz planes
+// into a halo plane of a slab with dst_nz planes (same plane shape, dtype).
+static int halo_copy_impl(const mlb_plan *p, void *d_dst, int dst_nz, const void *d_src,
+                          int src_nz, int face, cudaStream_t st)
+{
+    const long long plane = p->lay.plane;
+    const long long src_pop = (long long)(src_nz + 2) * plane;
+    const long long dst_pop = (long long)(dst_nz + 2) * plane;
+    mlb::HaloArgs h;
+    for (int j = 0; j < 5; ++j) {
+        const int q = face == 0 ? mlb::halo_up(j) : mlb::halo_down(j);
+        h.src_off[j] = q * src_pop + (face == 0 ? (long long)src_nz : 1LL) * plane;
+        h.dst_off[j] = q * dst_pop + (face == 0 ? 0LL : (long long)(dst_nz + 1)) * plane;
+    }
+    h.words = plane * p->lay.itemsize / 16;
+    const dim3 grid((unsigned)((h.words + 255) / 256), 5);
+    mlb::halo_copy_kernel<<<grid, 256, 0, st>>>(d_src, d_dst, h, p->lay.itemsize);
+    MLB_LAUNCHED();
+    return MLB_OK;
+}
+
 int mlb_halo_copy(const mlb_plan *p, void *d_dst, const void *d_src, int src_nz, int face,
                   void *stream)
 {
@@ -798,20 +851,53 @@ int mlb_halo_copy(const mlb_plan *p, void *d_dst, const void *d_src, int src_nz,
     if (src_nz < 1 || (face != 0 && face != 1))
         return fail(MLB_EINVAL, "bad src_nz %d / face %d", src_nz, face);
     MLB_CUDA(cudaSetDevice(p->device));
-    static const int UP[5] = {9, 11, 12, 15, 16};     // c_z = +1
-    static const int DOWN[5] = {10, 13, 14, 17, 18};  // c_z = -1
-    const long long plane = p->lay.plane;
-    const long long src_pop = (long long)(src_nz + 2) * plane;
-    mlb::HaloArgs h;
-    for (int j = 0; j < 5; ++j) {
-        const int q = face == 0 ? UP[j] : DOWN[j];
-        h.src_off[j] = q * src_pop + (face == 0 ? (long long)src_nz : 1LL) * plane;
-        h.dst_off[j] = q * p->lay.pop + (face == 0 ? 0LL : (long long)(p->nz + 1)) * plane;
-    }
-    h.words = plane * p->lay.itemsize / 16;
-    const dim3 grid((unsigned)((h.words + 255) / 256), 5);
-    mlb::halo_copy_kernel<<<grid, 256, 0, S(stream)>>>(d_src, d_dst, h, p->lay.itemsize);
-    MLB_LAUNCHED();
+    return halo_copy_impl(p, d_dst, p->nz, d_src, src_nz, face, S(stream));
+}
+
+int mlb_halo_push(const mlb_plan *p, const void *d_src, void *d_dst, int dst_nz, int face,
+                  void *stream)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (!d_dst || !d_src) return fail(MLB_EINVAL, "NULL population block");
+    if (dst_nz < 1 || (face != 0 && face != 1))
+        return fail(MLB_EINVAL, "bad dst_nz %d / face %d", dst_nz, face);
+    MLB_CUDA(cudaSetDevice(p->device));
+    return halo_copy_impl(p, d_dst, dst_nz, d_src, p->nz, face, S(stream));
+}
+
+int mlb_step_push_range(mlb_plan *p, const void *d_fpre, void *d_fpost, int z0, int z1,
+                        void *d_below_post, int nz_below, void *d_above_post, int nz_above,
+                        void *stream)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (!d_fpre || !d_fpost) return fail(MLB_EINVAL, "NULL population block");
+    if (d_fpre == d_fpost)
+        return fail(MLB_EINVAL, "fpre and fpost must be distinct blocks");
+    if (z0 < 0 || z1 > p->nz || z0 > z1)
+        return fail(MLB_EINVAL, "plane range [%d, %d) outside [0, %d)", z0, z1, p->nz);
+    if ((d_below_post && nz_below < 1) || (d_above_post && nz_above < 1))
+        return fail(MLB_EINVAL, "neighbour slab plane counts must be >= 1");
+    if (d_below_post == d_fpre || d_above_post == d_fpre)
+        return fail(MLB_EINVAL, "a push target is the block this step reads");
+    if (z0 == z1) return MLB_OK;
+    // only a launch that covers a boundary plane has anything to push
+    PushTarget t;
+    if (z0 == 0 && d_below_post) { t.below = d_below_post; t.nz_below = nz_below; }
+    if (z1 == p->nz && d_above_post) { t.above = d_above_post; t.nz_above = nz_above; }
+    const bool any = t.below || t.above;
+    MLB_CUDA(cudaSetDevice(p->device));
+    const bool open_cells = p->in_zoff[z1] > p->in_zoff[z0] || p->out_zoff[z1] > p->out_zoff[z0];
+    const bool fuse = can_fuse_open(p, resolve_variant(p));
+    if (!open_cells || fuse)
+        return launch_step(p, d_fpre, d_fpost, z0, z1, S(stream), fuse, any ? &t : nullptr);
+    // list-driven open-boundary pass: it rewrites cells of the boundary plane
+    // after the fused kernel, so the plane is pushed afterwards, as a copy
+    if (int rc = launch_step(p, d_fpre, d_fpost, z0, z1, S(stream))) return rc;
+    if (int rc = mlb_open_pass_range(p, d_fpost, z0, z1, stream)) return rc;
+    if (t.above)
+        if (int rc = halo_copy_impl(p, t.above, t.nz_above, d_fpost, p->nz, 0, S(stream))) return rc;
+    if (t.below)
+        if (int rc = halo_copy_impl(p, t.below, t.nz_below, d_fpost, p->nz, 1, S(stream))) return rc;
     return MLB_OK;
 }
 
@@ -894,6 +980,140 @@ int mlb_step_host(mlb_plan *p, const void *h_fpre, void *h_fpost, void *d_a, voi
     if (int rc = mlb_step(p, d_a, d_b, stream)) return rc;
     if (int rc = mlb_download(p, d_b, h_fpost, stream)) return rc;
     MLB_CUDA(cudaStreamSynchronize(S(stream)));
+    return MLB_OK;
+}
+
+// ---- peer memory: CUDA IPC mapping and stream-ordered signals --------------
+namespace {
+
+// driver entry points, resolved at run time (the library does not link libcuda,
+// so it still loads - and exports every symbol - on a box without a driver)
+typedef int (*cuStreamWaitValue32_t)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+typedef int (*cuMemGetAddressRange_t)(unsigned long long *, size_t *, unsigned long long);
+
+void *driver_entry(const char *name)
+{
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess
+        || q != cudaDriverEntryPointSuccess)
+        return nullptr;
+    return fn;
+}
+
+__global__ void signal_post_kernel(volatile unsigned int *slot, unsigned int value)
+{
+    // everything earlier on this stream (the boundary kernel's stores into the
+    // neighbour's halo) is ordered before the flag, system-wide
+    __threadfence_system();
+    *slot = value;
+}
+
+__global__ void signal_wait_kernel(const volatile unsigned int *slot, unsigned int value)
+{
+    // *slot >= value, wrap-around safe
+    while ((int)(*slot - value) < 0)
+        __nanosleep(200);
+    __threadfence_system();
+}
+
+}  // namespace
+
+int mlb_ipc_export(const void *d_ptr, unsigned char handle[MLB_IPC_HANDLE_BYTES],
+                   int64_t *offset)
+{
+    static_assert(sizeof(cudaIpcMemHandle_t) == MLB_IPC_HANDLE_BYTES, "IPC handle size");
+    if (!d_ptr || !handle || !offset) return fail(MLB_EINVAL, "NULL argument");
+    // the handle names the whole allocation; find its base (torch sub-allocates)
+    static cuMemGetAddressRange_t range = (cuMemGetAddressRange_t)driver_entry("cuMemGetAddressRange");
+    unsigned long long base = (unsigned long long)(uintptr_t)d_ptr;
+    size_t size = 0;
+    if (range) {
+        const int rc = range(&base, &size, (unsigned long long)(uintptr_t)d_ptr);
+        if (rc != 0)
+            return fail(MLB_ECUDA, "cuMemGetAddressRange failed (%d): not a device allocation?", rc);
+    }
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base);
+    if (e != cudaSuccess)
+        return fail(MLB_ECUDA, "cudaIpcGetMemHandle: %s (blocks must come from cudaMalloc - "
+                    "torch's default allocator does; expandable_segments / cudaMallocAsync "
+                    "pools do not)", cudaGetErrorString(e));
+    std::memcpy(handle, &h, sizeof(h));
+    *offset = (int64_t)((unsigned long long)(uintptr_t)d_ptr - base);
+    return MLB_OK;
+}
+
+int mlb_ipc_open(int device, const unsigned char handle[MLB_IPC_HANDLE_BYTES], void **d_base)
+{
+    if (!handle || !d_base) return fail(MLB_EINVAL, "NULL argument");
+    MLB_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    MLB_CUDA(cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess));
+    return MLB_OK;
+}
+
+int mlb_ipc_close(void *d_base)
+{
+    if (!d_base) return MLB_OK;
+    MLB_CUDA(cudaIpcCloseMemHandle(d_base));
+    return MLB_OK;
+}
+
+int mlb_signal_create(int device, void **d_sig)
+{
+    if (!d_sig) return fail(MLB_EINVAL, "NULL argument");
+    MLB_CUDA(cudaSetDevice(device));
+    MLB_CUDA(cudaMalloc(d_sig, MLB_SIGNAL_BYTES));
+    MLB_CUDA(cudaMemset(*d_sig, 0, MLB_SIGNAL_BYTES));
+    MLB_CUDA(cudaDeviceSynchronize());
+    return MLB_OK;
+}
+
+int mlb_signal_destroy(void *d_sig)
+{
+    if (d_sig) MLB_CUDA(cudaFree(d_sig));
+    return MLB_OK;
+}
+
+int mlb_signal_post(void *d_slot, uint32_t value, void *stream)
+{
+    if (!d_slot) return fail(MLB_EINVAL, "NULL slot");
+    signal_post_kernel<<<1, 1, 0, S(stream)>>>(static_cast<volatile unsigned int *>(d_slot), value);
+    MLB_LAUNCHED();
+    return MLB_OK;
+}
+
+int mlb_signal_wait(const void *d_slot, uint32_t value, int mode, void *stream)
+{
+    if (!d_slot) return fail(MLB_EINVAL, "NULL slot");
+    if (mode < 0 || mode > 2) return fail(MLB_EINVAL, "wait mode must be 0 (auto), 1 or 2");
+    static cuStreamWaitValue32_t wait32 = (cuStreamWaitValue32_t)driver_entry("cuStreamWaitValue32");
+    if (mode != 2 && wait32) {
+        // CU_STREAM_WAIT_VALUE_GEQ = 0: the stream stalls in the front end, no SM is held
+        const int rc = wait32(S(stream), (unsigned long long)(uintptr_t)d_slot, value, 0u);
+        if (rc == 0) return MLB_OK;
+        if (mode == 1) return fail(MLB_ECUDA, "cuStreamWaitValue32 failed (%d)", rc);
+    } else if (mode == 1) {
+        return fail(MLB_EUNSUPPORTED, "cuStreamWaitValue32 is not available from this driver");
+    }
+    signal_wait_kernel<<<1, 1, 0, S(stream)>>>(static_cast<const volatile unsigned int *>(d_slot),
+                                                 value);
+    MLB_LAUNCHED();
+    return MLB_OK;
+}
+
+int mlb_signal_wait_kind(void)
+{
+    static const bool memop = driver_entry("cuStreamWaitValue32") != nullptr;
+    return memop ? 1 : 2;
+}
+
+int mlb_signal_read(const void *d_slot, uint32_t *out)
+{
+    if (!d_slot || !out) return fail(MLB_EINVAL, "NULL argument");
+    MLB_CUDA(cudaMemcpy(out, d_slot, sizeof(uint32_t), cudaMemcpyDeviceToHost));
     return MLB_OK;
 }
 

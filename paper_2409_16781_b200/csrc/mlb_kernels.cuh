@@ -68,6 +68,27 @@ struct StepArgs {
     T k[Q];        // moving-wall terms 6 w_i (c_i . u_w), compute dtype
 };
 
+// Fused halo exchange (z-slabs over peer memory).  The launch
+// that updates a slab's boundary plane also stores the 5 populations that
+// cross that face straight into the ring neighbour's halo plane - a pointer
+// into the neighbour GPU's population block, mapped over NVLink (CUDA IPC /
+// peer access): plane lz = nz-1, c_z = +1 set -> `hi[j]`, the start of
+// population UP[j]'s halo plane lz = -1 of the slab above; plane lz = 0,
+// c_z = -1 set -> `lo[j]`, population DOWN[j]'s halo plane lz = nz of the slab
+// below.  The halo planes have the row pitch of this slab (same nx, ny,
+// dtype).  A NULL first pointer disables that face.  The values and the set
+// of cells stored are exactly those of the local store, so the neighbour's
+// halo ends up byte-identical to a copy of the plane after the launch.
+__host__ __device__ constexpr int halo_up(int j)    // c_z = +1: 9, 11, 12, 15, 16
+{ return j == 0 ? 9 : j == 1 ? 11 : j == 2 ? 12 : j == 3 ? 15 : 16; }
+__host__ __device__ constexpr int halo_down(int j)  // c_z = -1: 10, 13, 14, 17, 18
+{ return j == 0 ? 10 : j == 1 ? 13 : j == 2 ? 14 : j == 3 ? 17 : 18; }
+template <typename TS>
+struct PushArgs {
+    TS *lo[5];
+    TS *hi[5];
+};
+
 // Per-cell class word, built once from the flags (build_cls_kernel):
 //   bits 0..2   the reference's flag code (boundaries.py:20-24)
 //   bit  2 + i  (i = 1..18) the source cell of direction i is a wall (SOLID or
@@ -242,9 +263,9 @@ __host__ __device__ constexpr int opp(int i)
 //  * wall-adjacent lanes patch their bounced directions afterwards from the
 //    link bits of the class word - no flag reads, no 3-way branches; the
 //    patch loads hit lines the same warp has just pulled.
-template <typename TS>
-__device__ __forceinline__ void step_cell(const StepArgs<TS> &a, const int x, const int y,
-                                          const int lz)
+template <typename TS, bool PUSH>
+__device__ __forceinline__ void step_cell(const StepArgs<TS> &a, const PushArgs<TS> &ph,
+                                          const int x, const int y, const int lz)
 {
     using T = typename Store<TS>::C;
     const Geom &gm = a.g;
@@ -311,15 +332,28 @@ __device__ __forceinline__ void step_cell(const StepArgs<TS> &a, const int x, co
 #pragma unroll
     for (int i = 0; i < Q; ++i)
         a.post[i][d] = Store<TS>::down(g[i]);
+    if constexpr (PUSH) {
+        const int o = y * xp + x;  // offset inside a plane
+        if (lz == 0 && ph.lo[0] != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 5; ++j)
+                ph.lo[j][o] = Store<TS>::down(g[halo_down(j)]);
+        }
+        if (lz == gm.nz - 1 && ph.hi[0] != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 5; ++j)
+                ph.hi[j][o] = Store<TS>::down(g[halo_up(j)]);
+        }
+    }
 }
 
-template <typename TS, int BX>
-__global__ void __launch_bounds__(BX) step_kernel(const StepArgs<TS> a)
+template <typename TS, int BX, bool PUSH>
+__global__ void __launch_bounds__(BX) step_kernel(const StepArgs<TS> a, const PushArgs<TS> ph)
 {
     const int x = blockIdx.x * BX + threadIdx.x;
     if (x >= a.g.nx)
         return;
-    step_cell<TS>(a, x, blockIdx.y, a.z0 + blockIdx.z);
+    step_cell<TS, PUSH>(a, ph, x, blockIdx.y, a.z0 + blockIdx.z);
 }
 
 // ---------------------------------------------------------------------------
@@ -599,8 +633,9 @@ __device__ __forceinline__ void pull_pack(const TS *__restrict__ row, int x0, in
     X(13, -1, zq, rc) X(14, 1, zq, rc)  X(15, 0, zm, rm)  X(16, 0, zm, rq)       \
     X(17, 0, zq, rq)  X(18, 0, zq, rm)
 
-template <typename TS, int V, int LX>
-__global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a)
+template <typename TS, int V, int LX, bool PUSH>
+__global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
+                                                          const PushArgs<TS> ph)
 {
     using T = typename Store<TS>::C;
     constexpr int RPW = 32 / LX;        // rows per warp
@@ -714,6 +749,29 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a)
                 for (int i = 0; i < Q; ++i)
                     a.post[i][d + j] = Store<TS>::down(g[i][j]);
             }
+    }
+    if constexpr (PUSH) {
+        // the crossing populations of a boundary plane, also into the ring
+        // neighbour's halo plane (peer memory): same values, same cells
+        const bool lo = lz == 0 && ph.lo[0] != nullptr;
+        const bool hi = lz == gm.nz - 1 && ph.hi[0] != nullptr;
+        if (lo || hi) {
+            const int o = rc + x0;
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                if (allfluid || a.passthrough) {
+                    if (lo) PackIO<TS, V>::store(ph.lo[j] + o, g[halo_down(j)]);
+                    if (hi) PackIO<TS, V>::store(ph.hi[j] + o, g[halo_up(j)]);
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < V; ++jj)
+                        if ((c[jj] & CLS_FLAG) == 0) {
+                            if (lo) ph.lo[j][o + jj] = Store<TS>::down(g[halo_down(j)][jj]);
+                            if (hi) ph.hi[j][o + jj] = Store<TS>::down(g[halo_up(j)][jj]);
+                        }
+                }
+            }
+        }
     }
 }
 

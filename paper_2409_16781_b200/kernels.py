@@ -319,6 +319,26 @@ class KernelPlan:
                                             int(src.nz), int(face),
                                             _stream_ptr(self.device)))
 
+    def halo_push(self, src, dst_ptr, dst_nz, face):
+        """The same exchange from the sender's side: the boundary plane of the
+        local block `src` into the halo plane of a neighbour's block given as
+        a raw device pointer (peer memory, see slab.PeerRing)."""
+        _cabi.check(self._lib.mlb_halo_push(self._plan, src.ptr, ctypes.c_void_p(dst_ptr),
+                                            int(dst_nz), int(face),
+                                            _stream_ptr(self.device)))
+
+    def step_push_range(self, fpre, fpost, z0, z1, below=None, above=None):
+        """`step_open_range` whose boundary planes also store their crossing
+        populations into the ring neighbours' halo planes from inside the
+        fused kernel.  `below` / `above` are (device pointer, nz) of the
+        neighbours' post blocks, or None."""
+        bp, bn = below if below is not None else (None, 0)
+        ap, an = above if above is not None else (None, 0)
+        _cabi.check(self._lib.mlb_step_push_range(
+            self._plan, fpre.ptr, fpost.ptr, int(z0), int(z1),
+            ctypes.c_void_p(bp), int(bn), ctypes.c_void_p(ap), int(an),
+            _stream_ptr(self.device)))
+
     # -- diagnostics -------------------------------------------------------
     def macro(self, dev):
         """rho, ux, uy, uz as float64 CUDA tensors of shape (nz, ny, nx)."""

@@ -21,11 +21,25 @@ the wrap link carries data nobody reads, one code path either way.
 Per step on each rank (DistSlab.step):
   1. boundary planes lz = 0 and lz = nz-1 (+ their open-boundary cells) on a
      high-priority stream;
-  2. the exchange (NCCL send/recv over NVLink via torch.distributed) as soon
-     as (1) is done;
+  2. the exchange as soon as (1) is done;
   3. the interior planes on the main stream, concurrently with (2);
   4. join, swap.
 The data path has no collective - only the two neighbour exchanges.
+
+Two transports for (2):
+* `PeerRing` (the product path on one NVSwitch box): every rank maps its ring
+  neighbours' population blocks (CUDA IPC) and the boundary-plane launch of (1)
+  stores the crossing populations straight into the neighbour's halo planes
+  from inside the fused kernel - no pack buffer, no copy kernel, no NCCL call
+  on the data path.  Ordering between ranks is a pair of monotone step
+  counters per rank in device memory: after its boundary launches of step t a
+  rank posts t into both neighbours' counters; before its boundary launches of
+  step t it makes its stream wait (stream memory operation, no host sync)
+  until both neighbours have posted t-1 - which says both that the halos it is
+  about to read are complete and that the halos it is about to overwrite have
+  been read.
+* torch.distributed send/recv (NCCL over NVLink on GPUs, gloo on CPU): the
+  portable fallback, and what the CPU tests drive.
 
 `DistSlab` is written against a small "stepper" interface so the same
 driver code runs under `gloo` on CPU tensors in the tests (with the CPU
@@ -83,6 +97,125 @@ class CudaStepper:
         self.plan.step_open_range(pre, post, z0, z1)
 
 
+class PeerRing:
+    """The ring neighbours' blocks and step counters, mapped into this process.
+
+    `blocks` are this rank's two population blocks (DeviceFields of `plan`);
+    every rank passes its own and learns the others' through one object
+    all-gather of CUDA IPC handles (64 bytes each) - control plane only.
+    With world == 1 the ring closes on the rank's own blocks.
+    """
+
+    SLOT_FROM_BELOW, SLOT_FROM_ABOVE = 0, 128  # byte offsets inside the signal block
+
+    def __init__(self, plan, blocks, rank=0, world=1, group=None, wait_mode=0):
+        import ctypes
+        from . import _cabi
+        self.plan, self.blocks = plan, list(blocks)
+        self.rank, self.world, self.group = rank, world, group
+        self.wait_mode = int(wait_mode)
+        self._lib = lib = _cabi.lib()
+        self._ct = ctypes
+        self._check = _cabi.check
+        self.t = 0           # steps posted so far
+        self._opened = {}    # handle bytes -> mapped base address
+        dev = plan.device.index
+        sig = ctypes.c_void_p()
+        _cabi.check(lib.mlb_signal_create(dev, ctypes.byref(sig)))
+        self.sig = sig.value
+        below, above = ring_neighbours(rank, world)
+        if world == 1:
+            mine = {"nz": plan.nz, "blocks": [b.tensor.data_ptr() for b in self.blocks],
+                    "sig": self.sig}
+            self.below = self.above = mine
+            return
+        import torch.distributed as dist
+        card = {"nz": plan.nz, "blocks": [self._export(b.tensor.data_ptr()) for b in self.blocks],
+                "sig": self._export(self.sig)}
+        cards = [None] * world
+        dist.all_gather_object(cards, card, group=group)
+        self.below = self._map(cards[below])
+        self.above = self.below if above == below else self._map(cards[above])
+
+    def _export(self, ptr):
+        ct = self._ct
+        handle = ct.create_string_buffer(64)
+        off = ct.c_int64()
+        self._check(self._lib.mlb_ipc_export(ct.c_void_p(ptr), handle, ct.byref(off)))
+        return handle.raw, off.value
+
+    def _open(self, handle, off):
+        ct = self._ct
+        if handle not in self._opened:
+            base = ct.c_void_p()
+            self._check(self._lib.mlb_ipc_open(self.plan.device.index, handle, ct.byref(base)))
+            self._opened[handle] = base.value
+        return self._opened[handle] + off
+
+    def _map(self, card):
+        return {"nz": card["nz"], "blocks": [self._open(*h) for h in card["blocks"]],
+                "sig": self._open(*card["sig"])}
+
+    def index(self, block):
+        for k, b in enumerate(self.blocks):
+            if b is block:
+                return k
+        raise ValueError("block is not one of the ring's two population blocks")
+
+    def targets(self, k):
+        """((below ptr, nz), (above ptr, nz)) for pushes out of local block k."""
+        return ((self.below["blocks"][k], self.below["nz"]),
+                (self.above["blocks"][k], self.above["nz"]))
+
+    def _stream(self):
+        return self._ct.c_void_p(torch.cuda.current_stream(self.plan.device).cuda_stream)
+
+    def wait(self, value):
+        """Current stream waits until both neighbours have posted `value`."""
+        for off in (self.SLOT_FROM_BELOW, self.SLOT_FROM_ABOVE):
+            self._check(self._lib.mlb_signal_wait(self._ct.c_void_p(self.sig + off), value,
+                                                  self.wait_mode, self._stream()))
+
+    def post(self, value):
+        """After everything enqueued so far on the current stream: tell both
+        neighbours this rank's boundary planes of step `value` are done (its
+        pushes into their halos have landed, their halos in the other block
+        have been read)."""
+        # I am the slab ABOVE my below-neighbour, and BELOW my above-neighbour
+        self._check(self._lib.mlb_signal_post(
+            self._ct.c_void_p(self.below["sig"] + self.SLOT_FROM_ABOVE), value, self._stream()))
+        self._check(self._lib.mlb_signal_post(
+            self._ct.c_void_p(self.above["sig"] + self.SLOT_FROM_BELOW), value, self._stream()))
+        self.t = value
+
+    def barrier(self):
+        torch.cuda.synchronize(self.plan.device)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier(group=self.group)
+
+    def exchange(self, k):
+        """Fill the neighbours' halo planes of block k from this rank's
+        boundary planes (setup; the per-step exchange is fused into the
+        kernel).  Collective: returns when every rank's halos are filled."""
+        self.barrier()
+        (bp, bn), (ap, an) = self.targets(k)
+        self.plan.halo_push(self.blocks[k], ap, an, face=0)
+        self.plan.halo_push(self.blocks[k], bp, bn, face=1)
+        self.barrier()
+
+    def close(self):
+        if getattr(self, "sig", None) is None:
+            return
+        self.barrier()   # nobody is still storing into a mapping we are about to drop
+        for base in self._opened.values():
+            self._lib.mlb_ipc_close(self._ct.c_void_p(base))
+        self._opened = {}
+        self.barrier()
+        self._lib.mlb_signal_destroy(self._ct.c_void_p(self.sig))
+        self.sig = None
+
+
 class DistSlab:
     """One rank's slab of a z-decomposed run over torch.distributed.
 
@@ -93,13 +226,20 @@ class DistSlab:
     """
 
     def __init__(self, stepper, nz_local, rank=0, world=1, group=None,
-                 overlap=True):
+                 overlap=True, ring=None, force_dist=False):
         self.stepper = stepper
         self.nz = int(nz_local)
         self.rank, self.world, self.group = rank, world, group
         self.below, self.above = ring_neighbours(rank, world)
         self.cuda = isinstance(stepper, CudaStepper)
         self.overlap = bool(overlap) and self.cuda and self.nz >= 3
+        self.ring = ring  # PeerRing: fused peer-store exchange instead of send/recv
+        # world == 1 normally closes the ring with local copies; force_dist sends
+        # the planes through torch.distributed to this same rank instead (lets a
+        # one-GPU box exercise the NCCL send/recv path)
+        self.force_dist = bool(force_dist)
+        if ring is not None and not self.cuda:
+            raise ValueError("the peer-memory ring needs the CUDA stepper")
 
     # -- halo exchange -----------------------------------------------------
     def _ops(self, t):
@@ -113,9 +253,12 @@ class DistSlab:
 
     def exchange(self, block):
         """Fill both halo planes of `block` from the ring neighbours."""
+        if self.ring is not None:
+            self.ring.exchange(self.ring.index(block))
+            return []
         t = self.stepper.tensor(block)
         sends, recvs = self._ops(t)
-        if self.world == 1:
+        if self.world == 1 and not self.force_dist:
             for (src, _), (dst, _) in zip(sends, recvs):
                 dst.copy_(src)
             return []
@@ -136,6 +279,8 @@ class DistSlab:
         every plane, then the halo exchange of `post`).  Returns when the
         work is enqueued (CUDA) or done (CPU); the caller swaps."""
         st, nz = self.stepper, self.nz
+        if self.ring is not None:
+            return self._step_ring(pre, post)
         if not self.overlap:
             st.step_range(pre, post, 0, nz)
             for r in self.exchange(post):
@@ -156,6 +301,40 @@ class DistSlab:
         done = torch.cuda.Event()
         done.record(st.hi)
         main.wait_event(done)
+
+    def _step_ring(self, pre, post):
+        """One step with the exchange fused into the boundary-plane launches
+        (PeerRing).  Step t's boundary launches wait for both neighbours'
+        post of t-1, push into the neighbours' halos of the same-index block,
+        and post t."""
+        st, nz, ring = self.stepper, self.nz, self.ring
+        plan = st.plan
+        below, above = ring.targets(ring.index(post))
+        t = ring.t + 1
+        if not self.overlap:
+            ring.wait(t - 1)
+            plan.step_push_range(pre, post, 0, nz, below, above)
+            ring.post(t)
+            return
+        main = torch.cuda.current_stream(st.device)
+        ready = torch.cuda.Event()
+        ready.record(main)
+        st.hi.wait_event(ready)
+        with torch.cuda.stream(st.hi):
+            ring.wait(t - 1)
+            plan.step_push_range(pre, post, 0, 1, below, None)
+            plan.step_push_range(pre, post, nz - 1, nz, None, above)
+            ring.post(t)
+        st.step_range(pre, post, 1, nz - 1)  # interior: no halo, no neighbour involved
+        done = torch.cuda.Event()
+        done.record(st.hi)
+        main.wait_event(done)
+
+    def finish(self):
+        """After the last step, before anyone reads halos or frees blocks:
+        every rank's pushes have landed."""
+        if self.ring is not None:
+            self.ring.barrier()
 
     def run(self, a, b, nsteps):
         """`nsteps` steps alternating a -> b -> a; returns (newest, other)."""
@@ -195,4 +374,4 @@ def exchange_flag_halos(flags_slab, rank, world, group=None, device=None):
 
 
 __all__ = ["partition", "ring_neighbours", "slab_halo_flags", "CudaStepper",
-           "DistSlab", "exchange_flag_halos", "Q"]
+           "PeerRing", "DistSlab", "exchange_flag_halos", "Q"]

@@ -1,0 +1,146 @@
+"""The fused peer-store halo exchange across PROCESSES: two ranks, each with
+its own CUDA context, map each other's population blocks and step counters
+through CUDA IPC and run the real DistSlab + PeerRing driver.  The box has one
+GPU, so both ranks share device 0 - the memory mapping, the in-kernel stores
+into the neighbour's halo planes and the stream-ordered signal protocol are
+exactly what runs with one rank per GPU; only the wire (same-device instead
+of NVLink) differs.  The control plane (handle exchange, barriers) is gloo.
+The gathered result must be BITWISE the single-domain run."""
+
+import os
+import signal
+import socket
+
+import numpy as np
+import pytest
+
+from oracle.cpu import CpuOracle
+from paper_2409_16781_b200 import boundaries as B
+from paper_2409_16781_b200.fields import Layout, Precision
+
+from .helpers import geometries3d, random_block
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, geom, tag, steps, omega, wait_mode, overlap, passthrough, out_dir):
+    signal.alarm(240)  # a protocol bug must not hang the box
+    import torch
+    import torch.distributed as dist
+    from paper_2409_16781_b200 import slab
+    from paper_2409_16781_b200.kernels import KernelPlan
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        grid, wall_u, inlet_u = geometries3d()[geom]
+        prec = {"f64": Precision.DOUBLE, "f32": Precision.SINGLE, "f16": Precision.MIXED1}[tag]
+        nx, ny, nz = grid.shape
+        flags = B.flatten_mask(grid).reshape(nz, ny, nx)
+        f = random_block(np.random.default_rng(20240917), grid.size, prec.storage)
+        z0, z1 = slab.partition(nz, world)[rank]
+        n = z1 - z0
+        lo, hi = slab.exchange_flag_halos(flags[z0:z1], rank, world)
+        plan = KernelPlan(nx, ny, n, Layout.ROW, prec, flags[z0:z1], omega, wall_u,
+                          inlet_u=inlet_u, halo_lo=lo, halo_hi=hi, slab=True)
+        part = np.ascontiguousarray(f.reshape(19, nz, ny, nx)[:, z0:z1]).reshape(19, -1)
+        blocks = [plan.alloc(), plan.alloc()]
+        for blk in blocks:
+            blk.tensor.fill_(float("nan"))
+            plan.upload(part, blk)
+        if passthrough:
+            try:
+                plan.set_passthrough(True)
+            except ValueError:
+                pass
+        ring = slab.PeerRing(plan, blocks, rank, world, wait_mode=wait_mode)
+        runner = slab.DistSlab(slab.CudaStepper(plan), n, rank, world, overlap=overlap, ring=ring)
+        runner.exchange(blocks[0])
+        newest, _ = runner.run(blocks[0], blocks[1], steps)
+        runner.finish()
+        out = np.empty_like(part)
+        plan.download(newest, out)
+        np.save(os.path.join(out_dir, f"slab{rank}.npy"), out.reshape(19, n, ny, nx))
+        ring.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("wait_mode", [0, 2])
+@pytest.mark.parametrize("geom,tag,world,overlap,passthrough", [
+    ("cavity_oblique_lid", "f64", 2, False, False),
+    ("cavity16", "f32", 2, True, True),
+    ("channel40", "f32", 2, True, True),
+    ("channel", "f64", 3, True, False),
+    ("open_unfusable", "f32", 2, False, True),
+    ("periodic8", "f16", 2, False, True),
+    ("cavity16", "f32", 3, False, True),
+])
+def test_peer_ring_across_processes(geom, tag, world, overlap, passthrough, wait_mode, tmp_path):
+    import torch.multiprocessing as mp
+    steps, omega = 7, 1.3
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    nx, ny, nz = grid.shape
+    dtype = {"f64": np.float64, "f32": np.float32, "f16": np.float16}[tag]
+    f = random_block(np.random.default_rng(20240917), grid.size, dtype)
+    want = CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u, inlet_u).run(
+        f.copy(), f.copy(), steps)
+    mp.spawn(_worker, args=(world, _free_port(), geom, tag, steps, omega, wait_mode, overlap,
+                            passthrough, str(tmp_path)), nprocs=world, join=True)
+    got = np.concatenate([np.load(tmp_path / f"slab{r}.npy") for r in range(world)], axis=1)
+    np.testing.assert_array_equal(got.reshape(19, -1), want)
+
+
+def _nccl_worker(rank, port, geom, steps, omega, out_dir):
+    signal.alarm(240)
+    import torch
+    import torch.distributed as dist
+    from paper_2409_16781_b200 import slab
+    from paper_2409_16781_b200.kernels import KernelPlan
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        grid, wall_u, inlet_u = geometries3d()[geom]
+        nx, ny, nz = grid.shape
+        flags = B.flatten_mask(grid).reshape(nz, ny, nx)
+        f = random_block(np.random.default_rng(20240917), grid.size, np.float32)
+        lo, hi = slab.exchange_flag_halos(flags, 0, 1)
+        plan = KernelPlan(nx, ny, nz, Layout.ROW, Precision.SINGLE, flags, omega, wall_u,
+                          inlet_u=inlet_u, halo_lo=lo, halo_hi=hi, slab=True)
+        blocks = [plan.alloc(), plan.alloc()]
+        for blk in blocks:
+            blk.tensor.fill_(float("nan"))
+            plan.upload(f, blk)
+        runner = slab.DistSlab(slab.CudaStepper(plan), nz, 0, 1, force_dist=True)
+        for r in runner.exchange(blocks[0]):
+            r.wait()
+        newest, _ = runner.run(blocks[0], blocks[1], steps)
+        out = np.empty_like(f)
+        plan.download(newest, out)
+        np.save(os.path.join(out_dir, "nccl.npy"), out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("geom", ["cavity16", "channel40"])
+def test_send_recv_transport_over_nccl(geom, tmp_path):
+    """The send/recv fallback on the real NCCL backend: one rank whose ring
+    closes on itself THROUGH torch.distributed (batch_isend_irecv of the ten
+    crossing planes, boundary-first overlap on the high-priority stream)."""
+    import torch.multiprocessing as mp
+    steps, omega = 6, 1.3
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    nx, ny, nz = grid.shape
+    f = random_block(np.random.default_rng(20240917), grid.size, np.float32)
+    want = CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u, inlet_u).run(
+        f.copy(), f.copy(), steps)
+    mp.spawn(_nccl_worker, args=(_free_port(), geom, steps, omega, str(tmp_path)),
+             nprocs=1, join=True)
+    np.testing.assert_array_equal(np.load(tmp_path / "nccl.npy"), want)

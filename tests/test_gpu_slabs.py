@@ -109,3 +109,45 @@ def test_distslab_overlap_path_single_rank(geom, rng):
     out = np.empty_like(f)
     plan.download(newest, out)
     np.testing.assert_array_equal(out, want)
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+@pytest.mark.parametrize("tag", ["f64", "f32", "f16"])
+@pytest.mark.parametrize("geom", ["cavity_oblique_lid", "channel", "periodic", "cavity16",
+                                  "channel40", "open_chain", "open_unfusable"])
+def test_peer_ring_single_rank(geom, tag, overlap, rng):
+    """The fused exchange (PeerRing): the boundary-plane launches store the
+    crossing populations into the ring neighbour's halo planes themselves.
+    World = 1, so the neighbour is the slab's own block; strict and
+    pass-through stores, fused and list-driven open-boundary pass."""
+    from paper_2409_16781_b200 import slab
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    prec = {"f64": Precision.DOUBLE, "f32": Precision.SINGLE, "f16": Precision.MIXED1}[tag]
+    f = random_block(rng, grid.size, prec.storage)
+    steps, omega = 5, 1.4
+    want = single_domain(grid, prec, omega, wall_u, inlet_u, f, steps)
+    for passthrough in (False, True):
+        (plan, blocks, z0, z1), = make_slabs(grid, prec, omega, wall_u, inlet_u, f, 1)
+        if passthrough:
+            try:
+                plan.set_passthrough(True)
+            except ValueError:
+                continue  # chained outlets: the library refuses the mode
+        ring = slab.PeerRing(plan, blocks)
+        runner = slab.DistSlab(slab.CudaStepper(plan), z1 - z0, overlap=overlap, ring=ring)
+        assert runner.overlap == (overlap and z1 - z0 >= 3)
+        runner.exchange(blocks[0])
+        newest, _ = runner.run(blocks[0], blocks[1], steps)
+        runner.finish()
+        out = np.empty_like(f)
+        plan.download(newest, out)
+        np.testing.assert_array_equal(out, want)
+        # the halos of the newest block are what a plain halo copy would deliver
+        got = newest.tensor.clone()
+        plan.halo_copy(newest, newest, face=0)
+        plan.halo_copy(newest, newest, face=1)
+        import torch
+        nx = plan.nx
+        fluidish = torch.isfinite(got[:, :, :, :nx].float())
+        assert torch.equal(got[:, :, :, :nx][fluidish], newest.tensor[:, :, :, :nx][fluidish])
+        ring.close()
