@@ -108,6 +108,12 @@ int mlb_plan_set_flags(mlb_plan *plan, const uint8_t *h_flags,
 /* the flag bytes back, dense [nz][ny][nx], for bit-exact geometry checks */
 int mlb_plan_get_flags(const mlb_plan *plan, uint8_t *h_flags);
 
+/* out[0] = distinct (class word, moving-wall link bits) pairs in the plan's
+ * dictionary (the kernels read one index byte per cell), out[1] = cells beyond
+ * its 254 entries, which read full-width words instead (0 for ordinary
+ * geometries) */
+int mlb_plan_geometry_stats(const mlb_plan *plan, int64_t out[2]);
+
 /* ---- layout conversion: host dense (Q, N) <-> device padded SoA -----------
  * Interior planes only; halo planes of d_f are left untouched.  h_dense may
  * be pageable or pinned; the copies are asynchronous on `stream` when it is

@@ -26,7 +26,7 @@ SYMBOLS = (
     "mlb_plan_create", "mlb_plan_destroy", "mlb_plan_get_layout",
     "mlb_plan_set_physics", "mlb_plan_set_variant", "mlb_plan_set_passthrough",
     "mlb_plan_kernel_name", "mlb_plan_set_flags",
-    "mlb_plan_get_flags", "mlb_upload", "mlb_download", "mlb_step",
+    "mlb_plan_get_flags", "mlb_plan_geometry_stats", "mlb_upload", "mlb_download", "mlb_step",
     "mlb_step_range", "mlb_step_open_range", "mlb_open_pass", "mlb_open_pass_range",
     "mlb_run_steps",
     "mlb_run_steps_inplace", "mlb_inplace_normalize",
@@ -75,6 +75,7 @@ def lib():
         "mlb_plan_kernel_name": (ctypes.c_char_p, [vp]),
         "mlb_plan_set_flags": (i, [vp, vp, vp, vp]),
         "mlb_plan_get_flags": (i, [vp, vp]),
+        "mlb_plan_geometry_stats": (i, [vp, ctypes.POINTER(ctypes.c_int64)]),
         "mlb_upload": (i, [vp, vp, vp, vp]),
         "mlb_download": (i, [vp, vp, vp, vp]),
         "mlb_step": (i, [vp, vp, vp, vp]),

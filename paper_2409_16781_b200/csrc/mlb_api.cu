@@ -55,8 +55,15 @@ struct mlb_plan {
     mlb::Geom g{};
     bool have_flags = false;
     uint8_t *d_flags = nullptr;  // padded flag block incl. halo planes
-    uint32_t *d_cls = nullptr;     // per-cell class words, same shape
-    uint32_t *d_mlinks = nullptr;  // per-cell moving-wall link bits, same shape
+    // what the kernels read: one kind byte per cell (same shape as d_flags) + the
+    // dictionary of distinct (class word, moving-wall link bits) pairs
+    uint8_t *d_kind = nullptr;
+    unsigned long long *d_tab = nullptr;  // [256]
+    // full-width per-cell class words / link bits: scratch of the build, kept
+    // only when the geometry has more than 254 distinct pairs (escape cells)
+    uint32_t *d_cls = nullptr;
+    uint32_t *d_mlinks = nullptr;
+    unsigned int n_escape = 0, n_kinds = 0;
     // open-boundary index lists, sorted by (lz, y, x); *_zoff[lz] = first entry of plane lz
     long long n_in = 0, n_out = 0;
     long long *d_in = nullptr, *d_out = nullptr;
@@ -107,6 +114,16 @@ void set_geom(mlb_plan *p)
         p->g.zlo_src = 0;
         p->g.zhi_src = p->nz + 1;
     }
+}
+
+mlb::ClsTab cls_tab(const mlb_plan *p)
+{
+    mlb::ClsTab t;
+    t.kind = p->d_kind;
+    t.tab = reinterpret_cast<const uint2 *>(p->d_tab);  // little-endian: x = class word, y = links
+    t.cls_full = p->d_cls;
+    t.ml_full = p->d_mlinks;
+    return t;
 }
 
 template <typename T>
@@ -226,8 +243,7 @@ void fill_args(mlb_plan *p, const void *fpre, void *fpost, int z0, bool fuse_ope
         a.pre[q] = static_cast<const TS *>(fpre) + (long long)q * p->lay.pop;
         a.post[q] = static_cast<TS *>(fpost) + (long long)q * p->lay.pop;
     }
-    a.cls = p->d_cls;
-    a.mlinks = p->d_mlinks;
+    a.ct = cls_tab(p);
     a.g = p->g;
     a.z0 = z0;
     a.passthrough = p->passthrough;
@@ -332,17 +348,22 @@ int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cuda
 
 // in-place (AA pattern) launches: kind 0 = R0 -> R1 step, 1 = R1 -> R0 step, 2 = swap
 template <typename TS>
-int launch_aa(mlb_plan *p, void *f, int kind, cudaStream_t st)
+void fill_aa(mlb_plan *p, void *f, mlb::AAArgs<TS> &a)
 {
     using T = typename mlb::Store<TS>::C;
-    mlb::AAArgs<TS> a;
     for (int q = 0; q < MLB_Q; ++q)
         a.f[q] = static_cast<TS *>(f) + (long long)q * p->lay.pop;
-    a.cls = p->d_cls;
-    a.mlinks = p->d_mlinks;
+    a.ct = cls_tab(p);
     a.g = p->g;
     a.omega = T(p->omega);
     wall_terms<T>(p->wall_u, a.k);
+}
+
+template <typename TS>
+int launch_aa(mlb_plan *p, void *f, int kind, cudaStream_t st)
+{
+    mlb::AAArgs<TS> a;
+    fill_aa<TS>(p, f, a);
     constexpr int BX = 128;
     const dim3 grid((p->nx + BX - 1) / BX, p->ny, p->nz);
     if (kind == 0) mlb::aa_pull_kernel<TS, BX><<<grid, BX, 0, st>>>(a);
@@ -352,10 +373,49 @@ int launch_aa(mlb_plan *p, void *f, int kind, cudaStream_t st)
     return MLB_OK;
 }
 
+template <typename TS, int V, int LX>
+int launch_aa_vec(mlb_plan *p, void *f, int kind, cudaStream_t st)
+{
+    mlb::AAArgs<TS> a;
+    fill_aa<TS>(p, f, a);
+    const int rows = 128 / LX;
+    const dim3 grid((p->nx / V + LX - 1) / LX, (p->ny + rows - 1) / rows, p->nz);
+    if (kind == 0) mlb::aa_pull_vec_kernel<TS, V, LX><<<grid, 128, 0, st>>>(a);
+    else mlb::aa_local_vec_kernel<TS, V, LX><<<grid, 128, 0, st>>>(a);
+    MLB_LAUNCHED();
+    return MLB_OK;
+}
+
+template <typename TS, int V>
+int launch_aa_vec_lx(mlb_plan *p, void *f, int kind, int lx, cudaStream_t st)
+{
+    if (lx == 8) return launch_aa_vec<TS, V, 8>(p, f, kind, st);
+    if (lx == 16) return launch_aa_vec<TS, V, 16>(p, f, kind, st);
+    return launch_aa_vec<TS, V, 32>(p, f, kind, st);
+}
+
+// the in-place step kernels follow the plan's variant: pack kernels when the
+// two-buffer path would use one (and always for the swap: scalar)
 int launch_aa_any(mlb_plan *p, void *f, int kind, cudaStream_t st)
 {
-    if (p->dtype == MLB_F32) return launch_aa<float>(p, f, kind, st);
-    if (p->dtype == MLB_F64) return launch_aa<double>(p, f, kind, st);
+    int variant = p->variant;
+    if (variant == 0) {  // auto: packs whenever the row length allows
+        if (p->dtype == MLB_F32 && p->nx % 4 == 0 && p->nx >= 128) variant = 1016;
+        else if (p->dtype == MLB_F64 && p->nx % 2 == 0 && p->nx >= 128) variant = 1016;
+        else if (p->dtype == MLB_F16 && p->nx % 4 == 0 && p->nx >= 128) variant = 2016;
+        else variant = 128;
+    }
+    if (!variant_exists(p->dtype, variant))
+        return fail(MLB_EINVAL, "kernel variant %d does not exist for dtype code %d", variant,
+                    p->dtype);
+    const bool vec = variant >= 1000 && kind != 2 && p->nx % pack_cells(p->dtype, variant) == 0;
+    const int lx = variant % 1000;
+    if (p->dtype == MLB_F32)
+        return vec ? launch_aa_vec_lx<float, 4>(p, f, kind, lx, st) : launch_aa<float>(p, f, kind, st);
+    if (p->dtype == MLB_F64)
+        return vec ? launch_aa_vec_lx<double, 2>(p, f, kind, lx, st) : launch_aa<double>(p, f, kind, st);
+    if (vec && variant >= 3000) return launch_aa_vec_lx<__half, 2>(p, f, kind, lx, st);
+    if (vec) return launch_aa_vec_lx<__half, 4>(p, f, kind, lx, st);
     return launch_aa<__half>(p, f, kind, st);
 }
 
@@ -496,6 +556,7 @@ int mlb_plan_destroy(mlb_plan *p)
         return MLB_OK;
     cudaSetDevice(p->device);
     cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_mlinks); cudaFree(p->d_in);
+    cudaFree(p->d_kind); cudaFree(p->d_tab);
     cudaFree(p->d_out); cudaFree(p->d_out_tmp); cudaFree(p->d_partials); cudaFree(p->d_diag);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
@@ -635,8 +696,10 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
         p->passthrough = 0;  // see mlb_plan_set_passthrough
 
     cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_mlinks); cudaFree(p->d_in);
+    cudaFree(p->d_kind); cudaFree(p->d_tab);
     cudaFree(p->d_out); cudaFree(p->d_out_tmp);
     p->d_flags = nullptr; p->d_cls = p->d_mlinks = nullptr; p->d_in = p->d_out = nullptr;
+    p->d_kind = nullptr; p->d_tab = nullptr;
     p->d_out_tmp = nullptr;
     p->have_flags = false;
     MLB_CUDA(cudaMalloc(&p->d_flags, padded));
@@ -660,7 +723,29 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     const dim3 grid((unsigned)((xp + 127) / 128), ny, nz + 2);
     mlb::build_cls_kernel<<<grid, 128>>>(p->d_flags, p->d_cls, p->d_mlinks, p->g);
     MLB_LAUNCHED();
-    MLB_CUDA(cudaDeviceSynchronize());
+    // compress to one kind byte per cell + the dictionary of distinct pairs
+    unsigned int *d_esc = nullptr;
+    MLB_CUDA(cudaMalloc(&p->d_kind, padded));
+    MLB_CUDA(cudaMalloc(&p->d_tab, 256 * sizeof(unsigned long long)));
+    MLB_CUDA(cudaMalloc(&d_esc, sizeof(unsigned int)));
+    MLB_CUDA(cudaMemset(p->d_tab, 0xff, 256 * sizeof(unsigned long long)));
+    MLB_CUDA(cudaMemset(p->d_tab, 0, sizeof(unsigned long long)));  // slot 0 = bulk (0, 0)
+    MLB_CUDA(cudaMemset(d_esc, 0, sizeof(unsigned int)));
+    mlb::build_kind_kernel<<<(unsigned)((padded + 255) / 256), 256>>>(
+        p->d_cls, p->d_mlinks, (long long)padded, p->d_tab, p->d_kind, d_esc);
+    MLB_LAUNCHED();
+    MLB_CUDA(cudaMemcpy(&p->n_escape, d_esc, sizeof(unsigned int), cudaMemcpyDeviceToHost));
+    cudaFree(d_esc);
+    unsigned long long tab[256];
+    MLB_CUDA(cudaMemcpy(tab, p->d_tab, sizeof(tab), cudaMemcpyDeviceToHost));
+    p->n_kinds = 0;
+    for (int k = 0; k < 255; ++k)
+        p->n_kinds += tab[k] != mlb::KIND_EMPTY;
+    if (p->n_escape == 0) {
+        // the usual case: the dictionary covers the geometry, drop the 8 B / cell
+        cudaFree(p->d_cls); cudaFree(p->d_mlinks);
+        p->d_cls = p->d_mlinks = nullptr;
+    }
     p->have_flags = true;
     return MLB_OK;
 }
@@ -670,16 +755,36 @@ int mlb_plan_get_flags(const mlb_plan *p, uint8_t *h_flags)
     if (int rc = check_plan(p, true)) return rc;
     if (!h_flags) return fail(MLB_EINVAL, "h_flags is NULL");
     MLB_CUDA(cudaSetDevice(p->device));
-    // from the class words' low bits: proves the codes the kernel tests
+    // from what the kernels read - kind byte -> dictionary (or the full-width
+    // word for escape cells) -> low bits: proves the codes the kernel tests
     const size_t padded = (size_t)(p->nz + 2) * p->lay.plane;
-    std::vector<uint32_t> pad(padded);
-    MLB_CUDA(cudaMemcpy(pad.data(), p->d_cls, padded * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    std::vector<uint8_t> kind(padded);
+    MLB_CUDA(cudaMemcpy(kind.data(), p->d_kind, padded, cudaMemcpyDeviceToHost));
+    unsigned long long tab[256];
+    MLB_CUDA(cudaMemcpy(tab, p->d_tab, sizeof(tab), cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> full;
+    if (p->n_escape) {
+        full.resize(padded);
+        MLB_CUDA(cudaMemcpy(full.data(), p->d_cls, padded * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost));
+    }
     for (int z = 0; z < p->nz; ++z)
         for (int y = 0; y < p->ny; ++y)
-            for (int x = 0; x < p->nx; ++x)
-                h_flags[((size_t)z * p->ny + y) * p->nx + x] = (uint8_t)(
-                    pad[(size_t)(z + 1) * p->lay.plane + (size_t)y * p->lay.xp + x]
-                    & mlb::CLS_FLAG);
+            for (int x = 0; x < p->nx; ++x) {
+                const size_t d = (size_t)(z + 1) * p->lay.plane + (size_t)y * p->lay.xp + x;
+                const uint32_t c = kind[d] == mlb::KIND_ESCAPE ? full[d]
+                                                               : (uint32_t)tab[kind[d]];
+                h_flags[((size_t)z * p->ny + y) * p->nx + x] = (uint8_t)(c & mlb::CLS_FLAG);
+            }
+    return MLB_OK;
+}
+
+int mlb_plan_geometry_stats(const mlb_plan *p, int64_t out[2])
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (!out) return fail(MLB_EINVAL, "out is NULL");
+    out[0] = p->n_kinds;
+    out[1] = p->n_escape;
     return MLB_OK;
 }
 
@@ -928,13 +1033,13 @@ int mlb_diagnostics(mlb_plan *p, const void *d_f, double h_out[8], void *stream)
     MLB_CUDA(cudaSetDevice(p->device));
     if (p->dtype == MLB_F32)
         mlb::diag_kernel<float><<<p->diag_blocks, mlb::DIAG_THREADS, 0, S(stream)>>>(
-            static_cast<const float *>(d_f), p->d_cls, p->g, p->d_partials);
+            static_cast<const float *>(d_f), cls_tab(p), p->g, p->d_partials);
     else if (p->dtype == MLB_F64)
         mlb::diag_kernel<double><<<p->diag_blocks, mlb::DIAG_THREADS, 0, S(stream)>>>(
-            static_cast<const double *>(d_f), p->d_cls, p->g, p->d_partials);
+            static_cast<const double *>(d_f), cls_tab(p), p->g, p->d_partials);
     else
         mlb::diag_kernel<__half><<<p->diag_blocks, mlb::DIAG_THREADS, 0, S(stream)>>>(
-            static_cast<const __half *>(d_f), p->d_cls, p->g, p->d_partials);
+            static_cast<const __half *>(d_f), cls_tab(p), p->g, p->d_partials);
     MLB_LAUNCHED();
     mlb::diag_final_kernel<<<1, mlb::DIAG_THREADS, 0, S(stream)>>>(p->d_partials,
                                                                   p->diag_blocks, p->d_diag);

@@ -48,6 +48,44 @@ struct Geom {
     long long xp, plane, pop;  // row pitch, z-plane, population strides (elements)
 };
 
+// Per-cell class word, built once from the flags (build_cls_kernel):
+//   bits 0..2   the reference's flag code (boundaries.py:20-24)
+//   bit  2 + i  (i = 1..18) the source cell of direction i is a wall (SOLID or
+//               MOVING_WALL): that link bounces back
+//   bit  31     some bouncing link hits a MOVING_WALL: mlinks[d] bit i says which
+// cls == 0 is a bulk fluid cell.  One 4-byte load per cell tells the kernel
+// everything the reference learns from 19 flag reads (kernels.py:76-197).
+constexpr uint32_t CLS_FLAG = 0x7u;
+constexpr uint32_t CLS_MOVING = 0x80000000u;
+__host__ __device__ constexpr uint32_t cls_link(int i) { return 1u << (2 + i); }
+
+// What the kernels actually read per cell is ONE BYTE: `kind[d]`, an index into
+// a per-plan dictionary `tab` of the distinct (class word, moving-wall link bits)
+// pairs of the geometry (build_kind_kernel).  Index 0 is the bulk fluid cell
+// (class word 0): a pack of cells whose kind bytes are all zero needs nothing
+// else.  Everything else - walls, inlet / outlet cells, fluid cells next to a
+// wall - looks its pair up in the table (at most 2 KB, L1-resident).  A cavity
+// has ~30 distinct pairs; a geometry with more than 254 uses the escape index
+// 255 for the overflow cells, which read the full-width arrays `cls_full` /
+// `ml_full` (kept only in that case).  Compared with a 4-byte class word per
+// cell this takes 3 B per update off the HBM traffic (2 % in fp32, 4 % with
+// fp16 storage) and 7 B per cell off the footprint.
+constexpr uint32_t KIND_ESCAPE = 255u;
+struct ClsTab {
+    const uint8_t *__restrict__ kind;
+    const uint2 *__restrict__ tab;          // [256]: x = class word, y = moving-wall link bits
+    const uint32_t *__restrict__ cls_full;  // escape cells only (may be NULL)
+    const uint32_t *__restrict__ ml_full;
+};
+__device__ __forceinline__ uint32_t cls_of(const ClsTab &t, uint32_t k, int d)
+{
+    return k == KIND_ESCAPE ? t.cls_full[d] : __ldg(&t.tab[k].x);
+}
+__device__ __forceinline__ uint32_t mlinks_of(const ClsTab &t, uint32_t k, int d)
+{
+    return k == KIND_ESCAPE ? t.ml_full[d] : __ldg(&t.tab[k].y);
+}
+
 template <typename TS>
 struct StepArgs {
     using T = typename Store<TS>::C;  // compute type
@@ -56,8 +94,7 @@ struct StepArgs {
     // IMAD.WIDE of a 32-bit in-population offset onto a constant-bank base)
     const TS *pre[Q];
     TS *post[Q];
-    const uint32_t *__restrict__ cls;     // per-cell class word, see below
-    const uint32_t *__restrict__ mlinks;  // per-cell moving-wall link bits (rarely read)
+    ClsTab ct;     // per-cell kind byte + dictionary of class words, see below
     Geom g;
     int z0;        // first slab plane this launch updates (blockIdx.z = 0)
     int passthrough;  // 1: non-fluid cells are rewritten with fpre's value (see step_cell)
@@ -89,26 +126,17 @@ struct PushArgs {
     TS *hi[5];
 };
 
-// Per-cell class word, built once from the flags (build_cls_kernel):
-//   bits 0..2   the reference's flag code (boundaries.py:20-24)
-//   bit  2 + i  (i = 1..18) the source cell of direction i is a wall (SOLID or
-//               MOVING_WALL): that link bounces back
-//   bit  31     some bouncing link hits a MOVING_WALL: mlinks[d] bit i says which
-// cls == 0 is a bulk fluid cell.  One 4-byte load per cell tells the kernel
-// everything the reference learns from 19 flag reads (kernels.py:76-197).
-constexpr uint32_t CLS_FLAG = 0x7u;
-constexpr uint32_t CLS_MOVING = 0x80000000u;
-__host__ __device__ constexpr uint32_t cls_link(int i) { return 1u << (2 + i); }
-
 // ---------------------------------------------------------------------------
 // Lane algebra: the collide below is written once over a "lane" type L.
 //   float, double : one cell, plain IEEE operators;
 //   float2        : TWO cells side by side on Blackwell's packed-fp32
 //                   instructions (FADD2 / FMUL2 / FFMA2, sm_100+): each is one
-//                   issue slot for two independent round-to-nearest results,
-//                   so the 195 unfused operations of a cell cost ~98 slots.
+//                   issue slot for two independent round-to-nearest results.
 //                   a - b is FFMA2(b, -1, a): the product is exact, the sum is
 //                   rounded once - bit-identical to the scalar subtraction.
+//                   The 68 sums that consume a product stay scalar (addm / subm
+//                   below: ptxas would contract them), so a cell's 195 unfused
+//                   operations cost ~132 slots instead of 195.
 // Every element of every result is the same correctly rounded value the
 // scalar code (and the CPU oracle) produces.
 template <typename L> struct Alg;
@@ -118,6 +146,8 @@ template <> struct Alg<float> {
     static __device__ __forceinline__ float add(float a, float b) { return a + b; }
     static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
     static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
+    static __device__ __forceinline__ float addm(float a, float m) { return a + m; }
+    static __device__ __forceinline__ float subm(float a, float m) { return a - m; }
     static __device__ __forceinline__ float rcp0(float r) { return r != 0.0f ? 1.0f / r : 0.0f; }
 };
 template <> struct Alg<double> {
@@ -126,6 +156,8 @@ template <> struct Alg<double> {
     static __device__ __forceinline__ double add(double a, double b) { return a + b; }
     static __device__ __forceinline__ double sub(double a, double b) { return a - b; }
     static __device__ __forceinline__ double mul(double a, double b) { return a * b; }
+    static __device__ __forceinline__ double addm(double a, double m) { return a + m; }
+    static __device__ __forceinline__ double subm(double a, double m) { return a - m; }
     static __device__ __forceinline__ double rcp0(double r) { return r != 0.0 ? 1.0 / r : 0.0; }
 };
 template <> struct Alg<float2> {
@@ -135,6 +167,16 @@ template <> struct Alg<float2> {
     static __device__ __forceinline__ float2 sub(float2 a, float2 b)
     { return __ffma2_rn(b, make_float2(-1.0f, -1.0f), a); }
     static __device__ __forceinline__ float2 mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+    // a + m / a - m where m is the result of a mul().  ptxas 12.9 contracts a
+    // packed multiply followed by a packed add / subtract into FFMA2 - even
+    // for mul.rn.f32x2 + add.rn.f32x2 in PTX, even with --fmad=false - which
+    // skips the product's rounding (found as a 1-half-ulp parity failure, once
+    // in ~20 000 values).  Scalar adds are not contracted (-fmad=false holds
+    // for them), so sums that consume a product are done per element.
+    static __device__ __forceinline__ float2 addm(float2 a, float2 m)
+    { return make_float2(a.x + m.x, a.y + m.y); }
+    static __device__ __forceinline__ float2 subm(float2 a, float2 m)
+    { return make_float2(a.x - m.x, a.y - m.y); }
     static __device__ __forceinline__ float2 rcp0(float2 r)
     { return make_float2(r.x != 0.0f ? 1.0f / r.x : 0.0f, r.y != 0.0f ? 1.0f / r.y : 0.0f); }
 };
@@ -165,8 +207,9 @@ __device__ __forceinline__ void collide(L (&g)[Q], const typename Alg<L>::S omeg
         g[9], g[10]), g[11]), g[12]), g[13]), g[14]), g[15]), g[16]), g[17]), g[18]);
     const L inv = A::rcp0(rho);  // rho != 0 ? 1 / rho : 0
     const L ux = A::mul(mx, inv), uy = A::mul(my, inv), uz = A::mul(mz, inv);
-    const L usq = A::add(A::add(A::mul(ux, ux), A::mul(uy, uy)), A::mul(uz, uz));
-    const L um = A::sub(one, A::mul(c15, usq));
+    // (addm / subm: a sum one of whose operands is a product, see Alg<float2>)
+    const L usq = A::addm(A::addm(A::mul(ux, ux), A::mul(uy, uy)), A::mul(uz, uz));
+    const L um = A::subm(one, A::mul(c15, usq));
     const L wr0 = A::mul(w0, rho), wrs = A::mul(ws, rho), wrd = A::mul(wd, rho);
     const L a = A::add(ux, uy), b = A::sub(ux, uy), c = A::add(ux, uz), d = A::sub(ux, uz),
             h = A::add(uy, uz), kk = A::sub(uy, uz);
@@ -175,11 +218,11 @@ __device__ __forceinline__ void collide(L (&g)[Q], const typename Alg<L>::S omeg
     {                                                                          \
         const L q_ = A::mul(c45, A::mul((cu), (cu)));                          \
         const L t_ = A::mul(c3, (cu));                                         \
-        const L p_ = A::add(um, q_);                                           \
-        const L ep_ = A::mul((wr), A::add(p_, t_));                            \
-        const L em_ = A::mul((wr), A::sub(p_, t_));                            \
-        g[ip] = A::sub(g[ip], A::mul(omega, A::sub(g[ip], ep_)));              \
-        g[im] = A::sub(g[im], A::mul(omega, A::sub(g[im], em_)));              \
+        const L p_ = A::addm(um, q_);                                          \
+        const L ep_ = A::mul((wr), A::addm(p_, t_));                           \
+        const L em_ = A::mul((wr), A::subm(p_, t_));                           \
+        g[ip] = A::subm(g[ip], A::mul(omega, A::subm(g[ip], ep_)));            \
+        g[im] = A::subm(g[im], A::mul(omega, A::subm(g[im], em_)));            \
     }
     MLB_PAIR(ux, wrs, 1, 3)
     MLB_PAIR(uy, wrs, 2, 4)
@@ -193,7 +236,7 @@ __device__ __forceinline__ void collide(L (&g)[Q], const typename Alg<L>::S omeg
 #undef MLB_PAIR
     {
         const L e0 = A::mul(wr0, um);
-        g[0] = A::sub(g[0], A::mul(omega, A::sub(g[0], e0)));
+        g[0] = A::subm(g[0], A::mul(omega, A::subm(g[0], e0)));
     }
 }
 
@@ -283,7 +326,7 @@ __device__ __forceinline__ void step_cell(const StepArgs<TS> &a, const PushArgs<
     const int d = (lz + 1) * plane + y * xp + x;
     const int dm = d + dxm, dq = d + dxq, dc = d;
 
-    const uint32_t cd = a.cls[d];
+    const uint32_t kd = a.ct.kind[d];
     T g[Q];
     g[0] = Store<TS>::up(a.pre[0][d]);
 #define MLB_PULL(i, zz, rr, dd) g[i] = Store<TS>::up(a.pre[i][(dd) + ((zz) + (rr))]);
@@ -304,6 +347,7 @@ __device__ __forceinline__ void step_cell(const StepArgs<TS> &a, const PushArgs<
     // identical and only fluid / open-boundary cells ever change), so the
     // bytes in memory are the same as if the cell had not been touched and
     // every store of the warp is a full line.
+    const uint32_t cd = kd == 0 ? 0u : cls_of(a.ct, kd, d);
     const bool fluid = (cd & CLS_FLAG) == 0;
     if (!fluid && !a.passthrough)
         return;
@@ -312,7 +356,7 @@ __device__ __forceinline__ void step_cell(const StepArgs<TS> &a, const PushArgs<
         if (cd != 0) {
             // SOLID source -> own opposite population, MOVING_WALL source ->
             // that plus the wall term (kernels.py:88-96)
-            const uint32_t mv = (cd & CLS_MOVING) ? a.mlinks[d] : 0u;
+            const uint32_t mv = (cd & CLS_MOVING) ? mlinks_of(a.ct, kd, d) : 0u;
 #pragma unroll
             for (int i = 1; i < Q; ++i)
                 if (cd & cls_link(i)) {
@@ -383,8 +427,7 @@ template <typename TS>
 struct AAArgs {
     using T = typename Store<TS>::C;
     TS *f[Q];
-    const uint32_t *__restrict__ cls;
-    const uint32_t *__restrict__ mlinks;
+    ClsTab ct;
     Geom g;
     T omega;
     T k[Q];
@@ -444,16 +487,17 @@ __global__ void __launch_bounds__(BX) aa_pull_kernel(const AAArgs<TS> a)
     const int d = (lz + 1) * plane + y * xp + x;
     const int dm = d + dxm, dq = d + dxq, dc = d;
 
-    const uint32_t cd = a.cls[d];
+    const uint32_t kd = a.ct.kind[d];
     T g[Q];
     g[0] = Store<TS>::up(a.f[0][d]);
 #define MLB_X(i, zz, rr, dd) g[i] = Store<TS>::up(a.f[i][(dd) + ((zz) + (rr))]);
     MLB_AA_DIRS(MLB_X)
 #undef MLB_X
+    const uint32_t cd = kd == 0 ? 0u : cls_of(a.ct, kd, d);
     if (cd & CLS_FLAG)
         return;
     if (cd != 0) {
-        const uint32_t mv = (cd & CLS_MOVING) ? a.mlinks[d] : 0u;
+        const uint32_t mv = (cd & CLS_MOVING) ? mlinks_of(a.ct, kd, d) : 0u;
 #pragma unroll
         for (int i = 1; i < Q; ++i)
             if (cd & cls_link(i)) {
@@ -487,11 +531,12 @@ __global__ void __launch_bounds__(BX) aa_local_kernel(const AAArgs<TS> a)
     if (x >= a.g.nx)
         return;
     const int d = ((int)blockIdx.z + 1) * (int)a.g.plane + (int)blockIdx.y * (int)a.g.xp + x;
-    const uint32_t cd = a.cls[d];
+    const uint32_t kd = a.ct.kind[d];
     T g[Q];
 #pragma unroll
     for (int i = 0; i < Q; ++i)
         g[i] = Store<TS>::up(a.f[opp(i)][d]);
+    const uint32_t cd = kd == 0 ? 0u : cls_of(a.ct, kd, d);
     if (cd & CLS_FLAG) {
         // non-fluid cell: rewrite its own (untouched) values so that every
         // store of the warp is a full line - in place this is always valid
@@ -501,7 +546,7 @@ __global__ void __launch_bounds__(BX) aa_local_kernel(const AAArgs<TS> a)
         return;
     }
     if (cd & CLS_MOVING) {
-        const uint32_t mv = a.mlinks[d];
+        const uint32_t mv = mlinks_of(a.ct, kd, d);
 #pragma unroll
         for (int i = 1; i < Q; ++i)
             if (mv & (1u << i))
@@ -524,7 +569,8 @@ __global__ void __launch_bounds__(BX) aa_swap_kernel(const AAArgs<TS> a)
         return;
     int d, off[Q];
     aa_offsets<TS>(a.g, x, blockIdx.y, blockIdx.z, d, off);
-    const uint32_t cd = a.cls[d];
+    const uint32_t kd = a.ct.kind[d];
+    const uint32_t cd = kd == 0 ? 0u : cls_of(a.ct, kd, d);
     if (cd & CLS_FLAG)
         return;
 #pragma unroll
@@ -592,15 +638,15 @@ template <> struct PackIO<__half, 4> {
         *reinterpret_cast<uint2 *>(p) = u;
     }
 };
-// the class words of a pack
-template <int V> struct ClsIO;
-template <> struct ClsIO<2> {
-    static __device__ __forceinline__ void load(const uint32_t *p, uint32_t (&o)[2])
-    { const uint2 v = *reinterpret_cast<const uint2 *>(p); o[0] = v.x; o[1] = v.y; }
+// the kind bytes of a pack, as one word (byte j = cell j)
+template <int V> struct KindIO;
+template <> struct KindIO<2> {
+    static __device__ __forceinline__ uint32_t load(const uint8_t *p)
+    { return *reinterpret_cast<const uint16_t *>(p); }
 };
-template <> struct ClsIO<4> {
-    static __device__ __forceinline__ void load(const uint32_t *p, uint32_t (&o)[4])
-    { const uint4 v = *reinterpret_cast<const uint4 *>(p); o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+template <> struct KindIO<4> {
+    static __device__ __forceinline__ uint32_t load(const uint8_t *p)
+    { return *reinterpret_cast<const uint32_t *>(p); }
 };
 
 // The V values pulled along a direction with x component CX from the row
@@ -658,15 +704,29 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
     const int xr = (x0 + V >= gm.nx) ? 0 : x0 + V;
     const int d = zc + rc + x0;
 
-    // class words of the pack and all pulls, issued together
-    uint32_t c[V];
-    ClsIO<V>::load(a.cls + d, c);
+    // kind bytes of the pack and all pulls, issued together
+    const uint32_t kpack = KindIO<V>::load(a.ct.kind + d);
     T g[Q][V];
     PackIO<TS, V>::load(a.pre[0] + d, g[0]);
 #define MLB_X(i, CX, Z, R) pull_pack<TS, V, CX>(a.pre[i] + ((Z) + (R)), x0, xl, xr, g[i]);
     MLB_DIRS(MLB_X)
 #undef MLB_X
 
+    // class words: all zero for a pack of bulk cells (the usual case), else from
+    // the dictionary.  (A separate code path for bulk packs was measured and is
+    // slower: warps that mix bulk and wall packs then run the collide twice.)
+    uint32_t c[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+        c[j] = 0u;
+    if (kpack != 0u) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const uint32_t k = (kpack >> (8 * j)) & 0xffu;
+            if (k != 0u)
+                c[j] = cls_of(a.ct, k, d + j);
+        }
+    }
     uint32_t call = 0u;
     bool anyfluid = false, allfluid = true;
 #pragma unroll
@@ -683,7 +743,8 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
         uint32_t mv[V];
 #pragma unroll
         for (int j = 0; j < V; ++j)
-            mv[j] = ((c[j] & CLS_FLAG) == 0 && (c[j] & CLS_MOVING)) ? a.mlinks[d + j] : 0u;
+            mv[j] = ((c[j] & CLS_FLAG) == 0 && (c[j] & CLS_MOVING))
+                        ? mlinks_of(a.ct, (kpack >> (8 * j)) & 0xffu, d + j) : 0u;
 #pragma unroll
         for (int i = 1; i < Q; ++i)
             if (call & cls_link(i)) {
@@ -776,6 +837,257 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
 }
 
 // ---------------------------------------------------------------------------
+// Vectorised in-place kernels: the thread / warp layout, loads, link-bit
+// patching and collide of step_vec_kernel; what differs is where results go.
+//
+// aa_pull_vec_kernel (R0 -> R1).  A cell writes its result for opp(i) into
+// the location it read for i: A[i][x - c_i] (or its own A[opp(i)][x] when the
+// link bounces).  For the 8 directions with c_x = 0 that is an aligned pack
+// in a neighbouring row / plane.  For the 10 directions with c_x = +-1 the
+// pack is shifted by one cell; to keep every store an aligned 16-byte word, a
+// lane stores the aligned pack made of its own cells' results (all but one)
+// plus ONE value from the neighbouring lane (a warp shuffle): with c_x = +1
+// lane L stores the results of cells x0+1 .. x0+V (its cells 1..V-1 and the
+// right lane's cell 0) at A[i][x0 .. x0+V-1].  That is only valid when every
+// cell involved is a bulk fluid cell (kind 0: no bouncing link, so each of
+// these locations has exactly this one writer); both lanes know both kind
+// words (a shuffled predicate), so they agree on who writes what: if either
+// pack is not all-bulk, or the neighbour is in another warp row, each lane
+// falls back to per-cell stores for its own cells, with the scalar kernel's
+// rules.  Every location still has exactly one writer.
+#ifndef MLB_AA_MINB
+#define MLB_AA_MINB 3
+#endif
+template <typename TS, int V, int LX>
+__global__ void __launch_bounds__(128, MLB_AA_MINB) aa_pull_vec_kernel(const AAArgs<TS> a)
+{
+    using T = typename Store<TS>::C;
+    constexpr int RPW = 32 / LX;
+    constexpr unsigned FULL = 0xffffffffu;
+    const Geom &gm = a.g;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int seg = lane % LX;
+    int x0 = (blockIdx.x * LX + seg) * V;
+    int y = blockIdx.y * (4 * RPW) + warp * RPW + lane / LX;
+    const int lz = blockIdx.z;
+    // lanes outside the grid stay in the warp for the shuffles: they compute on
+    // a valid dummy pack and never store
+    const bool valid = x0 < gm.nx && y < gm.ny;
+    if (!valid) { x0 = 0; y = 0; }
+
+    const int xp = (int)gm.xp, plane = (int)gm.plane;
+    const int zc = (lz + 1) * plane;
+    const int zm = ((lz == 0) ? gm.zlo_src : lz) * plane;
+    const int zq = ((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) * plane;
+    const int ym = (y == 0) ? gm.ny - 1 : y - 1;
+    const int yq = (y == gm.ny - 1) ? 0 : y + 1;
+    const int rc = y * xp, rm = ym * xp, rq = yq * xp;
+    const int xl = (x0 == 0) ? gm.nx - 1 : x0 - 1;
+    const int xr = (x0 + V >= gm.nx) ? 0 : x0 + V;
+    const int d = zc + rc + x0;
+
+    const uint32_t kpack = KindIO<V>::load(a.ct.kind + d);
+    T g[Q][V];
+    PackIO<TS, V>::load(a.f[0] + d, g[0]);
+#define MLB_X(i, CX, Z, R) pull_pack<TS, V, CX>(a.f[i] + ((Z) + (R)), x0, xl, xr, g[i]);
+    MLB_DIRS(MLB_X)
+#undef MLB_X
+
+    const bool bulk = valid && kpack == 0u;
+    const bool bulk_r = __shfl_down_sync(FULL, (int)bulk, 1) != 0 && seg != LX - 1
+                        && x0 + V < gm.nx;
+    const bool bulk_l = __shfl_up_sync(FULL, (int)bulk, 1) != 0 && seg != 0;
+
+    uint32_t c[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+        c[j] = 0u;
+    if (kpack != 0u) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const uint32_t k = (kpack >> (8 * j)) & 0xffu;
+            if (k != 0u)
+                c[j] = cls_of(a.ct, k, d + j);
+        }
+    }
+    uint32_t call = 0u;
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+        call |= ((c[j] & CLS_FLAG) == 0) ? c[j] : 0u;
+    if (call != 0) {
+        uint32_t mv[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            mv[j] = ((c[j] & CLS_FLAG) == 0 && (c[j] & CLS_MOVING))
+                        ? mlinks_of(a.ct, (kpack >> (8 * j)) & 0xffu, d + j) : 0u;
+#pragma unroll
+        for (int i = 1; i < Q; ++i)
+            if (call & cls_link(i)) {
+                T o[V];
+                PackIO<TS, V>::load(a.f[opp(i)] + d, o);
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    if (c[j] & cls_link(i))
+                        g[i][j] = (mv[j] & (1u << i)) ? o[j] + a.k[i] : o[j];
+            }
+    }
+    if constexpr (UsePackedMath<TS>::value)
+        collide_cell_pairs<V>(g, a.omega);
+    else
+        collide_cells<T, V>(g, a.omega);
+
+    // ---- stores ---------------------------------------------------------------
+    // Bulk packs (no link bounces, every target location has this one writer):
+    // aligned packs wherever the neighbouring lane can supply (or take) the
+    // cell that crosses the pack boundary.  Directions are handled in three
+    // groups (c_x = +1, -1, 0) so that only five shuffled values are live at a
+    // time; every lane of the warp takes part in the shuffles.
+    {
+        T nb[5];
+        int n = 0;
+#define MLB_X(i, CX, Z, R) if (CX > 0) nb[n++] = __shfl_down_sync(FULL, g[opp(i)][0], 1);
+        MLB_DIRS(MLB_X)
+#undef MLB_X
+        if (bulk) {
+            n = 0;
+#define MLB_X(i, CX, Z, R)                                                            \
+            if (CX > 0) { /* locations x0 .. x0+V-1 take cells x0+1 .. x0+V */        \
+                TS *row = a.f[i] + ((Z) + (R));                                       \
+                if (bulk_r) {                                                         \
+                    T o[V];                                                           \
+                    _Pragma("unroll") for (int j = 0; j < V - 1; ++j) o[j] = g[opp(i)][j + 1]; \
+                    o[V - 1] = nb[n];                                                 \
+                    PackIO<TS, V>::store(row + x0, o);                                \
+                } else {                                                              \
+                    _Pragma("unroll") for (int j = 1; j < V; ++j)                     \
+                        row[x0 + j - 1] = Store<TS>::down(g[opp(i)][j]);              \
+                }                                                                     \
+                if (!bulk_l) row[xl] = Store<TS>::down(g[opp(i)][0]);                 \
+                ++n;                                                                  \
+            }
+            MLB_DIRS(MLB_X)
+#undef MLB_X
+        }
+        n = 0;
+#define MLB_X(i, CX, Z, R) if (CX < 0) nb[n++] = __shfl_up_sync(FULL, g[opp(i)][V - 1], 1);
+        MLB_DIRS(MLB_X)
+#undef MLB_X
+        if (bulk) {
+            n = 0;
+#define MLB_X(i, CX, Z, R)                                                            \
+            if (CX < 0) { /* locations x0 .. x0+V-1 take cells x0-1 .. x0+V-2 */      \
+                TS *row = a.f[i] + ((Z) + (R));                                       \
+                if (bulk_l) {                                                         \
+                    T o[V];                                                           \
+                    _Pragma("unroll") for (int j = 1; j < V; ++j) o[j] = g[opp(i)][j - 1]; \
+                    o[0] = nb[n];                                                     \
+                    PackIO<TS, V>::store(row + x0, o);                                \
+                } else {                                                              \
+                    _Pragma("unroll") for (int j = 0; j < V - 1; ++j)                 \
+                        row[x0 + j + 1] = Store<TS>::down(g[opp(i)][j]);              \
+                }                                                                     \
+                if (!bulk_r) row[xr] = Store<TS>::down(g[opp(i)][V - 1]);             \
+                ++n;                                                                  \
+            }
+            MLB_DIRS(MLB_X)
+#undef MLB_X
+            PackIO<TS, V>::store(a.f[0] + d, g[0]);
+#define MLB_X(i, CX, Z, R)                                                            \
+            if (CX == 0) PackIO<TS, V>::store(a.f[i] + ((Z) + (R)) + x0, g[opp(i)]);
+            MLB_DIRS(MLB_X)
+#undef MLB_X
+            return;
+        }
+    }
+    if (!valid)
+        return;
+    // a pack with walls (or next to one): per cell, the scalar kernel's rules -
+    // the result for opp(i) goes into the location read for i, or - bouncing
+    // link - stays in the cell's own slot of opp(i) (kernels.py:88-96 read that)
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+        if ((c[j] & CLS_FLAG) == 0)
+            a.f[0][d + j] = Store<TS>::down(g[0][j]);
+#define MLB_X(i, CX, Z, R)                                                            \
+    _Pragma("unroll") for (int j = 0; j < V; ++j)                                     \
+        if ((c[j] & CLS_FLAG) == 0) {                                                 \
+            const int xs = (CX) == 0 ? x0 + j                                         \
+                         : (CX) > 0 ? (j == 0 ? xl : x0 + j - 1)                      \
+                                    : (j == V - 1 ? xr : x0 + j + 1);                 \
+            if (c[j] & cls_link(i)) a.f[opp(i)][d + j] = Store<TS>::down(g[opp(i)][j]); \
+            else a.f[i][((Z) + (R)) + xs] = Store<TS>::down(g[opp(i)][j]);            \
+        }
+    MLB_DIRS(MLB_X)
+#undef MLB_X
+}
+
+// aa_local_vec_kernel (R1 -> R0): everything a cell needs is in its own slots.
+template <typename TS, int V, int LX>
+__global__ void __launch_bounds__(128, 4) aa_local_vec_kernel(const AAArgs<TS> a)
+{
+    using T = typename Store<TS>::C;
+    constexpr int RPW = 32 / LX;
+    const Geom &gm = a.g;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int x0 = (blockIdx.x * LX + (lane % LX)) * V;
+    const int y = blockIdx.y * (4 * RPW) + warp * RPW + lane / LX;
+    if (x0 >= gm.nx || y >= gm.ny)
+        return;
+    const int d = ((int)blockIdx.z + 1) * (int)gm.plane + y * (int)gm.xp + x0;
+
+    const uint32_t kpack = KindIO<V>::load(a.ct.kind + d);
+    T g[Q][V];
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+        PackIO<TS, V>::load(a.f[opp(i)] + d, g[i]);
+    uint32_t c[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+        c[j] = 0u;
+    if (kpack != 0u) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const uint32_t k = (kpack >> (8 * j)) & 0xffu;
+            if (k != 0u)
+                c[j] = cls_of(a.ct, k, d + j);
+        }
+        // a bounced population still lacks its moving-wall term
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            if ((c[j] & CLS_FLAG) == 0 && (c[j] & CLS_MOVING)) {
+                const uint32_t mv = mlinks_of(a.ct, (kpack >> (8 * j)) & 0xffu, d + j);
+#pragma unroll
+                for (int i = 1; i < Q; ++i)
+                    if (mv & (1u << i))
+                        g[i][j] = g[i][j] + a.k[i];
+            }
+    }
+    if constexpr (UsePackedMath<TS>::value)
+        collide_cell_pairs<V>(g, a.omega);
+    else
+        collide_cells<T, V>(g, a.omega);
+    bool allfluid = true;
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+        allfluid &= (c[j] & CLS_FLAG) == 0;
+    if (!allfluid) {
+        // non-fluid cells keep their (still unmodified) values: full-line stores
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            T o[V];
+            PackIO<TS, V>::load(a.f[i] + d, o);
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                if ((c[j] & CLS_FLAG) != 0)
+                    g[i][j] = o[j];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+        PackIO<TS, V>::store(a.f[i] + d, g[i]);
+}
+
+// ---------------------------------------------------------------------------
 // Class words (and the moving-wall link bits) from the padded flag block,
 // halo planes already filled.  One thread per padded element of storage
 // planes [0, nz+2).  Direction i's source is the neighbour at -c_i, with the
@@ -839,6 +1151,37 @@ __global__ void build_cls_kernel(const uint8_t *__restrict__ flags,
             }
     cls[d] = c | (mv ? CLS_MOVING : 0u);
     mlinks[d] = mv;
+}
+
+// The dictionary: every distinct (class word, link bits) pair gets a slot of a
+// 256-entry open-addressing table (slot 0 = the bulk pair (0, 0), slot 255 =
+// escape, never a key); kind[d] = the slot.  Slot numbers depend on insertion
+// order, which no result depends on.
+constexpr unsigned long long KIND_EMPTY = ~0ull;
+__global__ void build_kind_kernel(const uint32_t *__restrict__ cls,
+                                  const uint32_t *__restrict__ mlinks, long long n,
+                                  unsigned long long *__restrict__ tab, uint8_t *__restrict__ kind,
+                                  unsigned int *__restrict__ escapes)
+{
+    const long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n)
+        return;
+    const unsigned long long key = ((unsigned long long)mlinks[d] << 32) | cls[d];
+    if (key == 0ull) {
+        kind[d] = 0;
+        return;
+    }
+    unsigned int h = (unsigned int)((key * 0x9E3779B97F4A7C15ull) >> 40);
+    for (int probe = 0; probe < 254; ++probe) {
+        const unsigned int s = 1u + (h + probe) % 254u;  // 1..254
+        const unsigned long long old = atomicCAS(&tab[s], KIND_EMPTY, key);
+        if (old == KIND_EMPTY || old == key) {
+            kind[d] = (uint8_t)s;
+            return;
+        }
+    }
+    kind[d] = (uint8_t)KIND_ESCAPE;
+    atomicAdd(escapes, 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -1003,7 +1346,7 @@ __device__ __forceinline__ void diag_block_reduce(double (&acc)[DIAG_N], double 
 
 template <typename T>
 __global__ void __launch_bounds__(DIAG_THREADS)
-diag_kernel(const T *__restrict__ f, const uint32_t *__restrict__ cls, const Geom gm,
+diag_kernel(const T *__restrict__ f, const ClsTab ct, const Geom gm,
             double *__restrict__ partials)
 {
     double acc[DIAG_N];
@@ -1021,7 +1364,8 @@ diag_kernel(const T *__restrict__ f, const uint32_t *__restrict__ cls, const Geo
             cell_moments<T>(f, d, gm.pop, rr, mx, my, mz, &bad);
             acc[0] += rr;
             acc[6] += (double)bad;
-            if ((cls[d] & CLS_FLAG) == 0) {
+            const uint32_t kd = ct.kind[d];
+            if (kd == 0 || (cls_of(ct, kd, (int)d) & CLS_FLAG) == 0) {
                 acc[7] += 1.0;
                 acc[1] += mx;
                 acc[2] += my;

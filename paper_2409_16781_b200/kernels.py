@@ -187,6 +187,13 @@ class KernelPlan:
         _cabi.check(self._lib.mlb_plan_get_flags(self._plan, _host_ptr(out)))
         return out
 
+    def geometry_stats(self):
+        """(distinct wall-link patterns in the plan's dictionary, cells that
+        overflowed it and read full-width class words)."""
+        out = (ctypes.c_int64 * 2)()
+        _cabi.check(self._lib.mlb_plan_geometry_stats(self._plan, out))
+        return int(out[0]), int(out[1])
+
     def set_physics(self, omega=None, wall_u=None, inlet_u=None):
         if omega is not None:
             self.omega = float(omega)

@@ -38,7 +38,16 @@ def geometries3d():
     # the pack kernel, must fall back to the list-driven pass
     open_unfusable = open_chain.copy()
     open_unfusable[8, 4, 1:3] = B.OUTLET
+    # random porous medium with moving grains: far more than 254 distinct
+    # wall-link patterns, so the plan's pattern dictionary overflows and the
+    # escape path (full-width class words) is exercised
+    prng = np.random.default_rng(7)
+    porous = B.open_mask(24, 10, 8)
+    u = prng.random(porous.shape)
+    porous[u < 0.25] = B.SOLID
+    porous[u > 0.9] = B.MOVING_WALL
     return {"cavity": (cavity, (0.08, 0.0, 0.0), 0.0),
+            "porous": (porous, (0.03, -0.02, 0.04), 0.0),
             "cavity16": (cavity16, (0.05, 0.0, -0.03), 0.0),
             "channel40": (channel40, (0.0, 0.0, 0.0), 0.06),
             "periodic8": (periodic8, (0.02, 0.03, -0.04), 0.0),

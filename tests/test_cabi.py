@@ -63,3 +63,37 @@ def test_device_layout_mirror_matches_the_library():
         _cabi.check(lib.mlb_layout_query(nx, ny, nz, code, ctypes.byref(lay)))
         m = DeviceLayout(nx, ny, nz, sz)
         assert (m.xp, m.plane, m.pop, m.total) == (lay.xp, lay.plane, lay.pop, lay.total)
+
+
+def test_no_contracted_multiply_adds_in_the_device_code():
+    """Bit-exact parity rests on every floating-point operation being one IEEE
+    rounding.  -fmad=false keeps nvcc / ptxas from contracting scalar a*b+c,
+    but ptxas 12.9 contracts PACKED fp32 multiplies and adds (mul.rn.f32x2 +
+    add.rn.f32x2 -> FFMA2) regardless - which once cost a half-ulp in one of
+    ~20 000 values of the fp16-storage kernels.  Guard: in the built library
+    the only packed FMAs are the exact a - b = FFMA2(b, -1, a) form, and the
+    only scalar FMAs are those of the IEEE division / reciprocal sequences."""
+    import shutil
+    import subprocess
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump) or not os.path.exists(_cabi.LIB_PATH):
+        pytest.skip("cuobjdump or the built library is not available")
+    sass = subprocess.run([cuobjdump, "-sass", _cabi.LIB_PATH], capture_output=True,
+                          text=True, check=True).stdout
+    packed = [ln for ln in sass.splitlines() if " FFMA2 " in ln]
+    assert packed, "expected the packed-fp32 collide in the fp16-storage kernels"
+    bad = [ln.strip() for ln in packed if ", -1, " not in ln]
+    assert not bad, bad[:5]
+    # scalar kernels: count FFMA per kernel; the fused step kernels in fp32 may
+    # only contain the handful that belong to the division sequence (1 / rho)
+    per_kernel, name = {}, None
+    for ln in sass.splitlines():
+        if "Function :" in ln:
+            name = ln.split("Function :")[1].strip()
+            per_kernel[name] = 0
+        elif name and (" FFMA " in ln or " DFMA " in ln):
+            per_kernel[name] += 1
+    for name, n in per_kernel.items():
+        if "step_" in name or "aa_" in name:
+            # one division per cell of a pack: <= 8 packs' worth of Newton steps
+            assert n <= 80, (name, n)

@@ -18,7 +18,7 @@ from .helpers import geometries3d, random_block
 pytestmark = pytest.mark.gpu
 
 PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED1}
-WALL_GEOMS = ["cavity", "cavity_oblique_lid", "cavity16", "periodic", "periodic8", "wide"]
+WALL_GEOMS = ["porous", "cavity", "cavity_oblique_lid", "cavity16", "periodic", "periodic8", "wide"]
 
 
 def make(grid, prec, omega, wall_u):
@@ -44,6 +44,32 @@ def test_inplace_equals_oracle_bitwise(geom, tag, steps, rng):
     assert d.repr == steps % 2
     plan.normalize(d)
     assert d.repr == 0
+    got = np.empty_like(f)
+    plan.download(d, got)
+    np.testing.assert_array_equal(got, want)
+
+
+PACK_VARIANTS = {"f32": [1008, 1016, 1032], "f64": [1008, 1016, 1032],
+                 "f16": [2008, 2016, 2032, 3008, 3016, 3032]}
+
+
+@pytest.mark.parametrize("steps", [1, 2, 7])
+@pytest.mark.parametrize("tag,variant", [(t, v) for t in PACK_VARIANTS for v in PACK_VARIANTS[t]])
+@pytest.mark.parametrize("geom", ["porous", "cavity16", "periodic8", "wide"])
+def test_inplace_pack_kernels_bitwise(geom, tag, variant, steps, rng):
+    """The vectorised in-place kernels (aligned packs, the pack-boundary cell
+    passed between lanes by a shuffle): ragged rows, walls inside and between
+    packs, lanes outside the grid, periodic wrap at both row ends."""
+    grid, wall_u, _ = geometries3d()[geom]
+    prec = PREC[tag]
+    plan, orc = make(grid, prec, 1.45, wall_u)
+    plan.set_variant(variant)
+    f = random_block(rng, grid.size, prec.storage)
+    want = orc.run(f.copy(), f.copy(), steps)
+    d = plan.alloc()
+    plan.upload(f, d)
+    plan.run_steps_inplace(d, steps)
+    plan.normalize(d)
     got = np.empty_like(f)
     plan.download(d, got)
     np.testing.assert_array_equal(got, want)

@@ -83,7 +83,23 @@ def test_multi_step_with_open_pass_bitwise(geom, tag, rng):
     np.testing.assert_array_equal(got, want)
 
 
-VEC_GEOMS = ["cavity16", "channel40", "periodic8", "wide", "duct", "open_chain", "open_unfusable"]
+VEC_GEOMS = ["cavity16", "channel40", "periodic8", "wide", "duct", "open_chain", "open_unfusable",
+             "porous"]
+
+
+def test_pattern_dictionary_and_escape_cells():
+    """The kernels read one index byte per cell into a dictionary of distinct
+    wall-link patterns; geometries with more than 254 patterns send the
+    overflow cells to full-width class words.  Both paths must report the
+    reference's flag bytes exactly."""
+    g = geometries3d()
+    for name, escapes in (("cavity", False), ("channel40", False), ("porous", True)):
+        grid, wall_u, inlet_u = g[name]
+        plan = make_plan(grid, Precision.SINGLE, 1.0, wall_u, inlet_u)
+        kinds, esc = plan.geometry_stats()
+        assert 1 <= kinds <= 255
+        assert (esc > 0) == escapes, (name, kinds, esc)
+        np.testing.assert_array_equal(plan.device_flags(), B.flatten_mask(grid))
 
 
 @pytest.mark.parametrize("passthrough", [False, True])
