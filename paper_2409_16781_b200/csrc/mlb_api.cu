@@ -632,52 +632,91 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     const int nx = p->nx, ny = p->ny, nz = p->nz;
     const long long xp = p->lay.xp, plane = p->lay.plane;
     const size_t padded = (size_t)(nz + 2) * plane;
-    std::vector<uint8_t> pad(padded, (uint8_t)1);  // row padding = solid
+    const size_t dense_plane = (size_t)nx * ny;
+    const uint8_t *src_lo = h_lo ? h_lo : h_flags + (size_t)(nz - 1) * dense_plane;
+    const uint8_t *src_hi = h_hi ? h_hi : h_flags;
+
+    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_mlinks); cudaFree(p->d_in);
+    cudaFree(p->d_kind); cudaFree(p->d_tab);
+    cudaFree(p->d_out); cudaFree(p->d_out_tmp);
+    p->d_flags = nullptr; p->d_cls = p->d_mlinks = nullptr; p->d_in = p->d_out = nullptr;
+    p->d_kind = nullptr; p->d_tab = nullptr;
+    p->d_out_tmp = nullptr;
+    p->have_flags = false;
+    p->n_in = p->n_out = 0;
+
+    // the padded flag block on the device, straight from the caller's dense
+    // array (row padding = solid, never written); no padded host copy
+    MLB_CUDA(cudaMalloc(&p->d_flags, padded));
+    if (xp != nx)
+        MLB_CUDA(cudaMemset(p->d_flags, 1, padded));
+    if (xp == nx)
+        MLB_CUDA(cudaMemcpy(p->d_flags + plane, h_flags, (size_t)nz * dense_plane,
+                            cudaMemcpyHostToDevice));
+    else
+        MLB_CUDA(cudaMemcpy2D(p->d_flags + plane, (size_t)xp, h_flags, (size_t)nx, (size_t)nx,
+                              (size_t)nz * ny, cudaMemcpyHostToDevice));
+    MLB_CUDA(cudaMemcpy2D(p->d_flags, (size_t)xp, src_lo, (size_t)nx, (size_t)nx, (size_t)ny,
+                          cudaMemcpyHostToDevice));
+    MLB_CUDA(cudaMemcpy2D(p->d_flags + (size_t)(nz + 1) * plane, (size_t)xp, src_hi, (size_t)nx,
+                          (size_t)nx, (size_t)ny, cudaMemcpyHostToDevice));
+
+    // census on the device: open-boundary cells (inlet / outlet index lists are
+    // needed only if there are any) and invalid codes.  A cavity or a periodic
+    // box never walks its flags on the host.
+    unsigned long long *d_census = nullptr, census[3] = {0, 0, 0};
+    MLB_CUDA(cudaMalloc(&d_census, sizeof(census)));
+    MLB_CUDA(cudaMemset(d_census, 0, sizeof(census)));
+    {
+        const dim3 cgrid((unsigned)((xp + 255) / 256), ny, nz + 2);
+        mlb::flag_census_kernel<<<cgrid, 256>>>(p->d_flags, p->g, d_census);
+        MLB_LAUNCHED();
+    }
+    MLB_CUDA(cudaMemcpy(census, d_census, sizeof(census), cudaMemcpyDeviceToHost));
+    cudaFree(d_census);
+
     std::vector<long long> in_idx, out_idx;
     p->in_zoff.assign(nz + 1, 0);
     p->out_zoff.assign(nz + 1, 0);
     p->out_xmod8 = 0;
-    const size_t dense_plane = (size_t)nx * ny;
-    for (int sz = 0; sz < nz + 2; ++sz) {
-        const uint8_t *src;
-        if (sz == 0)
-            src = h_lo ? h_lo : h_flags + (size_t)(nz - 1) * dense_plane;
-        else if (sz == nz + 1)
-            src = h_hi ? h_hi : h_flags;
-        else
-            src = h_flags + (size_t)(sz - 1) * dense_plane;
-        const bool interior = sz >= 1 && sz <= nz;
-        if (interior) {
-            p->in_zoff[sz - 1] = (long long)in_idx.size();
-            p->out_zoff[sz - 1] = (long long)out_idx.size();
-        }
-        for (int y = 0; y < ny; ++y) {
-            const uint8_t *row = src + (size_t)y * nx;
-            const long long d0 = (long long)sz * plane + (long long)y * xp;
-            std::memcpy(&pad[d0], row, (size_t)nx);
-            // rows of plain fluid/solid/lid cells (all but a few) need no
-            // per-cell work: one vectorisable scan finds the exceptions
-            uint8_t special = 0;
-            for (int x = 0; x < nx; ++x)
-                special |= (uint8_t)(row[x] >= 3);
-            if (!special)
-                continue;
-            for (int x = 0; x < nx; ++x) {
-                const uint8_t m = row[x];
-                if (m > 4)
-                    return fail(MLB_EINVAL, "flag array holds unknown cell code %d at "
-                                "(x=%d, y=%d, plane=%d)", (int)m, x, y, sz - 1);
-                if (!interior)
+    if (census[0] || census[1] || census[2]) {
+        in_idx.reserve(census[0]);
+        out_idx.reserve(census[1]);
+        for (int sz = 0; sz < nz + 2; ++sz) {
+            const uint8_t *src = sz == 0 ? src_lo : sz == nz + 1 ? src_hi
+                                                  : h_flags + (size_t)(sz - 1) * dense_plane;
+            const bool interior = sz >= 1 && sz <= nz;
+            if (interior) {
+                p->in_zoff[sz - 1] = (long long)in_idx.size();
+                p->out_zoff[sz - 1] = (long long)out_idx.size();
+            }
+            for (int y = 0; y < ny; ++y) {
+                const uint8_t *row = src + (size_t)y * nx;
+                const long long d0 = (long long)sz * plane + (long long)y * xp;
+                // rows of plain fluid / solid / lid cells (all but a few) need no
+                // per-cell work: one vectorisable scan finds the exceptions
+                uint8_t special = 0;
+                for (int x = 0; x < nx; ++x)
+                    special |= (uint8_t)(row[x] >= 3);
+                if (!special)
                     continue;
-                if (m == 3)
-                    in_idx.push_back(d0 + x);
-                else if (m == 4) {
-                    if (interior)
+                for (int x = 0; x < nx; ++x) {
+                    const uint8_t m = row[x];
+                    if (m > 4)
+                        return fail(MLB_EINVAL, "flag array holds unknown cell code %d at "
+                                    "(x=%d, y=%d, plane=%d)", (int)m, x, y, sz - 1);
+                    if (!interior)
+                        continue;
+                    if (m == 3)
+                        in_idx.push_back(d0 + x);
+                    else if (m == 4) {
                         p->out_xmod8 |= 1u << (x & 7);
-                    if (x == 0)
-                        return fail(MLB_EUNSUPPORTED, "outlet cell at x = 0 (y=%d, z=%d): "
-                                    "its source would be the previous row's last cell", y, sz - 1);
-                    out_idx.push_back(d0 + x);
+                        if (x == 0)
+                            return fail(MLB_EUNSUPPORTED, "outlet cell at x = 0 (y=%d, z=%d): "
+                                        "its source would be the previous row's last cell", y,
+                                        sz - 1);
+                        out_idx.push_back(d0 + x);
+                    }
                 }
             }
         }
@@ -695,17 +734,8 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     if (p->out_chained)
         p->passthrough = 0;  // see mlb_plan_set_passthrough
 
-    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_mlinks); cudaFree(p->d_in);
-    cudaFree(p->d_kind); cudaFree(p->d_tab);
-    cudaFree(p->d_out); cudaFree(p->d_out_tmp);
-    p->d_flags = nullptr; p->d_cls = p->d_mlinks = nullptr; p->d_in = p->d_out = nullptr;
-    p->d_kind = nullptr; p->d_tab = nullptr;
-    p->d_out_tmp = nullptr;
-    p->have_flags = false;
-    MLB_CUDA(cudaMalloc(&p->d_flags, padded));
     MLB_CUDA(cudaMalloc(&p->d_cls, padded * sizeof(uint32_t)));
     MLB_CUDA(cudaMalloc(&p->d_mlinks, padded * sizeof(uint32_t)));
-    MLB_CUDA(cudaMemcpy(p->d_flags, pad.data(), padded, cudaMemcpyHostToDevice));
     p->n_in = (long long)in_idx.size();
     p->n_out = (long long)out_idx.size();
     if (p->n_in) {
@@ -746,6 +776,8 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
         cudaFree(p->d_cls); cudaFree(p->d_mlinks);
         p->d_cls = p->d_mlinks = nullptr;
     }
+    cudaFree(p->d_flags);  // only the build reads the raw flag block
+    p->d_flags = nullptr;
     p->have_flags = true;
     return MLB_OK;
 }

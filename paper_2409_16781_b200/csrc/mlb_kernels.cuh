@@ -1153,6 +1153,27 @@ __global__ void build_cls_kernel(const uint8_t *__restrict__ flags,
     mlinks[d] = mv;
 }
 
+// Census of the padded flag block: [0] inlet cells, [1] outlet cells (slab
+// planes only), [2] unknown codes (anywhere, halo planes included).
+__global__ void flag_census_kernel(const uint8_t *__restrict__ flags, const Geom gm,
+                                   unsigned long long *__restrict__ out)
+{
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int sz = blockIdx.z;
+    uint8_t m = 0;
+    if (x < gm.nx)
+        m = flags[(long long)sz * gm.plane + (long long)blockIdx.y * gm.xp + x];
+    const bool interior = sz >= 1 && sz <= gm.nz;
+    const unsigned b3 = __ballot_sync(0xffffffffu, interior && m == 3);
+    const unsigned b4 = __ballot_sync(0xffffffffu, interior && m == 4);
+    const unsigned bx = __ballot_sync(0xffffffffu, m > 4);
+    if ((threadIdx.x & 31) == 0) {
+        if (b3) atomicAdd(&out[0], (unsigned long long)__popc(b3));
+        if (b4) atomicAdd(&out[1], (unsigned long long)__popc(b4));
+        if (bx) atomicAdd(&out[2], (unsigned long long)__popc(bx));
+    }
+}
+
 // The dictionary: every distinct (class word, link bits) pair gets a slot of a
 // 256-entry open-addressing table (slot 0 = the bulk pair (0, 0), slot 255 =
 // escape, never a key); kind[d] = the slot.  Slot numbers depend on insertion

@@ -217,7 +217,7 @@ def state_from_macroscopic(rho, ux, uy, uz, mask_grid, layout, precision,
         params=params, wall_u=tuple(wall_u), inlet_u=float(inlet_u), case=case)
 
 
-def build_plan(state, config):
+def build_plan(state, config, defer_flags=False):
     """KernelPlan for a state (engine.py:183-190), same error behaviour."""
     if state.params is None:
         raise ValueError("state has no relaxation parameters attached")
@@ -226,7 +226,8 @@ def build_plan(state, config):
     tile = config.schedule.resolve(state.nx, state.ny, state.nz, state.layout)
     return KernelPlan(state.nx, state.ny, state.nz, state.layout, state.precision,
                       state.mask, state.params.omega, state.wall_u, tile,
-                      inlet_u=state.inlet_u, device=config.device)
+                      inlet_u=state.inlet_u, device=config.device,
+                      defer_flags=defer_flags)
 
 
 class Session:
@@ -258,7 +259,8 @@ class Session:
 
     def upload(self):
         st = self.state
-        self.plan.upload(st.f_pre.data, self.pre)
+        self.plan.upload(st.f_pre.data, self.pre)   # asynchronous (pinned host block)
+        self.plan.ensure_flags()                    # flag tables, while the DMA runs
         if self.inplace:
             self.pre.repr = 0
             self.host_stale = False
@@ -323,7 +325,8 @@ def open_session(state, config=None):
         return state.session
     config = config or RunConfig(steps=1, precision=state.precision,
                                  layout=state.layout)
-    state.session = Session(state, build_plan(state, config), inplace=config.inplace)
+    state.session = Session(state, build_plan(state, config, defer_flags=True),
+                            inplace=config.inplace)
     return state.session
 
 

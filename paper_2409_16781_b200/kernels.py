@@ -81,7 +81,7 @@ class KernelPlan:
     def __init__(self, nx, ny, nz, layout, precision, mask, omega,
                  wall_u=(0.0, 0.0, 0.0), tile=None, backend=None, *,
                  inlet_u=0.0, device=None, halo_lo=None, halo_hi=None,
-                 slab=False):
+                 slab=False, defer_flags=False):
         self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
         if layout is not Layout.ROW:
             raise ValueError("the CUDA path stores x fastest (Layout.ROW) only")
@@ -137,16 +137,31 @@ class KernelPlan:
 
         def plane(h):
             if h is None:
-                return None, ctypes.c_void_p(None)
+                return None
             h = np.ascontiguousarray(h, dtype=np.uint8).reshape(-1)
             if h.size != self.nx * self.ny:
                 raise ValueError("halo flag plane must have nx*ny cells")
-            return h, _host_ptr(h)
-        lo, lo_p = plane(halo_lo)
-        hi, hi_p = plane(halo_hi)
-        _cabi.check(lib.mlb_plan_set_flags(self._plan, _host_ptr(mask), lo_p, hi_p))
+            return h
+        self._halo = (plane(halo_lo), plane(halo_hi))
+        self._flags_set = False
         self._scratch = None
         self.passthrough = False
+        # defer_flags: the caller starts its (asynchronous) population upload
+        # first and calls ensure_flags() while the DMA runs
+        if not defer_flags:
+            self.ensure_flags()
+
+    def ensure_flags(self):
+        """Hand the flag array to the library (builds the per-cell tables on
+        the device).  Idempotent."""
+        if self._flags_set:
+            return
+        lo, hi = self._halo
+        _cabi.check(self._lib.mlb_plan_set_flags(
+            self._plan, _host_ptr(self.mask),
+            _host_ptr(lo) if lo is not None else ctypes.c_void_p(None),
+            _host_ptr(hi) if hi is not None else ctypes.c_void_p(None)))
+        self._flags_set = True
 
     # -- lifetime ----------------------------------------------------------
     def close(self):

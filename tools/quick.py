@@ -15,6 +15,9 @@ mask = B.flatten_mask(B.cavity_mask(n, n, n))
 for prec in (Precision.SINGLE, Precision.DOUBLE, Precision.MIXED1):
     for mode in ("ab", "inplace"):
         plan = KernelPlan(n, n, n, Layout.ROW, prec, mask, 1.53, (0.1, 0, 0))
+        if os.environ.get("MLB_VARIANT"):
+            v = int(os.environ["MLB_VARIANT"])
+            plan.set_variant(v if prec is not Precision.MIXED1 else v + 1000)
         a = plan.alloc()
         for q in range(19):
             a.tensor[q].fill_(float(W[q]))
