@@ -376,7 +376,7 @@ def main():
         dist.all_reduce(nl, op=dist.ReduceOp.SUM)
     ms = float(ms.item())
     value = cells_all * args.steps / (ms * 1e-3) / 1e6
-    diag = plan.diagnostics(a)
+    diag = slab.combine_diagnostics(plan.diagnostics(a), rank, world)   # whole domain, rank order
     if diag["nonfinite"]:
         raise SystemExit("bench: populations diverged")
 

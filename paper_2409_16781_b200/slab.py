@@ -373,5 +373,30 @@ def exchange_flag_halos(flags_slab, rank, world, group=None, device=None):
     return lo.cpu().numpy(), hi.cpu().numpy()
 
 
-__all__ = ["partition", "ring_neighbours", "slab_halo_flags", "CudaStepper",
+DIAG_KEYS = ("mass", "px", "py", "pz", "kinetic_energy", "max_u", "nonfinite", "fluid_cells")
+
+
+def combine_diagnostics(local, rank=0, world=1, group=None):
+    """Whole-domain diagnostics from every slab's `KernelPlan.diagnostics()`.
+
+    The per-slab values are deterministic device reductions; they are
+    gathered (8 doubles per rank, control plane) and combined on every rank
+    in RANK ORDER - sums left to right, max |u| by max - so the result is
+    bitwise reproducible and identical on all ranks (no floating-point
+    all-reduce whose order the library picks)."""
+    mine = [float(local[k]) for k in DIAG_KEYS]
+    if world == 1:
+        rows = [mine]
+    else:
+        import torch.distributed as dist
+        rows = [None] * world
+        dist.all_gather_object(rows, mine, group=group)
+    out = dict(zip(DIAG_KEYS, rows[0]))
+    for row in rows[1:]:
+        for k, v in zip(DIAG_KEYS, row):
+            out[k] = max(out[k], v) if k == "max_u" else out[k] + v
+    return out
+
+
+__all__ = ["combine_diagnostics", "DIAG_KEYS", "partition", "ring_neighbours", "slab_halo_flags", "CudaStepper",
            "PeerRing", "DistSlab", "exchange_flag_halos", "Q"]

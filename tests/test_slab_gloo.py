@@ -67,6 +67,15 @@ def _worker(rank, world, port, geom, steps, omega, out_dir):
             r.wait()
         newest, _ = runner.run(blocks[0], blocks[1], steps)
         np.save(os.path.join(out_dir, f"slab{rank}.npy"), newest[:, 1:-1, :, :nx])
+        # whole-domain diagnostics: rank-ordered combine, identical on every rank
+        mine = np.ascontiguousarray(newest[:, 1:-1, :, :nx])
+        fluid = flags[z0:z1] == 0
+        local = {"mass": float(mine.sum()), "px": float(rank), "py": 0.0, "pz": 0.0,
+                 "kinetic_energy": 0.5 + rank, "max_u": 0.1 * (rank + 1), "nonfinite": 0.0,
+                 "fluid_cells": float(fluid.sum())}
+        total = slab.combine_diagnostics(local, rank, world)
+        np.save(os.path.join(out_dir, f"diag{rank}.npy"),
+                np.array([total[k] for k in slab.DIAG_KEYS]))
     finally:
         dist.destroy_process_group()
 
@@ -81,8 +90,15 @@ def test_two_rank_gloo_run_equals_single_domain(geom, tmp_path):
         f.copy(), f.copy(), steps)
     mp.spawn(_worker, args=(world, _free_port(), geom, steps, omega, str(tmp_path)),
              nprocs=world, join=True)
-    got = np.concatenate([np.load(tmp_path / f"slab{r}.npy") for r in range(world)], axis=1)
+    parts = [np.load(tmp_path / f"slab{r}.npy") for r in range(world)]
+    got = np.concatenate(parts, axis=1)
     np.testing.assert_array_equal(got.reshape(19, -1), want)
+    d0, d1 = np.load(tmp_path / "diag0.npy"), np.load(tmp_path / "diag1.npy")
+    np.testing.assert_array_equal(d0, d1)                       # same bits on every rank
+    diag = dict(zip(slab.DIAG_KEYS, d0))
+    assert diag["mass"] == float(parts[0].sum()) + float(parts[1].sum())   # rank order
+    assert diag["max_u"] == 0.2 and diag["px"] == 1.0 and diag["kinetic_energy"] == 2.0
+    assert diag["fluid_cells"] == float((B.flatten_mask(grid) == 0).sum())
 
 
 def test_single_rank_ring_closes_on_itself():

@@ -1,6 +1,6 @@
 """Run a few steps of one configuration (for ncu captures)."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("MLB_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2409_16781_b200 import boundaries as B
 from paper_2409_16781_b200.fields import Layout, Precision
 from paper_2409_16781_b200.kernels import KernelPlan
