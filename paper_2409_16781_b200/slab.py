@@ -130,10 +130,21 @@ class PeerRing:
             self.below = self.above = mine
             return
         import torch.distributed as dist
-        card = {"nz": plan.nz, "blocks": [self._export(b.tensor.data_ptr()) for b in self.blocks],
-                "sig": self._export(self.sig)}
+        # every rank reaches the all-gather, also one whose export failed (its
+        # card then carries the error and every rank raises the same way)
+        try:
+            card = {"nz": plan.nz,
+                    "blocks": [self._export(b.tensor.data_ptr()) for b in self.blocks],
+                    "sig": self._export(self.sig)}
+        except (RuntimeError, ValueError) as exc:
+            card = {"error": f"rank {rank}: {exc}"}
         cards = [None] * world
         dist.all_gather_object(cards, card, group=group)
+        errors = [c["error"] for c in cards if "error" in c]
+        if errors:
+            lib.mlb_signal_destroy(ctypes.c_void_p(self.sig))
+            self.sig = None
+            raise RuntimeError("peer ring: " + "; ".join(errors))
         self.below = self._map(cards[below])
         self.above = self.below if above == below else self._map(cards[above])
 
