@@ -158,9 +158,12 @@ int mlb_run_steps(mlb_plan *plan, void *d_a, void *d_b, int nsteps,
  * mlb_upload writes and mlb_download / mlb_macro / mlb_diagnostics expect)
  * and a shifted one (*repr == 1) after an odd number of steps;
  * mlb_inplace_normalize brings it back to 0 without stepping.  *repr is
- * updated by both calls.  Walls only: plans whose flags contain INLET /
- * OUTLET cells, and MLB_Z_HALO plans, are rejected (MLB_EUNSUPPORTED).
- * Non-fluid cells are never modified. */
+ * updated by both calls.  Wall cells are never modified.  INLET / OUTLET
+ * cells are served by the pack kernels only (variant W*1000 + LX, or auto
+ * with nx >= 128), which apply the open-boundary pass inside the step when
+ * every outlet cell's x-1 neighbour lies in the same pack and no outlet cell
+ * copies from another; otherwise, and for MLB_Z_HALO plans, the call is
+ * rejected (MLB_EUNSUPPORTED). */
 int mlb_run_steps_inplace(mlb_plan *plan, void *d_f, int nsteps, int *repr,
                           void *stream, float *ms);
 int mlb_inplace_normalize(mlb_plan *plan, void *d_f, int *repr, void *stream);

@@ -357,6 +357,10 @@ void fill_aa(mlb_plan *p, void *f, mlb::AAArgs<TS> &a)
     a.g = p->g;
     a.omega = T(p->omega);
     wall_terms<T>(p->wall_u, a.k);
+    T cv[MLB_Q];
+    inlet_values<T>(p->inlet_u, cv);  // compute dtype, then storage dtype (engine.py:167-171)
+    for (int q = 0; q < MLB_Q; ++q)
+        a.inlet[q] = mlb::Store<TS>::down(cv[q]);
 }
 
 template <typename TS>
@@ -394,21 +398,50 @@ int launch_aa_vec_lx(mlb_plan *p, void *f, int kind, int lx, cudaStream_t st)
     return launch_aa_vec<TS, V, 32>(p, f, kind, st);
 }
 
+// the variant the in-place kernels run with (0 = auto: packs whenever the row
+// length allows)
+int resolve_aa_variant(const mlb_plan *p)
+{
+    if (p->variant != 0)
+        return p->variant;
+    if (p->dtype == MLB_F32 && p->nx % 4 == 0 && p->nx >= 128) return 1016;
+    if (p->dtype == MLB_F64 && p->nx % 2 == 0 && p->nx >= 128) return 1016;
+    if (p->dtype == MLB_F16 && p->nx % 4 == 0 && p->nx >= 128) return 2016;
+    return 128;
+}
+
+bool aa_uses_packs(const mlb_plan *p, int variant)
+{
+    return variant >= 1000 && variant_exists(p->dtype, variant)
+        && p->nx % pack_cells(p->dtype, variant) == 0;
+}
+
+// Open boundaries in place: the pack kernels apply the pass inside the step
+// (inlet cells take the constant, outlet cells copy their x-1 neighbour inside
+// the pack), which needs every outlet cell's x-1 neighbour in the same pack and
+// no outlet cell copying from another outlet cell.
+bool aa_open_ok(const mlb_plan *p, int variant)
+{
+    if (p->n_in == 0 && p->n_out == 0)
+        return true;
+    if (!aa_uses_packs(p, variant) || p->out_chained)
+        return false;
+    const int V = pack_cells(p->dtype, variant);
+    for (int r = 0; r < 8; r += V)
+        if (p->out_xmod8 & (1u << r))
+            return false;
+    return true;
+}
+
 // the in-place step kernels follow the plan's variant: pack kernels when the
-// two-buffer path would use one (and always for the swap: scalar)
+// two-buffer path would use one (the swap is always scalar)
 int launch_aa_any(mlb_plan *p, void *f, int kind, cudaStream_t st)
 {
-    int variant = p->variant;
-    if (variant == 0) {  // auto: packs whenever the row length allows
-        if (p->dtype == MLB_F32 && p->nx % 4 == 0 && p->nx >= 128) variant = 1016;
-        else if (p->dtype == MLB_F64 && p->nx % 2 == 0 && p->nx >= 128) variant = 1016;
-        else if (p->dtype == MLB_F16 && p->nx % 4 == 0 && p->nx >= 128) variant = 2016;
-        else variant = 128;
-    }
+    const int variant = resolve_aa_variant(p);
     if (!variant_exists(p->dtype, variant))
         return fail(MLB_EINVAL, "kernel variant %d does not exist for dtype code %d", variant,
                     p->dtype);
-    const bool vec = variant >= 1000 && kind != 2 && p->nx % pack_cells(p->dtype, variant) == 0;
+    const bool vec = kind != 2 && aa_uses_packs(p, variant);
     const int lx = variant % 1000;
     if (p->dtype == MLB_F32)
         return vec ? launch_aa_vec_lx<float, 4>(p, f, kind, lx, st) : launch_aa<float>(p, f, kind, st);
@@ -924,9 +957,11 @@ static int check_inplace(const mlb_plan *p, const void *d_f, const int *repr)
     if (p->z_mode != MLB_Z_PERIODIC)
         return fail(MLB_EUNSUPPORTED, "the in-place update needs an MLB_Z_PERIODIC plan "
                     "(whole domain on one GPU)");
-    if (p->n_in || p->n_out)
-        return fail(MLB_EUNSUPPORTED, "the in-place update handles walls only; this geometry "
-                    "has %lld inlet and %lld outlet cells - use the two-buffer path",
+    if (!aa_open_ok(p, resolve_aa_variant(p)))
+        return fail(MLB_EUNSUPPORTED, "the in-place update handles walls only unless a pack "
+                    "kernel runs (nx a multiple of the pack, variant W*1000 + LX or auto with "
+                    "nx >= 128) and every outlet cell has its x-1 neighbour in the same pack; this "
+                    "geometry has %lld inlet and %lld outlet cells - use the two-buffer path",
                     p->n_in, p->n_out);
     return MLB_OK;
 }

@@ -431,7 +431,18 @@ struct AAArgs {
     Geom g;
     T omega;
     T k[Q];
+    TS inlet[Q];  // equilibrium(1, u_in, 0, 0), storage dtype (open boundaries, pack kernels)
 };
+
+// In place, every non-wall cell takes part in the exchange of slots: fluid cells
+// collide; an INLET cell's new state is the constant equilibrium; an OUTLET
+// cell's new state is the new state of its x-1 neighbour (engine.py:156-180,
+// applied here as part of the step).
+__device__ __forceinline__ bool aa_participant(uint32_t c)
+{
+    const uint32_t fl = c & CLS_FLAG;
+    return fl != 1u && fl != 2u;
+}
 
 template <typename TS>
 struct CellPos {
@@ -571,7 +582,7 @@ __global__ void __launch_bounds__(BX) aa_swap_kernel(const AAArgs<TS> a)
     aa_offsets<TS>(a.g, x, blockIdx.y, blockIdx.z, d, off);
     const uint32_t kd = a.ct.kind[d];
     const uint32_t cd = kd == 0 ? 0u : cls_of(a.ct, kd, d);
-    if (cd & CLS_FLAG)
+    if (!aa_participant(cd))
         return;
 #pragma unroll
     for (int q = 1; q < Q; ++q) {
@@ -936,6 +947,43 @@ __global__ void __launch_bounds__(128, MLB_AA_MINB) aa_pull_vec_kernel(const AAA
     else
         collide_cells<T, V>(g, a.omega);
 
+    // open-boundary cells of the pack: their new state by rule instead of by
+    // collision (same order as the fused two-buffer pass: walls hold their own
+    // values, inlet cells the constant, then outlet cells copy their x-1
+    // neighbour, right to left; the host checked that no outlet cell starts a pack)
+    uint32_t fl_any = 0u;
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+        fl_any |= 1u << (c[j] & CLS_FLAG);
+    if (fl_any & ((1u << 3) | (1u << 4))) {
+        if ((fl_any & (1u << 4)) && (fl_any & ((1u << 1) | (1u << 2)))) {
+            // an outlet cell may copy from a wall cell: the wall's own (untouched) values
+#pragma unroll
+            for (int i = 0; i < Q; ++i) {
+                T o[V];
+                PackIO<TS, V>::load(a.f[i] + d, o);
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    if (!aa_participant(c[j]))
+                        g[i][j] = o[j];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            if ((c[j] & CLS_FLAG) == 3) {
+#pragma unroll
+                for (int i = 0; i < Q; ++i)
+                    g[i][j] = Store<TS>::up(a.inlet[i]);
+            }
+#pragma unroll
+        for (int j = V - 1; j >= 1; --j)
+            if ((c[j] & CLS_FLAG) == 4) {
+#pragma unroll
+                for (int i = 0; i < Q; ++i)
+                    g[i][j] = g[i][j - 1];
+            }
+    }
+
     // ---- stores ---------------------------------------------------------------
     // Bulk packs (no link bounces, every target location has this one writer):
     // aligned packs wherever the neighbouring lane can supply (or take) the
@@ -1006,11 +1054,11 @@ __global__ void __launch_bounds__(128, MLB_AA_MINB) aa_pull_vec_kernel(const AAA
     // link - stays in the cell's own slot of opp(i) (kernels.py:88-96 read that)
 #pragma unroll
     for (int j = 0; j < V; ++j)
-        if ((c[j] & CLS_FLAG) == 0)
+        if (aa_participant(c[j]))
             a.f[0][d + j] = Store<TS>::down(g[0][j]);
 #define MLB_X(i, CX, Z, R)                                                            \
     _Pragma("unroll") for (int j = 0; j < V; ++j)                                     \
-        if ((c[j] & CLS_FLAG) == 0) {                                                 \
+        if (aa_participant(c[j])) {                                                   \
             const int xs = (CX) == 0 ? x0 + j                                         \
                          : (CX) > 0 ? (j == 0 ? xl : x0 + j - 1)                      \
                                     : (j == V - 1 ? xr : x0 + j + 1);                 \
@@ -1071,7 +1119,7 @@ __global__ void __launch_bounds__(128, 4) aa_local_vec_kernel(const AAArgs<TS> a
     for (int j = 0; j < V; ++j)
         allfluid &= (c[j] & CLS_FLAG) == 0;
     if (!allfluid) {
-        // non-fluid cells keep their (still unmodified) values: full-line stores
+        // wall cells keep their (still unmodified) values: full-line stores
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
             T o[V];
@@ -1081,6 +1129,21 @@ __global__ void __launch_bounds__(128, 4) aa_local_vec_kernel(const AAArgs<TS> a
                 if ((c[j] & CLS_FLAG) != 0)
                     g[i][j] = o[j];
         }
+        // open-boundary cells: new state by rule (see aa_pull_vec_kernel)
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            if ((c[j] & CLS_FLAG) == 3) {
+#pragma unroll
+                for (int i = 0; i < Q; ++i)
+                    g[i][j] = Store<TS>::up(a.inlet[i]);
+            }
+#pragma unroll
+        for (int j = V - 1; j >= 1; --j)
+            if ((c[j] & CLS_FLAG) == 4) {
+#pragma unroll
+                for (int i = 0; i < Q; ++i)
+                    g[i][j] = g[i][j - 1];
+            }
     }
 #pragma unroll
     for (int i = 0; i < Q; ++i)
@@ -1122,10 +1185,12 @@ __global__ void build_cls_kernel(const uint8_t *__restrict__ flags,
         return;
     }
     const uint32_t fl = flags[d];
-    if (sz == 0 || sz == gm.nz + 1 || fl != 0) {
-        cls[d] = fl;  // halo planes are only ever sources; non-fluid cells have no links
+    if (sz == 0 || sz == gm.nz + 1 || fl == 1 || fl == 2) {
+        cls[d] = fl;  // halo planes are only ever sources; walls have no links
         return;
     }
+    // fluid cells - and inlet / outlet cells, whose link bits only the in-place
+    // kernels look at (there every non-wall cell takes part in the exchange)
     const int lz = sz - 1;
     // index 0: same, 1: the "minus" neighbour (source for c = +1), 2: the "plus" one
     const int xs[3] = {x, (x == 0) ? gm.nx - 1 : x - 1, (x == gm.nx - 1) ? 0 : x + 1};
@@ -1149,7 +1214,7 @@ __global__ void build_cls_kernel(const uint8_t *__restrict__ flags,
                 if (m == 2)
                     mv |= 1u << i;
             }
-    cls[d] = c | (mv ? CLS_MOVING : 0u);
+    cls[d] = fl | c | (mv ? CLS_MOVING : 0u);
     mlinks[d] = mv;
 }
 

@@ -243,9 +243,6 @@ class Session:
         self.state = state
         self.plan = plan
         self.inplace = bool(inplace)
-        if self.inplace and np.any(state.mask >= boundaries.INLET):
-            raise ValueError("the in-place update handles walls only; this "
-                             "geometry has inlet/outlet cells - use inplace=False")
         self.pre = plan.alloc()
         self.post = None if self.inplace else plan.alloc()
         self.host_stale = False

@@ -102,6 +102,48 @@ def test_split_runs_and_normalize_in_the_middle(rng):
     assert plan.diagnostics(d) == plan.diagnostics(newest)
 
 
+@pytest.mark.parametrize("steps", [1, 2, 7])
+@pytest.mark.parametrize("tag,variant", [("f32", 1008), ("f32", 1016), ("f64", 1008), ("f64", 1032),
+                                         ("f16", 2008), ("f16", 3016)])
+@pytest.mark.parametrize("geom", ["channel40", "duct", "channel"])
+def test_inplace_open_boundaries_bitwise(geom, tag, variant, steps, rng):
+    """Inlet / outlet cells in place: with the pack kernels every non-wall cell
+    takes part in the exchange of slots - inlet cells' new state is the
+    constant equilibrium, outlet cells copy their x-1 neighbour inside the
+    pack - and the result equals step + open-boundary pass of the oracle."""
+    from paper_2409_16781_b200.kernels import KernelPlan
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    nx, ny, nz = grid.shape
+    prec = PREC[tag]
+    if geom == "channel" and variant // 1000 != 3 and prec is not Precision.DOUBLE:
+        pytest.skip("nx = 14 is not a multiple of this pack")
+    plan = KernelPlan(nx, ny, nz, Layout.ROW, prec, B.flatten_mask(grid), 1.3, wall_u,
+                      inlet_u=inlet_u)
+    plan.set_variant(variant)
+    orc = CpuOracle(nx, ny, nz, B.flatten_mask(grid), 1.3, wall_u, inlet_u)
+    f = random_block(rng, grid.size, prec.storage)
+    want = orc.run(f.copy(), f.copy(), steps)
+    d = plan.alloc()
+    plan.upload(f, d)
+    plan.run_steps_inplace(d, steps)
+    plan.normalize(d)
+    got = np.empty_like(f)
+    plan.download(d, got)
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("geom", ["open_chain", "open_unfusable"])
+def test_inplace_refuses_outlets_it_cannot_serve_inside_a_pack(geom):
+    from paper_2409_16781_b200.kernels import KernelPlan
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    nx, ny, nz = grid.shape
+    plan = KernelPlan(nx, ny, nz, Layout.ROW, Precision.SINGLE, B.flatten_mask(grid), 1.0,
+                      wall_u, inlet_u=inlet_u)
+    plan.set_variant(1008)
+    with pytest.raises(ValueError, match="walls only"):
+        plan.run_steps_inplace(plan.alloc(zero=True), 1)
+
+
 def test_open_boundaries_are_rejected(rng):
     grid, wall_u, inlet_u = geometries3d()["channel40"]
     from paper_2409_16781_b200.kernels import KernelPlan
@@ -166,3 +208,18 @@ def test_ldc_1024_cubed_fp32_on_one_gpu():
     wall = d.tensor[:, 1:-1, 0, :n]
     assert all(bool((wall[q] == float(np.float32(L.W[q]))).all()) for q in range(19))
     print(f"1024^3 fp32 in place: {n ** 3 * 6 / ms / 1e3:.0f} MLUPS")
+
+
+def test_engine_run_inplace_channel_equals_two_buffer_run():
+    """engine.run(inplace=True) on a channel with inlet, outlet and obstacle
+    (nx = 128: the pack kernels serve the open boundaries inside the step)."""
+    from paper_2409_16781_b200 import cases, engine
+    spec = cases.CaseSpec("vks", 128, 48, 12, re=100.0, u0=0.08)
+    a = cases.init(spec, Precision.SINGLE)
+    b = cases.init(spec, Precision.SINGLE)
+    engine.run(a, engine.RunConfig(steps=23))
+    engine.run(b, engine.RunConfig(steps=23, inplace=True))
+    np.testing.assert_array_equal(a.f_pre.data, b.f_pre.data)
+    orc = CpuOracle(128, 48, 12, a.mask, a.params.omega, inlet_u=a.inlet_u, threads=8)
+    f0 = cases.init(spec, Precision.SINGLE).f_pre.data
+    np.testing.assert_array_equal(a.f_pre.data, orc.run(f0.copy(), f0.copy(), 23))

@@ -18,3 +18,14 @@ b = plan.alloc(); b.tensor.copy_(a.tensor)
 plan.run_steps(a, b, 4)
 _, _, ms = plan.run_steps(a, b, 20, timed=True)
 print(f"channel: {nx*ny*nz*20/ms/1e3:.0f} MLUPS, {ms/20:.3f} ms/step")
+# the same channel in place (one block): bit-compare with the two-buffer result
+import torch
+newest = a  # 24 steps (even) end in a
+c = plan.alloc()
+for q in range(19):
+    c.tensor[q].fill_(float(eq[q]))
+plan.run_steps_inplace(c, 4)
+ms = plan.run_steps_inplace(c, 20, timed=True)
+plan.normalize(c)
+same = bool(torch.equal(c.tensor[:, 1:-1], newest.tensor[:, 1:-1]))
+print(f"channel in place: {nx*ny*nz*20/ms/1e3:.0f} MLUPS, {ms/20:.3f} ms/step, equals two-buffer result bitwise: {same}")
