@@ -292,49 +292,8 @@ def main():
     runner = None
     transport = None
 
-    def agree(ok):
-        """Every rank takes the same branch: True only if all ranks say so."""
-        if world == 1:
-            return bool(ok)
-        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=device)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        return bool(flag.item())
-
-    def halo_planes(blk):
-        t = blk.tensor
-        return torch.stack([t[q, 0] for q in slab.UP] + [t[q, n + 1] for q in slab.DOWN])
-
     def make_runner(p, x, y):
-        """DistSlab over the peer ring when it can be set up and delivers the
-        very planes the send/recv exchange delivers, else over send/recv."""
-        why = None
-        if args.transport == "peer":
-            ring, err = None, None
-            try:
-                ring = slab.PeerRing(p, [x, y], rank, world)
-            except Exception as exc:  # cudaIpc* refused (allocator, no P2P, ...)
-                err = f"{type(exc).__name__}: {exc}"
-            if agree(ring is not None):
-                rr = slab.DistSlab(slab.CudaStepper(p), n, rank, world, ring=ring)
-                rr.exchange(x)
-                got = halo_planes(x).clone()
-                if world > 1 and not args.share_gpu:
-                    plain = slab.DistSlab(slab.CudaStepper(p), n, rank, world)
-                    for r in plain.exchange(x):
-                        r.wait()
-                    torch.cuda.synchronize()
-                if agree(torch.equal(got, halo_planes(x))):
-                    return rr, "peer"
-                why = "pre-flight mismatch against send/recv"
-                ring.close()
-            else:
-                why = err or "a peer rank could not map the ring"
-                if ring is not None:
-                    ring.close()
-        rr = slab.DistSlab(slab.CudaStepper(p), n, rank, world)
-        for r in rr.exchange(x):
-            r.wait()
-        return rr, "nccl" if why is None else f"nccl (peer ring unavailable: {why})"
+        return slab.open_runner(p, x, y, rank, world, transport=args.transport)
 
     if slab_mode:
         runner, transport = make_runner(plan, a, b)
@@ -350,14 +309,10 @@ def main():
     if runner is not None:
         runner.finish()
     barrier()
-    if runner is not None and runner.ring is not None and world > 1 and not args.share_gpu:
+    if runner is not None and runner.ring is not None:
         # the fused exchange against the plain one, on live data: the halos the
         # kernels stored into this rank must be the planes send/recv delivers
-        got = halo_planes(a).clone()
-        for r in slab.DistSlab(slab.CudaStepper(plan), n, rank, world).exchange(a):
-            r.wait()
-        torch.cuda.synchronize()
-        if not agree(torch.equal(got, halo_planes(a))):
+        if not slab.halos_match_send_recv(plan, a, rank, world):
             raise SystemExit("bench: fused peer-store halos differ from the send/recv exchange")
     launches0 = _cabi.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -89,7 +89,12 @@ class RunConfig:
     checkpoint_every: int = 0
     out_dir: str = "out"
     device: int | None = None
-    inplace: bool = False  # one device block instead of two (AA pattern; walls only)
+    inplace: bool = False  # one device block instead of two (AA pattern)
+    # z-slab decomposition over torch.distributed (one rank per GPU): None =
+    # automatically when a process group with more than one rank is initialised
+    distributed: bool | None = None
+    gather: bool = True          # distributed runs: every rank ends with the whole host state
+    transport: str = "peer"      # distributed runs: "peer" (fused peer stores) or "nccl"
 
     def __post_init__(self):
         if self.steps < 1:
@@ -353,6 +358,7 @@ class RunStats:
     mlups: float
     probe_series: np.ndarray | None = None
     probe_samples: np.ndarray | None = None
+    transport: str | None = None  # distributed runs: how the halos travelled
 
 
 def run(state, config, on_output=None, on_checkpoint=None, probe=None):
@@ -365,6 +371,8 @@ def run(state, config, on_output=None, on_checkpoint=None, probe=None):
     device; `RunStats.probe_series` is the y-velocity series as in the
     reference, `probe_samples` the full (steps, 4) rho/u record.
     """
+    if _wants_slabs(config):
+        return _run_slabs(state, config, on_output, on_checkpoint, probe)
     own = state.session is None
     sess = open_session(state, config)
     if not own:
@@ -417,6 +425,148 @@ def run(state, config, on_output=None, on_checkpoint=None, probe=None):
                     nz=state.nz, mlups=mlups,
                     probe_series=(rec[:, 2].copy() if rec is not None else None),
                     probe_samples=rec)
+
+
+def _wants_slabs(config):
+    if config.distributed is False:
+        return False
+    import torch.distributed as dist
+    on = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+    if config.distributed and not on:
+        raise ValueError("RunConfig(distributed=True) needs an initialised torch.distributed "
+                         "process group with more than one rank (launch with torchrun)")
+    return on
+
+
+def _run_slabs(state, config, on_output, on_checkpoint, probe):
+    """`run` under torch.distributed: the SAME call, one rank per GPU.
+
+    Every rank holds the (global) host state, as the reference's driver
+    does; rank r uploads and advances only its z-slab [z0, z1) - 1-D slabs,
+    5-population halos, the exchange fused into the boundary-plane kernel
+    over peer memory (slab.PeerRing) or send/recv - and the loop body,
+    hook cadence, finite check and timing are those of the single-GPU run.
+    Before a hook fires, and at the end, each rank downloads its slab into
+    its part of the host arrays; with `config.gather` the slabs are then
+    broadcast so that every rank sees the whole state (switch it off for
+    domains whose host copy is only ever looked at slab-wise).
+    RunStats.seconds is the device time of the loop, max over ranks.
+    """
+    import torch.distributed as dist
+    from . import slab
+    if config.inplace:
+        raise ValueError("the in-place update runs on one GPU; distributed runs use two blocks")
+    if state.session is not None:
+        state.session.close()
+    if state.params is None:
+        raise ValueError("state has no relaxation parameters attached")
+    if state.params.has_source:
+        raise ValueError("the fused kernel runs the zero-source path only")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    nx, ny, nz = state.nx, state.ny, state.nz
+    z0, z1 = slab.partition(nz, world)[rank]
+    n = z1 - z0
+    flags = state.mask.reshape(nz, ny, nx)
+    lo, hi = slab.slab_halo_flags(flags, nx, ny, z0, z1)
+    tile = config.schedule.resolve(nx, ny, n, state.layout)
+    plan = KernelPlan(nx, ny, n, state.layout, state.precision, flags[z0:z1], state.params.omega,
+                      state.wall_u, tile, inlet_u=state.inlet_u, device=config.device,
+                      halo_lo=lo, halo_hi=hi, slab=True)
+    dev = plan.device
+    dense = state.f_pre.data.reshape(Q, nz, ny, nx)
+    mine = pinned_empty((Q, n * ny * nx), state.precision.storage)   # this rank's slab, contiguous
+    np.copyto(mine.reshape(Q, n, ny, nx), dense[:, z0:z1])
+    a, b = plan.alloc(), plan.alloc()
+    plan.upload(mine, a)
+    b.tensor.copy_(a.tensor)
+    try:
+        plan.set_passthrough(True)      # both blocks identical (engine.py:148)
+    except ValueError:
+        plan.set_passthrough(False)
+    runner, transport = slab.open_runner(plan, a, b, rank, world, transport=config.transport)
+    pre, post = a, b
+
+    def sync_host():
+        """This rank's slab into the host arrays; all slabs with config.gather."""
+        plan.download(pre, mine)
+        np.copyto(dense[:, z0:z1], mine.reshape(Q, n, ny, nx))
+        if state.f_post_ is not None:
+            np.copyto(state.f_post_.data, state.f_pre.data)
+        if not config.gather:
+            return
+        parts = slab.partition(nz, world)
+        biggest = max(e - s for s, e in parts)
+        tdt = pre.tensor.dtype
+        scratch = torch.empty((Q, biggest, ny, nx), dtype=tdt, device=dev)
+        own = pre.tensor[:, 1:-1, :, :nx].contiguous()
+        for r, (s0, s1) in enumerate(parts):
+            buf = own if r == rank else scratch[:, :s1 - s0].contiguous()
+            dist.broadcast(buf, src=r)
+            if r != rank:
+                np.copyto(dense[:, s0:s1], buf.cpu().numpy())
+        if state.f_post_ is not None:
+            np.copyto(state.f_post_.data, state.f_pre.data)
+
+    owner = probe is not None and z0 <= probe[2] < z1
+    samples = (torch.zeros((config.steps, 4), dtype=torch.float64, device=dev)
+               if probe is not None else None)
+    end_t = state.t + config.steps
+    events, done = [], 0
+    try:
+        while done < config.steps:
+            chunk = config.steps - done
+            if probe is not None:
+                chunk = 1
+            for every in (config.output_every, config.checkpoint_every):
+                if every:
+                    chunk = min(chunk, every - state.t % every)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.current_stream(dev))
+            pre, post = runner.run(pre, post, chunk)
+            e1.record(torch.cuda.current_stream(dev))
+            events.append((e0, e1))
+            state.t += chunk
+            done += chunk
+            if owner:
+                plan.probe(pre, probe[0], probe[1], probe[2] - z0, samples[done - 1])
+            hook_out = config.output_every and state.t % config.output_every == 0
+            hook_ckp = (config.checkpoint_every and state.t < end_t
+                        and state.t % config.checkpoint_every == 0)
+            if hook_out or hook_ckp:
+                runner.finish()
+            if hook_out:
+                total = slab.combine_diagnostics(plan.diagnostics(pre), rank, world)
+                if total["nonfinite"] != 0:
+                    raise DivergenceError(f"divergence at step {state.t}")
+                if on_output is not None:
+                    sync_host()
+                    on_output(state)
+            if hook_ckp and on_checkpoint is not None:
+                sync_host()
+                on_checkpoint(state)
+        runner.finish()
+        sync_host()
+        torch.cuda.synchronize(dev)
+        ms = torch.tensor([sum(x.elapsed_time(y) for x, y in events)], dtype=torch.float64,
+                          device=dev)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        rec = None
+        if samples is not None:
+            # the rank that owns the probe cell holds the series; everyone gets it
+            src = next(r for r, (s, e) in enumerate(slab.partition(nz, world)) if s <= probe[2] < e)
+            dist.broadcast(samples, src=src)
+            rec = samples.cpu().numpy()
+    finally:
+        if runner.ring is not None:
+            runner.ring.close()
+        plan.close()
+    seconds = float(ms.item()) * 1e-3
+    updates = nx * ny * nz * config.steps
+    mlups = updates / (seconds * 1e6) if seconds > 0.0 else float("inf")
+    return RunStats(steps=config.steps, seconds=seconds, nx=nx, ny=ny, nz=nz, mlups=mlups,
+                    probe_series=(rec[:, 2].copy() if rec is not None else None),
+                    probe_samples=rec, transport=transport)
 
 
 def checkpoint(state, path):

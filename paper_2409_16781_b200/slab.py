@@ -384,6 +384,74 @@ def exchange_flag_halos(flags_slab, rank, world, group=None, device=None):
     return lo.cpu().numpy(), hi.cpu().numpy()
 
 
+def _agree(ok, world, group, device):
+    """Every rank takes the same branch: True only if all ranks say so."""
+    if world == 1:
+        return bool(ok)
+    import torch.distributed as dist
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    return bool(flag.item())
+
+
+def halo_planes(block, nz):
+    """The ten halo planes the exchange fills, stacked (for comparisons)."""
+    t = block.tensor
+    return torch.stack([t[q, 0] for q in UP] + [t[q, nz + 1] for q in DOWN])
+
+
+def halos_match_send_recv(plan, block, rank, world, group=None):
+    """Cross-check of the fused exchange on live data: are the halo planes
+    `block` holds exactly the planes a send/recv exchange delivers?  Runs
+    that exchange (which rewrites the same planes with the same data when
+    the answer is yes).  Collective; needs a backend that moves CUDA tensors
+    point to point (NCCL) - returns True untested otherwise."""
+    if world == 1:
+        return True
+    import torch.distributed as dist
+    if dist.get_backend(group) != "nccl":
+        return True
+    got = halo_planes(block, plan.nz).clone()
+    for r in DistSlab(CudaStepper(plan), plan.nz, rank, world, group).exchange(block):
+        r.wait()
+    torch.cuda.synchronize(plan.device)
+    return _agree(torch.equal(got, halo_planes(block, plan.nz)), world, group, plan.device)
+
+
+def open_runner(plan, a, b, rank=0, world=1, group=None, transport="peer", overlap=True):
+    """A DistSlab for this rank's slab with its halos filled, and the name
+    of the transport it uses.
+
+    transport "peer": the fused peer-store exchange (PeerRing) when every
+    rank can map its neighbours and the ring delivers exactly the planes
+    send/recv delivers; otherwise - and with transport "nccl" - the
+    send/recv exchange, the returned name saying why.  Collective."""
+    dev = plan.device
+    why = None
+    if transport == "peer":
+        ring, err = None, None
+        try:
+            ring = PeerRing(plan, [a, b], rank, world, group)
+        except Exception as exc:  # cudaIpc* refused (allocator, no P2P, ...)
+            err = f"{type(exc).__name__}: {exc}"
+        if _agree(ring is not None, world, group, dev):
+            runner = DistSlab(CudaStepper(plan), plan.nz, rank, world, group,
+                              overlap=overlap, ring=ring)
+            runner.exchange(a)
+            if halos_match_send_recv(plan, a, rank, world, group):
+                return runner, "peer"
+            why = "pre-flight mismatch against send/recv"
+            ring.close()
+        else:
+            why = err or "a peer rank could not map the ring"
+            if ring is not None:
+                ring.close()
+    runner = DistSlab(CudaStepper(plan), plan.nz, rank, world, group, overlap=overlap)
+    for r in runner.exchange(a):
+        r.wait()
+    return runner, "nccl" if why is None else f"nccl (peer ring unavailable: {why})"
+
+
 DIAG_KEYS = ("mass", "px", "py", "pz", "kinetic_energy", "max_u", "nonfinite", "fluid_cells")
 
 
@@ -409,5 +477,6 @@ def combine_diagnostics(local, rank=0, world=1, group=None):
     return out
 
 
-__all__ = ["combine_diagnostics", "DIAG_KEYS", "partition", "ring_neighbours", "slab_halo_flags", "CudaStepper",
+__all__ = ["combine_diagnostics", "DIAG_KEYS", "open_runner", "halos_match_send_recv",
+           "halo_planes", "partition", "ring_neighbours", "slab_halo_flags", "CudaStepper",
            "PeerRing", "DistSlab", "exchange_flag_halos", "Q"]

@@ -144,3 +144,52 @@ def test_send_recv_transport_over_nccl(geom, tmp_path):
     mp.spawn(_nccl_worker, args=(_free_port(), geom, steps, omega, str(tmp_path)),
              nprocs=1, join=True)
     np.testing.assert_array_equal(np.load(tmp_path / "nccl.npy"), want)
+
+
+def _engine_worker(rank, world, port, case, tag, out_dir):
+    signal.alarm(240)
+    import torch
+    import torch.distributed as dist
+    from paper_2409_16781_b200 import cases, engine
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        prec = {"f64": Precision.DOUBLE, "f32": Precision.SINGLE}[tag]
+        spec = (cases.CaseSpec("ldc", 24, 20, 17, re=100.0, u0=0.1) if case == "ldc"
+                else cases.CaseSpec("vks", 48, 32, 11, re=100.0, u0=0.08))
+        probe = (12, 10, 9) if case == "ldc" else (30, 16, 2)
+        # the same driver code twice: once alone on this GPU, once as one of `world` slabs
+        alone = cases.init(spec, prec)
+        seen_alone = []
+        ra = engine.run(alone, engine.RunConfig(steps=23, precision=prec, output_every=10,
+                                                distributed=False),
+                        on_output=lambda st: seen_alone.append((st.t, st.f_pre.data.copy())),
+                        probe=probe)
+        state = cases.init(spec, prec)
+        seen = []
+        rs = engine.run(state, engine.RunConfig(steps=23, precision=prec, output_every=10),
+                        on_output=lambda st: seen.append((st.t, st.f_pre.data.copy())),
+                        probe=probe)
+        assert rs.transport == "peer", rs.transport
+        assert state.t == alone.t == 23
+        np.testing.assert_array_equal(state.f_pre.data, alone.f_pre.data)   # gathered: whole state
+        assert [t for t, _ in seen] == [t for t, _ in seen_alone] == [10, 20]
+        for (_, x), (_, y) in zip(seen, seen_alone):
+            np.testing.assert_array_equal(x, y)
+        np.testing.assert_array_equal(rs.probe_samples, ra.probe_samples)
+        open(os.path.join(out_dir, f"ok{rank}"), "w").write("ok")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,tag,world", [("ldc", "f64", 2), ("ldc", "f32", 3), ("vks", "f32", 2)])
+def test_engine_run_is_the_same_call_under_torch_distributed(case, tag, world, tmp_path):
+    """The reference's driver call, unchanged, with one rank per slab: with a
+    process group initialised, engine.run splits the domain into z-slabs, runs
+    the fused peer-store exchange, fires the hooks at the same cadence with the
+    whole host state gathered, and ends bit-identical to the single-GPU run."""
+    import torch.multiprocessing as mp
+    mp.spawn(_engine_worker, args=(world, _free_port(), case, tag, str(tmp_path)),
+             nprocs=world, join=True)
+    assert all((tmp_path / f"ok{r}").exists() for r in range(world))
