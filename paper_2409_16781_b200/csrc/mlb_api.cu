@@ -1079,6 +1079,21 @@ int mlb_macro(const mlb_plan *p, const void *d_f, double *d_rho, double *d_ux, d
     if (int rc = check_plan(p, false)) return rc;
     if (!d_f || !d_rho || !d_ux || !d_uy || !d_uz) return fail(MLB_EINVAL, "NULL buffer");
     MLB_CUDA(cudaSetDevice(p->device));
+    const int V = p->dtype == MLB_F64 ? 2 : 4;   // cells per pack (16 / 16 / 8 bytes)
+    if (p->nx % V == 0) {
+        const dim3 grid((p->nx / V + 127) / 128, p->ny, p->nz);
+        if (p->dtype == MLB_F32)
+            mlb::macro_vec_kernel<float, 4><<<grid, 128, 0, S(stream)>>>(
+                static_cast<const float *>(d_f), p->g, d_rho, d_ux, d_uy, d_uz);
+        else if (p->dtype == MLB_F64)
+            mlb::macro_vec_kernel<double, 2><<<grid, 128, 0, S(stream)>>>(
+                static_cast<const double *>(d_f), p->g, d_rho, d_ux, d_uy, d_uz);
+        else
+            mlb::macro_vec_kernel<__half, 4><<<grid, 128, 0, S(stream)>>>(
+                static_cast<const __half *>(d_f), p->g, d_rho, d_ux, d_uy, d_uz);
+        MLB_LAUNCHED();
+        return MLB_OK;
+    }
     const dim3 grid((p->nx + 127) / 128, p->ny, p->nz);
     if (p->dtype == MLB_F32)
         mlb::macro_kernel<float><<<grid, 128, 0, S(stream)>>>(
@@ -1098,15 +1113,22 @@ int mlb_diagnostics(mlb_plan *p, const void *d_f, double h_out[8], void *stream)
     if (int rc = check_plan(p, true)) return rc;
     if (!d_f || !h_out) return fail(MLB_EINVAL, "NULL buffer");
     MLB_CUDA(cudaSetDevice(p->device));
-    if (p->dtype == MLB_F32)
-        mlb::diag_kernel<float><<<p->diag_blocks, mlb::DIAG_THREADS, 0, S(stream)>>>(
-            static_cast<const float *>(d_f), cls_tab(p), p->g, p->d_partials);
-    else if (p->dtype == MLB_F64)
-        mlb::diag_kernel<double><<<p->diag_blocks, mlb::DIAG_THREADS, 0, S(stream)>>>(
-            static_cast<const double *>(d_f), cls_tab(p), p->g, p->d_partials);
-    else
-        mlb::diag_kernel<__half><<<p->diag_blocks, mlb::DIAG_THREADS, 0, S(stream)>>>(
-            static_cast<const __half *>(d_f), cls_tab(p), p->g, p->d_partials);
+    const bool packs = p->nx % (p->dtype == MLB_F64 ? 2 : 4) == 0;
+    const mlb::ClsTab ct = cls_tab(p);
+    const int nb = p->diag_blocks, nt = mlb::DIAG_THREADS;
+    if (p->dtype == MLB_F32) {
+        const float *f = static_cast<const float *>(d_f);
+        if (packs) mlb::diag_vec_kernel<float, 4><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
+        else mlb::diag_kernel<float><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
+    } else if (p->dtype == MLB_F64) {
+        const double *f = static_cast<const double *>(d_f);
+        if (packs) mlb::diag_vec_kernel<double, 2><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
+        else mlb::diag_kernel<double><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
+    } else {
+        const __half *f = static_cast<const __half *>(d_f);
+        if (packs) mlb::diag_vec_kernel<__half, 4><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
+        else mlb::diag_kernel<__half><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
+    }
     MLB_LAUNCHED();
     mlb::diag_final_kernel<<<1, mlb::DIAG_THREADS, 0, S(stream)>>>(p->d_partials,
                                                                   p->diag_blocks, p->d_diag);

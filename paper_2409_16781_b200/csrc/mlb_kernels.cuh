@@ -1386,6 +1386,76 @@ __global__ void probe_kernel(const T *__restrict__ f, const Geom gm, int x, int 
     out4[3] = (r != 0.0) ? mz / r : 0.0;
 }
 
+// Pack forms of the two diagnostics kernels: V consecutive cells per thread,
+// all 19 pack loads issued together (16-byte words in fp32 / fp64, 8 bytes
+// with fp16 storage), moments accumulated in float64 in the SAME left-to-right
+// order as cell_moments - the terms of rho, m_x, m_y, m_z all appear in
+// increasing population order - so every value is bit-identical to the
+// one-cell-per-thread kernels (and the oracle).
+template <typename TS, int V>
+__device__ __forceinline__ void pack_moments(const TS *__restrict__ f, long long d, long long pop,
+                                             double (&r)[V], double (&mx)[V], double (&my)[V],
+                                             double (&mz)[V], int *bad)
+{
+    using T = typename Store<TS>::C;
+    T w[Q][V];
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+        PackIO<TS, V>::load(f + (long long)i * pop + d, w[i]);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        double v[Q];
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            v[i] = (double)w[i][j];
+            if (bad && !isfinite(w[i][j]))
+                ++*bad;
+        }
+        double t = v[0];
+#pragma unroll
+        for (int i = 1; i < Q; ++i)
+            t = t + v[i];
+        r[j] = t;
+        mx[j] = v[1] - v[3] + v[5] - v[6] - v[7] + v[8] + v[11] - v[12] - v[13] + v[14];
+        my[j] = v[2] - v[4] + v[5] + v[6] - v[7] - v[8] + v[15] - v[16] - v[17] + v[18];
+        mz[j] = v[9] - v[10] + v[11] + v[12] - v[13] - v[14] + v[15] + v[16] - v[17] - v[18];
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void store_doubles(double *p, const double (&v)[V])
+{
+#pragma unroll
+    for (int j = 0; j < V; j += 2)
+        *reinterpret_cast<double2 *>(p + j) = make_double2(v[j], v[j + 1]);
+}
+
+template <typename TS, int V>
+__global__ void __launch_bounds__(128)
+macro_vec_kernel(const TS *__restrict__ f, const Geom gm, double *__restrict__ rho,
+                 double *__restrict__ ux, double *__restrict__ uy, double *__restrict__ uz)
+{
+    const int x0 = (blockIdx.x * 128 + threadIdx.x) * V;
+    if (x0 >= gm.nx)
+        return;
+    const int y = blockIdx.y, lz = blockIdx.z;
+    const long long d = (long long)(lz + 1) * gm.plane + (long long)y * gm.xp + x0;
+    const long long o = ((long long)lz * gm.ny + y) * gm.nx + x0;
+    double r[V], mx[V], my[V], mz[V];
+    pack_moments<TS, V>(f, d, gm.pop, r, mx, my, mz, nullptr);
+    double a[V], b[V], c[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        a[j] = (r[j] != 0.0) ? mx[j] / r[j] : 0.0;
+        b[j] = (r[j] != 0.0) ? my[j] / r[j] : 0.0;
+        c[j] = (r[j] != 0.0) ? mz[j] / r[j] : 0.0;
+    }
+    store_doubles<V>(rho + o, r);
+    store_doubles<V>(ux + o, a);
+    store_doubles<V>(uy + o, b);
+    store_doubles<V>(uz + o, c);
+}
+
 // ---------------------------------------------------------------------------
 // Scalar diagnostics: per-thread accumulation over a fixed row assignment,
 // warp-shuffle tree, fixed-order cross-warp sum, per-block partials, then a
@@ -1459,7 +1529,56 @@ diag_kernel(const T *__restrict__ f, const ClsTab ct, const Geom gm,
                 if (rr != 0.0) {
                     const double u2 = (mx * mx + my * my + mz * mz) / (rr * rr);
                     acc[4] += 0.5 * rr * u2;
-                    acc[5] = fmax(acc[5], sqrt(u2));
+                    acc[5] = fmax(acc[5], u2);  // max |u|^2; the root is taken once, at the end
+                }
+            }
+        }
+    }
+    diag_block_reduce(acc, partials + (long long)blockIdx.x * DIAG_N);
+}
+
+// pack form: a fixed assignment of packs to threads, cells of a pack in order
+template <typename TS, int V>
+__global__ void __launch_bounds__(DIAG_THREADS)
+diag_vec_kernel(const TS *__restrict__ f, const ClsTab ct, const Geom gm,
+                double *__restrict__ partials)
+{
+    double acc[DIAG_N];
+#pragma unroll
+    for (int i = 0; i < DIAG_N; ++i)
+        acc[i] = 0.0;
+    // a block works on `rpi` rows per iteration: thread t owns pack t % ppr of
+    // sub-row t / ppr (short rows), or packs t, t + 256, ... of one row (long rows)
+    const int ppr = gm.nx / V;  // packs per row
+    const int rpi = ppr >= DIAG_THREADS ? 1 : DIAG_THREADS / ppr;
+    const int sub = ppr >= DIAG_THREADS ? 0 : (int)threadIdx.x / ppr;
+    const int pk0 = ppr >= DIAG_THREADS ? (int)threadIdx.x : (int)threadIdx.x - sub * ppr;
+    const long long rows = (long long)gm.nz * gm.ny;
+    for (long long row = (long long)blockIdx.x * rpi + sub; sub < rpi && row < rows;
+         row += (long long)gridDim.x * rpi) {
+        const int lz = (int)(row / gm.ny), y = (int)(row - (long long)lz * gm.ny);
+        for (int x0 = pk0 * V; x0 < gm.nx; x0 += DIAG_THREADS * V) {
+            const long long d = (long long)(lz + 1) * gm.plane + (long long)y * gm.xp + x0;
+            const uint32_t kpack = KindIO<V>::load(ct.kind + d);
+            double rr[V], mx[V], my[V], mz[V];
+            int bad = 0;
+            pack_moments<TS, V>(f, d, gm.pop, rr, mx, my, mz, &bad);
+            acc[6] += (double)bad;
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                acc[0] += rr[j];
+                const uint32_t kd = (kpack >> (8 * j)) & 0xffu;
+                if (kd == 0 || (cls_of(ct, kd, (int)d + j) & CLS_FLAG) == 0) {
+                    acc[7] += 1.0;
+                    acc[1] += mx[j];
+                    acc[2] += my[j];
+                    acc[3] += mz[j];
+                    if (rr[j] != 0.0) {
+                        const double u2 = (mx[j] * mx[j] + my[j] * my[j] + mz[j] * mz[j])
+                                          / (rr[j] * rr[j]);
+                        acc[4] += 0.5 * rr[j] * u2;
+                        acc[5] = fmax(acc[5], u2);
+                    }
                 }
             }
         }
@@ -1483,6 +1602,10 @@ diag_final_kernel(const double *__restrict__ partials, int nblocks,
         diag_combine(acc, p);
     }
     diag_block_reduce(acc, out);
+    // the kernels track max |u|^2: sqrt is monotone and correctly rounded, so the
+    // root of the maximum is the maximum of the roots
+    if (threadIdx.x == 0)
+        out[5] = sqrt(out[5]);
 }
 
 }  // namespace mlb
