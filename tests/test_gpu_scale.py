@@ -213,3 +213,57 @@ def test_channel_1024x512x512_fp32_flag_mask_path():
         pre, post = post, pre
     assert torch.equal(slabs[0][1][pre].tensor[:, 1:-1], ref[:, :256])
     assert torch.equal(slabs[1][1][pre].tensor[:, 1:-1], ref[:, 256:])
+
+
+def test_ldc1024_maximum_sizes_in_place_and_two_buffer():
+    """configs[3]'s 1024^3 cavity on ONE B200.  (a) 1024 x 1024 x 512 fp32: the
+    in-place run (one 41 GB block) against the two-buffer run (two blocks),
+    bit for bit after an odd and an even number of steps; (b) 1024^3 fp32 in
+    place (82 GB - two blocks would not fit): mass conserved in the closed box
+    to rounding, fields finite, walls untouched, lid drags the fluid."""
+    import torch
+    from paper_2409_16781_b200.kernels import KernelPlan
+    from paper_2409_16781_b200.lattice import omega_from_reynolds
+    eq = L.equilibrium(1.0, 0.0, 0.0, 0.0).astype(np.float32)
+
+    def fill(blk):
+        for q in range(19):
+            blk.tensor[q].fill_(float(eq[q]))
+
+    # (a)
+    nx, ny, nz = 1024, 1024, 512
+    omega = omega_from_reynolds(1000.0, 0.1, nx).omega
+    plan = KernelPlan(nx, ny, nz, Layout.ROW, Precision.SINGLE,
+                      B.flatten_mask(B.cavity_mask(nx, ny, nz)), omega, (0.1, 0.0, 0.0))
+    a, b, c = plan.alloc(), plan.alloc(), plan.alloc()
+    fill(a); fill(c)
+    b.tensor.copy_(a.tensor)
+    plan.set_passthrough(True)
+    for steps in (5, 6):
+        a, b, _ = plan.run_steps(a, b, steps)
+        plan.run_steps_inplace(c, steps)
+        plan.normalize(c)
+        assert torch.equal(a.tensor[:, 1:-1], c.tensor[:, 1:-1]), steps
+    plan.close()
+    del a, b, c
+    torch.cuda.empty_cache()
+
+    # (b)
+    n = 1024
+    plan = KernelPlan(n, n, n, Layout.ROW, Precision.SINGLE,
+                      B.flatten_mask(B.cavity_mask(n, n, n)), omega, (0.1, 0.0, 0.0))
+    assert plan.field_bytes > 80e9
+    f = plan.alloc()
+    fill(f)
+    d0 = plan.diagnostics(f)
+    wall = f.tensor[:, 1, :, :].clone()            # the z = 0 wall plane
+    plan.run_steps_inplace(f, 11)
+    plan.normalize(f)
+    d1 = plan.diagnostics(f)
+    assert d1["nonfinite"] == 0 and d1["fluid_cells"] == (n - 2) ** 3
+    assert abs(d1["mass"] - d0["mass"]) <= 1e-6 * d0["mass"]     # fp32 storage, 11 steps
+    assert 0.0 < d1["max_u"] < 0.1 and d1["px"] > 0.0            # the lid drags the fluid along +x
+    assert torch.equal(f.tensor[:, 1, :, :], wall)
+    plan.close()
+    del f
+    torch.cuda.empty_cache()
