@@ -866,11 +866,13 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
 // pack is not all-bulk, or the neighbour is in another warp row, each lane
 // falls back to per-cell stores for its own cells, with the scalar kernel's
 // rules.  Every location still has exactly one writer.
-#ifndef MLB_AA_MINB
-#define MLB_AA_MINB 3
-#endif
+// resident blocks per SM the register allocation aims at (measured: fp64 is
+// better off with 168 registers and no spills, fp32 / fp16 storage with 128)
+template <typename TS> struct AaMinBlocks { static constexpr int value = 4; };
+template <> struct AaMinBlocks<double> { static constexpr int value = 3; };
 template <typename TS, int V, int LX>
-__global__ void __launch_bounds__(128, MLB_AA_MINB) aa_pull_vec_kernel(const AAArgs<TS> a)
+__global__ void __launch_bounds__(128, AaMinBlocks<TS>::value)
+aa_pull_vec_kernel(const AAArgs<TS> a)
 {
     using T = typename Store<TS>::C;
     constexpr int RPW = 32 / LX;
@@ -985,6 +987,18 @@ __global__ void __launch_bounds__(128, MLB_AA_MINB) aa_pull_vec_kernel(const AAA
     }
 
     // ---- stores ---------------------------------------------------------------
+    // The stores go to the very addresses the loads came from; left alone the
+    // compiler keeps all 29 64-bit addresses alive across the collide (58
+    // registers, which cost a resident block).  Laundering the 32-bit offsets
+    // through an empty asm makes it rebuild them - one IMAD.WIDE each.
+    int x0s = x0, xls = xl, xrs = xr, ds = d, zcs = zc, zms = zm, zqs = zq, rcs = rc, rms = rm,
+        rqs = rq;
+    asm volatile("" : "+r"(x0s), "+r"(xls), "+r"(xrs), "+r"(ds), "+r"(zcs), "+r"(zms), "+r"(zqs),
+                      "+r"(rcs), "+r"(rms), "+r"(rqs));
+    {
+    const int x0 = x0s, xl = xls, xr = xrs, d = ds, zc = zcs, zm = zms, zq = zqs, rc = rcs,
+              rm = rms, rq = rqs;
+    (void)zc; (void)rc;
     // Bulk packs (no link bounces, every target location has this one writer):
     // aligned packs wherever the neighbouring lane can supply (or take) the
     // cell that crosses the pack boundary.  Directions are handled in three
@@ -1000,17 +1014,17 @@ __global__ void __launch_bounds__(128, MLB_AA_MINB) aa_pull_vec_kernel(const AAA
             n = 0;
 #define MLB_X(i, CX, Z, R)                                                            \
             if (CX > 0) { /* locations x0 .. x0+V-1 take cells x0+1 .. x0+V */        \
-                TS *row = a.f[i] + ((Z) + (R));                                       \
+                const int row = (Z) + (R); /* 32-bit offsets onto constant-bank bases */ \
                 if (bulk_r) {                                                         \
                     T o[V];                                                           \
                     _Pragma("unroll") for (int j = 0; j < V - 1; ++j) o[j] = g[opp(i)][j + 1]; \
                     o[V - 1] = nb[n];                                                 \
-                    PackIO<TS, V>::store(row + x0, o);                                \
+                    PackIO<TS, V>::store(a.f[i] + (row + x0), o);                     \
                 } else {                                                              \
                     _Pragma("unroll") for (int j = 1; j < V; ++j)                     \
-                        row[x0 + j - 1] = Store<TS>::down(g[opp(i)][j]);              \
+                        a.f[i][row + x0 + j - 1] = Store<TS>::down(g[opp(i)][j]);     \
                 }                                                                     \
-                if (!bulk_l) row[xl] = Store<TS>::down(g[opp(i)][0]);                 \
+                if (!bulk_l) a.f[i][row + xl] = Store<TS>::down(g[opp(i)][0]);        \
                 ++n;                                                                  \
             }
             MLB_DIRS(MLB_X)
@@ -1024,24 +1038,24 @@ __global__ void __launch_bounds__(128, MLB_AA_MINB) aa_pull_vec_kernel(const AAA
             n = 0;
 #define MLB_X(i, CX, Z, R)                                                            \
             if (CX < 0) { /* locations x0 .. x0+V-1 take cells x0-1 .. x0+V-2 */      \
-                TS *row = a.f[i] + ((Z) + (R));                                       \
+                const int row = (Z) + (R);                                            \
                 if (bulk_l) {                                                         \
                     T o[V];                                                           \
                     _Pragma("unroll") for (int j = 1; j < V; ++j) o[j] = g[opp(i)][j - 1]; \
                     o[0] = nb[n];                                                     \
-                    PackIO<TS, V>::store(row + x0, o);                                \
+                    PackIO<TS, V>::store(a.f[i] + (row + x0), o);                     \
                 } else {                                                              \
                     _Pragma("unroll") for (int j = 0; j < V - 1; ++j)                 \
-                        row[x0 + j + 1] = Store<TS>::down(g[opp(i)][j]);              \
+                        a.f[i][row + x0 + j + 1] = Store<TS>::down(g[opp(i)][j]);     \
                 }                                                                     \
-                if (!bulk_r) row[xr] = Store<TS>::down(g[opp(i)][V - 1]);             \
+                if (!bulk_r) a.f[i][row + xr] = Store<TS>::down(g[opp(i)][V - 1]);    \
                 ++n;                                                                  \
             }
             MLB_DIRS(MLB_X)
 #undef MLB_X
             PackIO<TS, V>::store(a.f[0] + d, g[0]);
 #define MLB_X(i, CX, Z, R)                                                            \
-            if (CX == 0) PackIO<TS, V>::store(a.f[i] + ((Z) + (R)) + x0, g[opp(i)]);
+            if (CX == 0) PackIO<TS, V>::store(a.f[i] + ((Z) + (R) + x0), g[opp(i)]);
             MLB_DIRS(MLB_X)
 #undef MLB_X
             return;
@@ -1067,6 +1081,7 @@ __global__ void __launch_bounds__(128, MLB_AA_MINB) aa_pull_vec_kernel(const AAA
         }
     MLB_DIRS(MLB_X)
 #undef MLB_X
+    }
 }
 
 // aa_local_vec_kernel (R1 -> R0): everything a cell needs is in its own slots.
