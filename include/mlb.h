@@ -168,6 +168,25 @@ int mlb_run_steps_inplace(mlb_plan *plan, void *d_f, int nsteps, int *repr,
                           void *stream, float *ms);
 int mlb_inplace_normalize(mlb_plan *plan, void *d_f, int *repr, void *stream);
 
+/* The in-place update over z-slabs (MLB_Z_HALO plans, pack kernels, peer
+ * memory).  One half-step on slab planes [z0, z1); `repr` says which: 0 = the
+ * pull half (normal -> shifted): boundary planes read their halo planes and
+ * write the results for the crossing directions straight into the ring
+ * neighbours' boundary planes (d_below / d_above: the neighbours' blocks, with
+ * nz_below / nz_above planes; for a single slab the block itself); 1 = the
+ * local half (shifted -> normal): own cells only, and boundary planes also
+ * fill the neighbours' halo planes for the next pull half.  The caller flips
+ * its representation flag once all planes of the slab are done, and orders
+ * the boundary launches against the neighbours' with mlb_signal_* exactly as
+ * for mlb_step_push_range.  mlb_inplace_swap_slab is mlb_inplace_normalize's
+ * kernel for a slab (pairs that straddle the top face reach into the slab
+ * above); the caller refills the halo planes afterwards (mlb_halo_push). */
+int mlb_step_inplace_range(mlb_plan *plan, void *d_f, int repr, int z0, int z1,
+                           void *d_below, int nz_below, void *d_above,
+                           int nz_above, void *stream);
+int mlb_inplace_swap_slab(mlb_plan *plan, void *d_f, void *d_above,
+                          int nz_above, void *stream);
+
 /* ---- z-slab halo exchange ----------------------------------
  * Copies the 5 crossing populations of one boundary plane of d_src (a
  * population block of a slab with the same nx, ny, dtype; possibly on a

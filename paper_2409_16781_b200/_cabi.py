@@ -30,6 +30,7 @@ SYMBOLS = (
     "mlb_step_range", "mlb_step_open_range", "mlb_open_pass", "mlb_open_pass_range",
     "mlb_run_steps",
     "mlb_run_steps_inplace", "mlb_inplace_normalize",
+    "mlb_step_inplace_range", "mlb_inplace_swap_slab",
     "mlb_halo_copy", "mlb_halo_push", "mlb_step_push_range",
     "mlb_ipc_export", "mlb_ipc_open", "mlb_ipc_close",
     "mlb_signal_create", "mlb_signal_destroy", "mlb_signal_post", "mlb_signal_wait",
@@ -87,6 +88,8 @@ def lib():
         "mlb_run_steps_inplace": (i, [vp, vp, i, ctypes.POINTER(ctypes.c_int), vp,
                                       ctypes.POINTER(ctypes.c_float)]),
         "mlb_inplace_normalize": (i, [vp, vp, ctypes.POINTER(ctypes.c_int), vp]),
+        "mlb_step_inplace_range": (i, [vp, vp, i, i, i, vp, i, vp, i, vp]),
+        "mlb_inplace_swap_slab": (i, [vp, vp, vp, i, vp]),
         "mlb_halo_copy": (i, [vp, vp, vp, i, i, vp]),
         "mlb_halo_push": (i, [vp, vp, vp, i, i, vp]),
         "mlb_step_push_range": (i, [vp, vp, vp, i, i, vp, i, vp, i, vp]),

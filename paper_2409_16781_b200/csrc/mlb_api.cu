@@ -347,8 +347,16 @@ int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cuda
 }
 
 // in-place (AA pattern) launches: kind 0 = R0 -> R1 step, 1 = R1 -> R0 step, 2 = swap
+// plane range and ring neighbours of one in-place launch (z-slabs; all-zero =
+// the whole domain on one GPU)
+struct AaRange {
+    int z0 = 0, z1 = -1;                      // z1 < 0: all planes
+    void *below = nullptr, *above = nullptr;  // the neighbours' blocks (peer memory)
+    int nz_below = 0, nz_above = 0;
+};
+
 template <typename TS>
-void fill_aa(mlb_plan *p, void *f, mlb::AAArgs<TS> &a)
+void fill_aa(mlb_plan *p, void *f, const AaRange &r, mlb::AAArgs<TS> &a)
 {
     using T = typename mlb::Store<TS>::C;
     for (int q = 0; q < MLB_Q; ++q)
@@ -361,41 +369,74 @@ void fill_aa(mlb_plan *p, void *f, mlb::AAArgs<TS> &a)
     inlet_values<T>(p->inlet_u, cv);  // compute dtype, then storage dtype (engine.py:167-171)
     for (int q = 0; q < MLB_Q; ++q)
         a.inlet[q] = mlb::Store<TS>::down(cv[q]);
+    a.z0 = r.z0;
+    const long long plane = p->lay.plane;
+    for (int j = 0; j < 5; ++j) {
+        // slab below: its top plane lz = nz_below-1 (storage nz_below), c_z = +1 populations
+        a.lo[j] = r.below ? static_cast<TS *>(r.below)
+                                + ((long long)mlb::halo_up(j) * (r.nz_below + 2) + r.nz_below) * plane
+                          : nullptr;
+        // slab above: its bottom plane lz = 0 (storage 1), c_z = -1 populations
+        a.hi[j] = r.above ? static_cast<TS *>(r.above)
+                                + ((long long)mlb::halo_down(j) * (r.nz_above + 2) + 1) * plane
+                          : nullptr;
+    }
 }
 
 template <typename TS>
-int launch_aa(mlb_plan *p, void *f, int kind, cudaStream_t st)
+int launch_aa(mlb_plan *p, void *f, int kind, const AaRange &r, cudaStream_t st)
 {
     mlb::AAArgs<TS> a;
-    fill_aa<TS>(p, f, a);
+    fill_aa<TS>(p, f, r, a);
     constexpr int BX = 128;
-    const dim3 grid((p->nx + BX - 1) / BX, p->ny, p->nz);
+    const int n = (r.z1 < 0 ? p->nz : r.z1) - r.z0;
+    const dim3 grid((p->nx + BX - 1) / BX, p->ny, n);
+    const bool remote = r.below || r.above;
     if (kind == 0) mlb::aa_pull_kernel<TS, BX><<<grid, BX, 0, st>>>(a);
     else if (kind == 1) mlb::aa_local_kernel<TS, BX><<<grid, BX, 0, st>>>(a);
-    else mlb::aa_swap_kernel<TS, BX><<<grid, BX, 0, st>>>(a);
+    else if (remote) mlb::aa_swap_kernel<TS, BX, true><<<grid, BX, 0, st>>>(a);
+    else mlb::aa_swap_kernel<TS, BX, false><<<grid, BX, 0, st>>>(a);
     MLB_LAUNCHED();
     return MLB_OK;
 }
 
 template <typename TS, int V, int LX>
-int launch_aa_vec(mlb_plan *p, void *f, int kind, cudaStream_t st)
+int launch_aa_vec(mlb_plan *p, void *f, int kind, const AaRange &r, cudaStream_t st)
 {
     mlb::AAArgs<TS> a;
-    fill_aa<TS>(p, f, a);
+    fill_aa<TS>(p, f, r, a);
     const int rows = 128 / LX;
-    const dim3 grid((p->nx / V + LX - 1) / LX, (p->ny + rows - 1) / rows, p->nz);
-    if (kind == 0) mlb::aa_pull_vec_kernel<TS, V, LX><<<grid, 128, 0, st>>>(a);
-    else mlb::aa_local_vec_kernel<TS, V, LX><<<grid, 128, 0, st>>>(a);
+    const int n = (r.z1 < 0 ? p->nz : r.z1) - r.z0;
+    const dim3 grid((p->nx / V + LX - 1) / LX, (p->ny + rows - 1) / rows, n);
+    const bool remote = r.below || r.above;
+    if (kind == 0) {
+        // pull half: results for crossing directions go into the neighbours' planes
+        if (remote) mlb::aa_pull_vec_kernel<TS, V, LX, true><<<grid, 128, 0, st>>>(a);
+        else mlb::aa_pull_vec_kernel<TS, V, LX, false><<<grid, 128, 0, st>>>(a);
+    } else {
+        // local half: back in the normal representation; boundary planes also fill
+        // the neighbours' halo planes (the two-buffer kernel's push)
+        mlb::PushArgs<TS> ph{};
+        if (remote) {
+            PushTarget t;
+            if (r.z0 == 0) { t.below = r.below; t.nz_below = r.nz_below; }
+            if ((r.z1 < 0 ? p->nz : r.z1) == p->nz) { t.above = r.above; t.nz_above = r.nz_above; }
+            fill_push<TS>(p, t, ph);
+            mlb::aa_local_vec_kernel<TS, V, LX, true><<<grid, 128, 0, st>>>(a, ph);
+        } else {
+            mlb::aa_local_vec_kernel<TS, V, LX, false><<<grid, 128, 0, st>>>(a, ph);
+        }
+    }
     MLB_LAUNCHED();
     return MLB_OK;
 }
 
 template <typename TS, int V>
-int launch_aa_vec_lx(mlb_plan *p, void *f, int kind, int lx, cudaStream_t st)
+int launch_aa_vec_lx(mlb_plan *p, void *f, int kind, int lx, const AaRange &r, cudaStream_t st)
 {
-    if (lx == 8) return launch_aa_vec<TS, V, 8>(p, f, kind, st);
-    if (lx == 16) return launch_aa_vec<TS, V, 16>(p, f, kind, st);
-    return launch_aa_vec<TS, V, 32>(p, f, kind, st);
+    if (lx == 8) return launch_aa_vec<TS, V, 8>(p, f, kind, r, st);
+    if (lx == 16) return launch_aa_vec<TS, V, 16>(p, f, kind, r, st);
+    return launch_aa_vec<TS, V, 32>(p, f, kind, r, st);
 }
 
 // the variant the in-place kernels run with (0 = auto: packs whenever the row
@@ -435,7 +476,7 @@ bool aa_open_ok(const mlb_plan *p, int variant)
 
 // the in-place step kernels follow the plan's variant: pack kernels when the
 // two-buffer path would use one (the swap is always scalar)
-int launch_aa_any(mlb_plan *p, void *f, int kind, cudaStream_t st)
+int launch_aa_any(mlb_plan *p, void *f, int kind, cudaStream_t st, const AaRange &r = AaRange())
 {
     const int variant = resolve_aa_variant(p);
     if (!variant_exists(p->dtype, variant))
@@ -444,12 +485,14 @@ int launch_aa_any(mlb_plan *p, void *f, int kind, cudaStream_t st)
     const bool vec = kind != 2 && aa_uses_packs(p, variant);
     const int lx = variant % 1000;
     if (p->dtype == MLB_F32)
-        return vec ? launch_aa_vec_lx<float, 4>(p, f, kind, lx, st) : launch_aa<float>(p, f, kind, st);
+        return vec ? launch_aa_vec_lx<float, 4>(p, f, kind, lx, r, st)
+                   : launch_aa<float>(p, f, kind, r, st);
     if (p->dtype == MLB_F64)
-        return vec ? launch_aa_vec_lx<double, 2>(p, f, kind, lx, st) : launch_aa<double>(p, f, kind, st);
-    if (vec && variant >= 3000) return launch_aa_vec_lx<__half, 2>(p, f, kind, lx, st);
-    if (vec) return launch_aa_vec_lx<__half, 4>(p, f, kind, lx, st);
-    return launch_aa<__half>(p, f, kind, st);
+        return vec ? launch_aa_vec_lx<double, 2>(p, f, kind, lx, r, st)
+                   : launch_aa<double>(p, f, kind, r, st);
+    if (vec && variant >= 3000) return launch_aa_vec_lx<__half, 2>(p, f, kind, lx, r, st);
+    if (vec) return launch_aa_vec_lx<__half, 4>(p, f, kind, lx, r, st);
+    return launch_aa<__half>(p, f, kind, r, st);
 }
 
 template <typename T>
@@ -992,6 +1035,51 @@ int mlb_inplace_normalize(mlb_plan *p, void *d_f, int *repr, void *stream)
     if (int rc = launch_aa_any(p, d_f, 2, S(stream))) return rc;
     *repr = 0;
     return MLB_OK;
+}
+
+int mlb_step_inplace_range(mlb_plan *p, void *d_f, int repr, int z0, int z1, void *d_below,
+                           int nz_below, void *d_above, int nz_above, void *stream)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (!d_f) return fail(MLB_EINVAL, "NULL population block");
+    if (repr != 0 && repr != 1)
+        return fail(MLB_EINVAL, "representation must be 0 (normal) or 1 (shifted), got %d", repr);
+    if (z0 < 0 || z1 > p->nz || z0 > z1)
+        return fail(MLB_EINVAL, "plane range [%d, %d) outside [0, %d)", z0, z1, p->nz);
+    if (p->z_mode != MLB_Z_HALO)
+        return fail(MLB_EUNSUPPORTED, "mlb_step_inplace_range is the z-slab form (MLB_Z_HALO "
+                    "plans); a whole domain uses mlb_run_steps_inplace");
+    if (!d_below || !d_above || nz_below < 1 || nz_above < 1)
+        return fail(MLB_EINVAL, "the in-place slab step needs both ring neighbours' blocks "
+                    "(with one slab: the block itself)");
+    const int variant = resolve_aa_variant(p);
+    if (!aa_uses_packs(p, variant))
+        return fail(MLB_EUNSUPPORTED, "the in-place slab step needs a pack kernel (nx a multiple "
+                    "of the pack; variant W*1000 + LX, or auto with nx >= 128)");
+    if (!aa_open_ok(p, variant))
+        return fail(MLB_EUNSUPPORTED, "the in-place update handles walls only unless every outlet "
+                    "cell has its x-1 neighbour in the same pack; this geometry has %lld inlet "
+                    "and %lld outlet cells", p->n_in, p->n_out);
+    if (z0 == z1) return MLB_OK;
+    MLB_CUDA(cudaSetDevice(p->device));
+    AaRange r;
+    r.z0 = z0; r.z1 = z1;
+    r.below = d_below; r.nz_below = nz_below;
+    r.above = d_above; r.nz_above = nz_above;
+    return launch_aa_any(p, d_f, repr, S(stream), r);
+}
+
+int mlb_inplace_swap_slab(mlb_plan *p, void *d_f, void *d_above, int nz_above, void *stream)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (!d_f || !d_above || nz_above < 1) return fail(MLB_EINVAL, "NULL / empty block");
+    if (p->z_mode != MLB_Z_HALO)
+        return fail(MLB_EUNSUPPORTED, "mlb_inplace_swap_slab is the z-slab form; a whole domain "
+                    "uses mlb_inplace_normalize");
+    MLB_CUDA(cudaSetDevice(p->device));
+    AaRange r;
+    r.above = d_above; r.nz_above = nz_above;
+    return launch_aa_any(p, d_f, 2, S(stream), r);
 }
 
 // 5 crossing populations of one boundary plane of a slab with src_nz planes

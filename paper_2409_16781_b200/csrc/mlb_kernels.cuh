@@ -432,7 +432,37 @@ struct AAArgs {
     T omega;
     T k[Q];
     TS inlet[Q];  // equilibrium(1, u_in, 0, 0), storage dtype (open boundaries, pack kernels)
+    int z0;       // first slab plane this launch updates (blockIdx.z = 0)
+    // z-slabs (REMOTE kernels): the pull half writes each result into the location
+    // it was pulled from - and for a boundary plane's crossing directions that
+    // location belongs to the ring neighbour.  It is READ from the local halo plane
+    // (filled by the previous local half's push, as in the two-buffer path) and
+    // WRITTEN straight into the neighbour's boundary plane over peer memory:
+    // lo[j] = start of population halo_up(j)'s plane lz = nz_below-1 of the slab
+    // below (the source plane of c_z = +1 pulls of our plane 0), hi[j] = start of
+    // population halo_down(j)'s plane lz = 0 of the slab above.
+    TS *lo[5];
+    TS *hi[5];
 };
+__host__ __device__ constexpr int up_index(int i)    // inverse of halo_up
+{ return i == 9 ? 0 : i == 11 ? 1 : i == 12 ? 2 : i == 15 ? 3 : 4; }
+__host__ __device__ constexpr int down_index(int i)  // inverse of halo_down
+{ return i == 10 ? 0 : i == 13 ? 1 : i == 14 ? 2 : i == 17 ? 3 : 4; }
+// c_z of the directions whose source plane is named zc / zm / zq in the tables
+constexpr int CZ_zc = 0, CZ_zm = 1, CZ_zq = -1;
+
+// where the pull half stores its result for direction i (source plane offset Z,
+// row offset R): the location it read - or the neighbour slab's copy of it
+// (x = element offset inside the row; everything is folded into ONE 32-bit offset
+// onto a constant-bank base pointer)
+template <typename TS, int CZ, bool REMOTE>
+__device__ __forceinline__ TS *aa_target(const AAArgs<TS> &a, int i, int Z, int R, int x,
+                                         bool rlo, bool rhi)
+{
+    if (REMOTE && CZ > 0 && rlo) return a.lo[up_index(i)] + (R + x);
+    if (REMOTE && CZ < 0 && rhi) return a.hi[down_index(i)] + (R + x);
+    return a.f[i] + (Z + R + x);
+}
 
 // In place, every non-wall cell takes part in the exchange of slots: fluid cells
 // collide; an INLET cell's new state is the constant equilibrium; an OUTLET
@@ -485,7 +515,7 @@ __global__ void __launch_bounds__(BX) aa_pull_kernel(const AAArgs<TS> a)
     const int x = blockIdx.x * BX + threadIdx.x;
     if (x >= gm.nx)
         return;
-    const int y = blockIdx.y, lz = blockIdx.z;
+    const int y = blockIdx.y, lz = a.z0 + blockIdx.z;
     const int xp = (int)gm.xp, plane = (int)gm.plane;
     // same index arithmetic as step_cell
     const int dxm = (x == 0) ? gm.nx - 1 : -1;
@@ -541,7 +571,7 @@ __global__ void __launch_bounds__(BX) aa_local_kernel(const AAArgs<TS> a)
     const int x = blockIdx.x * BX + threadIdx.x;
     if (x >= a.g.nx)
         return;
-    const int d = ((int)blockIdx.z + 1) * (int)a.g.plane + (int)blockIdx.y * (int)a.g.xp + x;
+    const int d = (a.z0 + (int)blockIdx.z + 1) * (int)a.g.plane + (int)blockIdx.y * (int)a.g.xp + x;
     const uint32_t kd = a.ct.kind[d];
     T g[Q];
 #pragma unroll
@@ -572,21 +602,25 @@ __global__ void __launch_bounds__(BX) aa_local_kernel(const AAArgs<TS> a)
 // R1 <-> R0 without a step: swap each pair of locations {(q, x), (opp(q), x + c_q)}
 // whose link does not bounce; each pair is owned by the cell on the "positive"
 // side (q in {1,2,5,6,9,11,12,15,16}; x + c_q = the source cell of opp(q)).
-template <typename TS, int BX>
+template <typename TS, int BX, bool REMOTE>
 __global__ void __launch_bounds__(BX) aa_swap_kernel(const AAArgs<TS> a)
 {
     const int x = blockIdx.x * BX + threadIdx.x;
     if (x >= a.g.nx)
         return;
+    const int lz = a.z0 + blockIdx.z;
     int d, off[Q];
-    aa_offsets<TS>(a.g, x, blockIdx.y, blockIdx.z, d, off);
+    aa_offsets<TS>(a.g, x, blockIdx.y, lz, d, off);
     const uint32_t kd = a.ct.kind[d];
     const uint32_t cd = kd == 0 ? 0u : cls_of(a.ct, kd, d);
     if (!aa_participant(cd))
         return;
+    // z-slabs: the partner of a top-plane cell along a c_z = +1 direction lives in
+    // the slab above (its plane 0), not in our halo
+    const bool rhi = REMOTE && lz == a.g.nz - 1 && a.hi[0] != nullptr;
+    const int halo_hi = a.g.zhi_src * (int)a.g.plane;
 #pragma unroll
     for (int q = 1; q < Q; ++q) {
-        constexpr int dummy = 0; (void)dummy;
         const bool positive = (q == 1 || q == 2 || q == 5 || q == 6 || q == 9 || q == 11
                                || q == 12 || q == 15 || q == 16);
         if (!positive)
@@ -594,9 +628,11 @@ __global__ void __launch_bounds__(BX) aa_swap_kernel(const AAArgs<TS> a)
         const int o = opp(q);           // x + c_q is the source cell of direction o
         if (cd & cls_link(o))
             continue;                   // bouncing link: both representations agree
-        const TS u = a.f[q][d], v = a.f[o][off[o]];
+        const bool up = (q == 9 || q == 11 || q == 12 || q == 15 || q == 16);  // c_z(q) = +1
+        TS *partner = (up && rhi) ? a.hi[down_index(o)] + (off[o] - halo_hi) : a.f[o] + off[o];
+        const TS u = a.f[q][d], v = *partner;
         a.f[q][d] = v;
-        a.f[o][off[o]] = u;
+        *partner = u;
     }
 }
 
@@ -870,7 +906,7 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
 // better off with 168 registers and no spills, fp32 / fp16 storage with 128)
 template <typename TS> struct AaMinBlocks { static constexpr int value = 4; };
 template <> struct AaMinBlocks<double> { static constexpr int value = 3; };
-template <typename TS, int V, int LX>
+template <typename TS, int V, int LX, bool REMOTE>
 __global__ void __launch_bounds__(128, AaMinBlocks<TS>::value)
 aa_pull_vec_kernel(const AAArgs<TS> a)
 {
@@ -882,7 +918,10 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
     const int seg = lane % LX;
     int x0 = (blockIdx.x * LX + seg) * V;
     int y = blockIdx.y * (4 * RPW) + warp * RPW + lane / LX;
-    const int lz = blockIdx.z;
+    const int lz = a.z0 + blockIdx.z;
+    // z-slabs: crossing directions of a boundary plane store into the neighbour slab
+    const bool rlo = REMOTE && lz == 0 && a.lo[0] != nullptr;
+    const bool rhi = REMOTE && lz == gm.nz - 1 && a.hi[0] != nullptr;
     // lanes outside the grid stay in the warp for the shuffles: they compute on
     // a valid dummy pack and never store
     const bool valid = x0 < gm.nx && y < gm.ny;
@@ -987,6 +1026,7 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
     }
 
     // ---- stores ---------------------------------------------------------------
+#define MLB_T(i, Z, R, X) aa_target<TS, CZ_##Z, REMOTE>(a, i, (Z), (R), (X), rlo, rhi)
     // The stores go to the very addresses the loads came from; left alone the
     // compiler keeps all 29 64-bit addresses alive across the collide (58
     // registers, which cost a resident block).  Laundering the 32-bit offsets
@@ -1014,17 +1054,16 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
             n = 0;
 #define MLB_X(i, CX, Z, R)                                                            \
             if (CX > 0) { /* locations x0 .. x0+V-1 take cells x0+1 .. x0+V */        \
-                const int row = (Z) + (R); /* 32-bit offsets onto constant-bank bases */ \
                 if (bulk_r) {                                                         \
                     T o[V];                                                           \
                     _Pragma("unroll") for (int j = 0; j < V - 1; ++j) o[j] = g[opp(i)][j + 1]; \
                     o[V - 1] = nb[n];                                                 \
-                    PackIO<TS, V>::store(a.f[i] + (row + x0), o);                     \
+                    PackIO<TS, V>::store(MLB_T(i, Z, R, x0), o);                      \
                 } else {                                                              \
                     _Pragma("unroll") for (int j = 1; j < V; ++j)                     \
-                        a.f[i][row + x0 + j - 1] = Store<TS>::down(g[opp(i)][j]);     \
+                        *MLB_T(i, Z, R, x0 + j - 1) = Store<TS>::down(g[opp(i)][j]);  \
                 }                                                                     \
-                if (!bulk_l) a.f[i][row + xl] = Store<TS>::down(g[opp(i)][0]);        \
+                if (!bulk_l) *MLB_T(i, Z, R, xl) = Store<TS>::down(g[opp(i)][0]);     \
                 ++n;                                                                  \
             }
             MLB_DIRS(MLB_X)
@@ -1038,24 +1077,24 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
             n = 0;
 #define MLB_X(i, CX, Z, R)                                                            \
             if (CX < 0) { /* locations x0 .. x0+V-1 take cells x0-1 .. x0+V-2 */      \
-                const int row = (Z) + (R);                                            \
                 if (bulk_l) {                                                         \
                     T o[V];                                                           \
                     _Pragma("unroll") for (int j = 1; j < V; ++j) o[j] = g[opp(i)][j - 1]; \
                     o[0] = nb[n];                                                     \
-                    PackIO<TS, V>::store(a.f[i] + (row + x0), o);                     \
+                    PackIO<TS, V>::store(MLB_T(i, Z, R, x0), o);                      \
                 } else {                                                              \
                     _Pragma("unroll") for (int j = 0; j < V - 1; ++j)                 \
-                        a.f[i][row + x0 + j + 1] = Store<TS>::down(g[opp(i)][j]);     \
+                        *MLB_T(i, Z, R, x0 + j + 1) = Store<TS>::down(g[opp(i)][j]);  \
                 }                                                                     \
-                if (!bulk_r) a.f[i][row + xr] = Store<TS>::down(g[opp(i)][V - 1]);    \
+                if (!bulk_r) *MLB_T(i, Z, R, xr) = Store<TS>::down(g[opp(i)][V - 1]); \
                 ++n;                                                                  \
             }
             MLB_DIRS(MLB_X)
 #undef MLB_X
             PackIO<TS, V>::store(a.f[0] + d, g[0]);
 #define MLB_X(i, CX, Z, R)                                                            \
-            if (CX == 0) PackIO<TS, V>::store(a.f[i] + ((Z) + (R) + x0), g[opp(i)]);
+            if (CX == 0)                                                              \
+                PackIO<TS, V>::store(MLB_T(i, Z, R, x0), g[opp(i)]);
             MLB_DIRS(MLB_X)
 #undef MLB_X
             return;
@@ -1077,16 +1116,18 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
                          : (CX) > 0 ? (j == 0 ? xl : x0 + j - 1)                      \
                                     : (j == V - 1 ? xr : x0 + j + 1);                 \
             if (c[j] & cls_link(i)) a.f[opp(i)][d + j] = Store<TS>::down(g[opp(i)][j]); \
-            else a.f[i][((Z) + (R)) + xs] = Store<TS>::down(g[opp(i)][j]);            \
+            else *MLB_T(i, Z, R, xs) = Store<TS>::down(g[opp(i)][j]);                 \
         }
     MLB_DIRS(MLB_X)
 #undef MLB_X
+#undef MLB_T
     }
 }
 
 // aa_local_vec_kernel (R1 -> R0): everything a cell needs is in its own slots.
-template <typename TS, int V, int LX>
-__global__ void __launch_bounds__(128, 4) aa_local_vec_kernel(const AAArgs<TS> a)
+template <typename TS, int V, int LX, bool PUSH>
+__global__ void __launch_bounds__(128, 4) aa_local_vec_kernel(const AAArgs<TS> a,
+                                                              const PushArgs<TS> ph)
 {
     using T = typename Store<TS>::C;
     constexpr int RPW = 32 / LX;
@@ -1096,7 +1137,8 @@ __global__ void __launch_bounds__(128, 4) aa_local_vec_kernel(const AAArgs<TS> a
     const int y = blockIdx.y * (4 * RPW) + warp * RPW + lane / LX;
     if (x0 >= gm.nx || y >= gm.ny)
         return;
-    const int d = ((int)blockIdx.z + 1) * (int)gm.plane + y * (int)gm.xp + x0;
+    const int lz = a.z0 + (int)blockIdx.z;
+    const int d = (lz + 1) * (int)gm.plane + y * (int)gm.xp + x0;
 
     const uint32_t kpack = KindIO<V>::load(a.ct.kind + d);
     T g[Q][V];
@@ -1163,6 +1205,23 @@ __global__ void __launch_bounds__(128, 4) aa_local_vec_kernel(const AAArgs<TS> a
 #pragma unroll
     for (int i = 0; i < Q; ++i)
         PackIO<TS, V>::store(a.f[i] + d, g[i]);
+    if constexpr (PUSH) {
+        // z-slabs: the block is back in the normal representation; the crossing
+        // populations of a boundary plane also go into the ring neighbour's halo
+        // plane, exactly as in the two-buffer kernel (full packs: the halo of a
+        // wall cell then holds the wall's own values, which nobody reads)
+        const int o = y * (int)gm.xp + x0;
+        if (lz == 0 && ph.lo[0] != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 5; ++j)
+                PackIO<TS, V>::store(ph.lo[j] + o, g[halo_down(j)]);
+        }
+        if (lz == gm.nz - 1 && ph.hi[0] != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 5; ++j)
+                PackIO<TS, V>::store(ph.hi[j] + o, g[halo_up(j)]);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -454,8 +454,6 @@ def _run_slabs(state, config, on_output, on_checkpoint, probe):
     """
     import torch.distributed as dist
     from . import slab
-    if config.inplace:
-        raise ValueError("the in-place update runs on one GPU; distributed runs use two blocks")
     if state.session is not None:
         state.session.close()
     if state.params is None:
@@ -476,15 +474,46 @@ def _run_slabs(state, config, on_output, on_checkpoint, probe):
     dense = state.f_pre.data.reshape(Q, nz, ny, nx)
     mine = pinned_empty((Q, n * ny * nx), state.precision.storage)   # this rank's slab, contiguous
     np.copyto(mine.reshape(Q, n, ny, nx), dense[:, z0:z1])
-    a, b = plan.alloc(), plan.alloc()
+    a = plan.alloc()
     plan.upload(mine, a)
-    b.tensor.copy_(a.tensor)
-    try:
-        plan.set_passthrough(True)      # both blocks identical (engine.py:148)
-    except ValueError:
-        plan.set_passthrough(False)
-    runner, transport = slab.open_runner(plan, a, b, rank, world, transport=config.transport)
+    if config.inplace:
+        # one block per rank (AA pattern over peer memory)
+        b = None
+        runner, transport = slab.open_inplace_runner(plan, a, rank, world), "peer"
+    else:
+        b = plan.alloc()
+        b.tensor.copy_(a.tensor)
+        try:
+            plan.set_passthrough(True)      # both blocks identical (engine.py:148)
+        except ValueError:
+            plan.set_passthrough(False)
+        runner, transport = slab.open_runner(plan, a, b, rank, world, transport=config.transport)
     pre, post = a, b
+
+    fence = False
+
+    def advance(k):
+        nonlocal pre, post, fence
+        if config.inplace:
+            # In place the neighbours' next pull half writes into THIS rank's
+            # boundary planes (not into halo planes nobody else reads): whatever
+            # read the block since the last settle() - probe, diagnostics,
+            # download - must be over on every rank before anyone steps on.
+            if fence:
+                runner.fence()
+                fence = False
+            runner.run_inplace(pre, k)
+        else:
+            pre, post = runner.run(pre, post, k)
+
+    def settle():
+        """Before anything reads the block: pushes landed, normal representation."""
+        nonlocal fence
+        if config.inplace:
+            runner.normalize(pre)
+            fence = True
+        else:
+            runner.finish()
 
     def sync_host():
         """This rank's slab into the host arrays; all slabs with config.gather."""
@@ -523,18 +552,20 @@ def _run_slabs(state, config, on_output, on_checkpoint, probe):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(torch.cuda.current_stream(dev))
-            pre, post = runner.run(pre, post, chunk)
+            advance(chunk)
             e1.record(torch.cuda.current_stream(dev))
             events.append((e0, e1))
             state.t += chunk
             done += chunk
+            if probe is not None and config.inplace:
+                settle()            # collective: every rank, not only the probe's owner
             if owner:
                 plan.probe(pre, probe[0], probe[1], probe[2] - z0, samples[done - 1])
             hook_out = config.output_every and state.t % config.output_every == 0
             hook_ckp = (config.checkpoint_every and state.t < end_t
                         and state.t % config.checkpoint_every == 0)
             if hook_out or hook_ckp:
-                runner.finish()
+                settle()
             if hook_out:
                 total = slab.combine_diagnostics(plan.diagnostics(pre), rank, world)
                 if total["nonfinite"] != 0:
@@ -545,7 +576,7 @@ def _run_slabs(state, config, on_output, on_checkpoint, probe):
             if hook_ckp and on_checkpoint is not None:
                 sync_host()
                 on_checkpoint(state)
-        runner.finish()
+        settle()
         sync_host()
         torch.cuda.synchronize(dev)
         ms = torch.tensor([sum(x.elapsed_time(y) for x, y in events)], dtype=torch.float64,

@@ -334,6 +334,23 @@ class KernelPlan:
                                                     _stream_ptr(self.device)))
         f.repr = r.value
 
+    def step_inplace_range(self, f, z0, z1, below, above):
+        """One in-place half-step (pull if f.repr == 0, local if 1) on planes
+        [z0, z1) of a z-slab; `below` / `above` = (device pointer, nz) of the
+        ring neighbours' blocks.  Does not flip f.repr (the caller does, once
+        all planes are done)."""
+        _cabi.check(self._lib.mlb_step_inplace_range(
+            self._plan, f.ptr, int(f.repr), int(z0), int(z1),
+            ctypes.c_void_p(below[0]), int(below[1]), ctypes.c_void_p(above[0]), int(above[1]),
+            _stream_ptr(self.device)))
+
+    def inplace_swap_slab(self, f, above):
+        """Shifted -> normal representation of a slab without a step (the halo
+        planes must be refilled afterwards)."""
+        _cabi.check(self._lib.mlb_inplace_swap_slab(
+            self._plan, f.ptr, ctypes.c_void_p(above[0]), int(above[1]),
+            _stream_ptr(self.device)))
+
     def halo_copy(self, dst, src, face):
         """Fill one halo plane of `dst` from the matching boundary plane of
         `src` (5 crossing populations), on this device or a peer."""

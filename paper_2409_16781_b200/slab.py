@@ -341,6 +341,67 @@ class DistSlab:
         done.record(st.hi)
         main.wait_event(done)
 
+    # -- the in-place update over slabs (one block per rank, PeerRing) ----------
+    def step_inplace(self, f):
+        """One in-place step of this slab (mlb_step_inplace_range): the pull
+        half writes its results for the crossing directions into the
+        neighbours' boundary planes, the local half refills the neighbours'
+        halo planes.  Same boundary-first schedule and the same step counters
+        as the two-buffer step."""
+        st, nz, ring = self.stepper, self.nz, self.ring
+        if ring is None:
+            raise ValueError("the in-place slab step needs the peer-memory ring")
+        plan = st.plan
+        below, above = ring.targets(ring.index(f))
+        t = ring.t + 1
+        if not self.overlap:
+            ring.wait(t - 1)
+            plan.step_inplace_range(f, 0, nz, below, above)
+            ring.post(t)
+        else:
+            main = torch.cuda.current_stream(st.device)
+            ready = torch.cuda.Event()
+            ready.record(main)
+            st.hi.wait_event(ready)
+            with torch.cuda.stream(st.hi):
+                ring.wait(t - 1)
+                plan.step_inplace_range(f, 0, 1, below, above)
+                plan.step_inplace_range(f, nz - 1, nz, below, above)
+                ring.post(t)
+            plan.step_inplace_range(f, 1, nz - 1, below, above)
+            done = torch.cuda.Event()
+            done.record(st.hi)
+            main.wait_event(done)
+        f.repr ^= 1
+
+    def run_inplace(self, f, nsteps):
+        for _ in range(nsteps):
+            self.step_inplace(f)
+        return f
+
+    def normalize(self, f):
+        """Bring an in-place slab back to the normal representation (a no-op
+        after an even number of steps).  Collective.
+
+        In place the neighbours' next pull half writes into THIS rank's
+        boundary planes, so whatever reads the block afterwards (probe,
+        diagnostics, download) must be finished on every rank before anyone
+        steps on: call `fence()` between the reads and the next step."""
+        ring = self.ring
+        ring.barrier()
+        if f.repr == 1:
+            k = ring.index(f)
+            below, above = ring.targets(k)
+            self.stepper.plan.inplace_swap_slab(f, above)
+            f.repr = 0
+            ring.barrier()          # every slab normal before any halo is refilled
+            ring.exchange(k)
+        ring.barrier()
+
+    def fence(self):
+        """Device synchronisation + barrier over the ring's ranks."""
+        self.ring.barrier()
+
     def finish(self):
         """After the last step, before anyone reads halos or frees blocks:
         every rank's pushes have landed."""
@@ -452,6 +513,26 @@ def open_runner(plan, a, b, rank=0, world=1, group=None, transport="peer", overl
     return runner, "nccl" if why is None else f"nccl (peer ring unavailable: {why})"
 
 
+def open_inplace_runner(plan, f, rank=0, world=1, group=None, overlap=True):
+    """A DistSlab that advances ONE block per rank in place.  The in-place
+    exchange writes into the neighbours' boundary planes, so it exists over
+    peer memory only: if some rank cannot map its neighbours every rank
+    raises.  Collective."""
+    ring, err = None, None
+    try:
+        ring = PeerRing(plan, [f], rank, world, group)
+    except Exception as exc:
+        err = f"{type(exc).__name__}: {exc}"
+    if not _agree(ring is not None, world, group, plan.device):
+        if ring is not None:
+            ring.close()
+        raise RuntimeError("the in-place update over z-slabs needs peer memory between the "
+                           "ranks (CUDA IPC): " + (err or "a peer rank could not map the ring"))
+    runner = DistSlab(CudaStepper(plan), plan.nz, rank, world, group, overlap=overlap, ring=ring)
+    runner.exchange(f)
+    return runner
+
+
 DIAG_KEYS = ("mass", "px", "py", "pz", "kinetic_energy", "max_u", "nonfinite", "fluid_cells")
 
 
@@ -477,6 +558,6 @@ def combine_diagnostics(local, rank=0, world=1, group=None):
     return out
 
 
-__all__ = ["combine_diagnostics", "DIAG_KEYS", "open_runner", "halos_match_send_recv",
+__all__ = ["combine_diagnostics", "DIAG_KEYS", "open_runner", "open_inplace_runner", "halos_match_send_recv",
            "halo_planes", "partition", "ring_neighbours", "slab_halo_flags", "CudaStepper",
            "PeerRing", "DistSlab", "exchange_flag_halos", "Q"]

@@ -146,7 +146,7 @@ def test_send_recv_transport_over_nccl(geom, tmp_path):
     np.testing.assert_array_equal(np.load(tmp_path / "nccl.npy"), want)
 
 
-def _engine_worker(rank, world, port, case, tag, out_dir):
+def _engine_worker(rank, world, port, case, tag, out_dir, inplace=False):
     signal.alarm(240)
     import torch
     import torch.distributed as dist
@@ -157,8 +157,11 @@ def _engine_worker(rank, world, port, case, tag, out_dir):
         torch.cuda.set_device(0)
         prec = {"f64": Precision.DOUBLE, "f32": Precision.SINGLE}[tag]
         spec = (cases.CaseSpec("ldc", 24, 20, 17, re=100.0, u0=0.1) if case == "ldc"
+                else cases.CaseSpec("ldc", 128, 12, 9, re=100.0, u0=0.1) if case == "ldc128"
+                else cases.CaseSpec("vks", 128, 32, 7, re=100.0, u0=0.08) if case == "vks128"
                 else cases.CaseSpec("vks", 48, 32, 11, re=100.0, u0=0.08))
-        probe = (12, 10, 9) if case == "ldc" else (30, 16, 2)
+        probe = {"ldc": (12, 10, 9), "ldc128": (60, 10, 5), "vks128": (90, 16, 2)}.get(
+            case, (30, 16, 2))
         # the same driver code twice: once alone on this GPU, once as one of `world` slabs
         alone = cases.init(spec, prec)
         seen_alone = []
@@ -168,7 +171,8 @@ def _engine_worker(rank, world, port, case, tag, out_dir):
                         probe=probe)
         state = cases.init(spec, prec)
         seen = []
-        rs = engine.run(state, engine.RunConfig(steps=23, precision=prec, output_every=10),
+        rs = engine.run(state, engine.RunConfig(steps=23, precision=prec, output_every=10,
+                                                inplace=inplace),
                         on_output=lambda st: seen.append((st.t, st.f_pre.data.copy())),
                         probe=probe)
         assert rs.transport == "peer", rs.transport
@@ -183,13 +187,79 @@ def _engine_worker(rank, world, port, case, tag, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case,tag,world", [("ldc", "f64", 2), ("ldc", "f32", 3), ("vks", "f32", 2)])
-def test_engine_run_is_the_same_call_under_torch_distributed(case, tag, world, tmp_path):
+@pytest.mark.parametrize("case,tag,world,inplace", [
+    ("ldc", "f64", 2, False), ("ldc", "f32", 3, False), ("vks", "f32", 2, False),
+    ("ldc128", "f32", 2, True), ("vks128", "f32", 3, True)])
+def test_engine_run_is_the_same_call_under_torch_distributed(case, tag, world, inplace, tmp_path):
     """The reference's driver call, unchanged, with one rank per slab: with a
     process group initialised, engine.run splits the domain into z-slabs, runs
     the fused peer-store exchange, fires the hooks at the same cadence with the
     whole host state gathered, and ends bit-identical to the single-GPU run."""
     import torch.multiprocessing as mp
-    mp.spawn(_engine_worker, args=(world, _free_port(), case, tag, str(tmp_path)),
+    mp.spawn(_engine_worker, args=(world, _free_port(), case, tag, str(tmp_path), inplace),
              nprocs=world, join=True)
     assert all((tmp_path / f"ok{r}").exists() for r in range(world))
+
+
+def _inplace_worker(rank, world, port, geom, tag, variant, steps, overlap, wait_mode, out_dir):
+    signal.alarm(240)
+    import torch
+    import torch.distributed as dist
+    from paper_2409_16781_b200 import slab
+    from paper_2409_16781_b200.kernels import KernelPlan
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        grid, wall_u, inlet_u = geometries3d()[geom]
+        prec = {"f64": Precision.DOUBLE, "f32": Precision.SINGLE, "f16": Precision.MIXED1}[tag]
+        nx, ny, nz = grid.shape
+        flags = B.flatten_mask(grid).reshape(nz, ny, nx)
+        f = random_block(np.random.default_rng(20240917), grid.size, prec.storage)
+        z0, z1 = slab.partition(nz, world)[rank]
+        n = z1 - z0
+        lo, hi = slab.exchange_flag_halos(flags[z0:z1], rank, world)
+        plan = KernelPlan(nx, ny, n, Layout.ROW, prec, flags[z0:z1], 1.3, wall_u,
+                          inlet_u=inlet_u, halo_lo=lo, halo_hi=hi, slab=True)
+        plan.set_variant(variant)
+        part = np.ascontiguousarray(f.reshape(19, nz, ny, nx)[:, z0:z1]).reshape(19, -1)
+        blk = plan.alloc()
+        blk.tensor.fill_(float("nan"))
+        plan.upload(part, blk)
+        ring = slab.PeerRing(plan, [blk], rank, world, wait_mode=wait_mode)
+        runner = slab.DistSlab(slab.CudaStepper(plan), n, rank, world, overlap=overlap, ring=ring)
+        runner.exchange(blk)
+        runner.run_inplace(blk, steps)
+        runner.normalize(blk)
+        out = np.empty_like(part)
+        plan.download(blk, out)
+        np.save(os.path.join(out_dir, f"slab{rank}.npy"), out.reshape(19, n, ny, nx))
+        ring.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("geom,tag,variant,world,steps,overlap,wait_mode", [
+    ("cavity16", "f32", 1008, 2, 7, False, 0),
+    ("cavity16", "f32", 1016, 2, 6, True, 2),
+    ("porous", "f64", 1008, 3, 5, False, 0),
+    ("channel40", "f32", 1008, 2, 7, False, 0),
+    ("periodic8", "f16", 2008, 2, 4, False, 0),
+    ("porous", "f32", 1008, 2, 9, True, 0),
+])
+def test_inplace_slabs_across_processes(geom, tag, variant, world, steps, overlap, wait_mode,
+                                        tmp_path):
+    """One block per rank: the in-place update over z-slabs, ranks in separate
+    processes writing into each other's boundary planes (pull half) and halo
+    planes (local half) through CUDA IPC mappings."""
+    import torch.multiprocessing as mp
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    nx, ny, nz = grid.shape
+    dtype = {"f64": np.float64, "f32": np.float32, "f16": np.float16}[tag]
+    f = random_block(np.random.default_rng(20240917), grid.size, dtype)
+    want = CpuOracle(nx, ny, nz, B.flatten_mask(grid), 1.3, wall_u, inlet_u).run(
+        f.copy(), f.copy(), steps)
+    mp.spawn(_inplace_worker, args=(world, _free_port(), geom, tag, variant, steps, overlap,
+                                    wait_mode, str(tmp_path)), nprocs=world, join=True)
+    got = np.concatenate([np.load(tmp_path / f"slab{r}.npy") for r in range(world)], axis=1)
+    np.testing.assert_array_equal(got.reshape(19, -1), want)

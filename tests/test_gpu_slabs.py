@@ -151,3 +151,41 @@ def test_peer_ring_single_rank(geom, tag, overlap, rng):
         fluidish = torch.isfinite(got[:, :, :, :nx].float())
         assert torch.equal(got[:, :, :, :nx][fluidish], newest.tensor[:, :, :, :nx][fluidish])
         ring.close()
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+@pytest.mark.parametrize("steps", [1, 2, 7])
+@pytest.mark.parametrize("tag,variant", [("f32", 1008), ("f64", 1016), ("f16", 2008)])
+@pytest.mark.parametrize("geom", ["cavity16", "periodic8", "porous", "channel40"])
+def test_inplace_slab_single_rank(geom, tag, variant, steps, overlap, rng):
+    """The in-place update on a z-slab (halo planes, peer ring closed on the
+    slab's own block): the pull half stores its crossing results into the
+    'neighbour's' boundary planes, the local half refills the halo planes."""
+    from paper_2409_16781_b200 import slab
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    prec = {"f64": Precision.DOUBLE, "f32": Precision.SINGLE, "f16": Precision.MIXED1}[tag]
+    f = random_block(rng, grid.size, prec.storage)
+    omega = 1.4
+    nx, ny, nz = grid.shape
+    want = CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u, inlet_u).run(
+        f.copy(), f.copy(), steps)
+    (plan, blocks, z0, z1), = make_slabs(grid, prec, omega, wall_u, inlet_u, f, 1)
+    plan.set_variant(variant)
+    blk = blocks[0]
+    ring = slab.PeerRing(plan, [blk])
+    runner = slab.DistSlab(slab.CudaStepper(plan), z1 - z0, overlap=overlap, ring=ring)
+    runner.exchange(blk)
+    runner.run_inplace(blk, steps)
+    assert blk.repr == steps % 2
+    runner.normalize(blk)
+    out = np.empty_like(f)
+    plan.download(blk, out)
+    np.testing.assert_array_equal(out, want)
+    # and on from the normalised state: halos were refilled
+    runner.run_inplace(blk, 2)
+    runner.normalize(blk)
+    plan.download(blk, out)
+    want2 = CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u, inlet_u).run(
+        want.copy(), want.copy(), 2)
+    np.testing.assert_array_equal(out, want2)
+    ring.close()
