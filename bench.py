@@ -71,6 +71,9 @@ def parse():
                          "planes from inside the fused kernel over CUDA-IPC-mapped peer memory "
                          "(default; falls back to 'nccl' if the mapping cannot be set up), "
                          "'nccl' = torch.distributed send/recv")
+    ap.add_argument("--inplace", action="store_true",
+                    help="the in-place update (one population block per GPU instead of two; same "
+                         "arithmetic and traffic)")
     ap.add_argument("--share-gpu", action="store_true",
                     help="debug, not a benchmark: all ranks use device 0 with a gloo control plane, so "
                          "a one-GPU box can drive the N > 1 code path (peer ring across processes)")
@@ -78,7 +81,7 @@ def parse():
     return ap.parse_args()
 
 
-def workload_config(n, nz_global, world, prec, omega):
+def workload_config(n, nz_global, world, prec, omega, inplace=False):
     size = f"{n}^3" if world == 1 else f"{n}x{n}x{nz_global}"
     return {
         "workload": f"D3Q19 BGK lid-driven cavity {size} {PREC_NAME[prec]}"
@@ -86,7 +89,8 @@ def workload_config(n, nz_global, world, prec, omega):
         "nx": n, "ny": n, "nz_per_gpu": n, "nz_global": nz_global,
         "re": RE, "u0": U0, "omega": omega,
         "decomposition": f"{world} z-slab(s), 5-population halos" if world > 1 else "single GPU",
-        "l2_policy": "inputs exceed L2: two population blocks of "
+        "blocks_per_gpu": 1 if inplace else 2,
+        "l2_policy": f"inputs exceed L2: {'one population block' if inplace else 'two population blocks'} of "
                      f"{19 * n ** 3 * PREC_BYTES[prec] / 1e9:.1f} GB per GPU vs 126 MB L2",
     }
 
@@ -284,32 +288,56 @@ def main():
             host[q].fill(W[q])
     if args.variant:
         plan.set_variant(args.variant)
-    kernel_name = plan.kernel_name
-    a, b = plan.alloc(), plan.alloc()
+    kernel_name = plan.kernel_name if not args.inplace else \
+        "mlb::aa_pull_vec_kernel + mlb::aa_local_vec_kernel (alternating)"
+    a = plan.alloc()
     plan.upload(host, a)
-    b.tensor.copy_(a.tensor)
-    plan.set_passthrough(True)   # both blocks identical: what engine.Session establishes
     runner = None
     transport = None
+    if args.inplace:
+        b = None
+        if slab_mode:
+            runner, transport = slab.open_inplace_runner(plan, a, rank, world), "peer"
+    else:
+        b = plan.alloc()
+        b.tensor.copy_(a.tensor)
+        plan.set_passthrough(True)   # both blocks identical: what engine.Session establishes
 
     def make_runner(p, x, y):
         return slab.open_runner(p, x, y, rank, world, transport=args.transport)
 
-    if slab_mode:
+    if slab_mode and not args.inplace:
         runner, transport = make_runner(plan, a, b)
 
     def advance(x, y, k):
+        if args.inplace:
+            if runner is None:
+                plan.run_steps_inplace(x, k)
+            else:
+                runner.run_inplace(x, k)
+            return x, y
         if runner is None:
             newest, other, _ = plan.run_steps(x, y, k)
             return newest, other
         return runner.run(x, y, k)
 
+    def settle(x):
+        """Pushes landed; in place: the block back in the normal representation."""
+        if runner is not None and args.inplace:
+            runner.normalize(x)
+        elif runner is not None:
+            runner.finish()
+        elif args.inplace:
+            plan.normalize(x)
+
     # ---- device-timed run: W warm-up, then exactly K steps -------------------
     a, b = advance(a, b, args.warmup)
-    if runner is not None:
+    if not args.inplace:
+        settle(a)
+    elif runner is not None:
         runner.finish()
     barrier()
-    if runner is not None and runner.ring is not None:
+    if runner is not None and runner.ring is not None and not args.inplace:
         # the fused exchange against the plain one, on live data: the halos the
         # kernels stored into this rank must be the planes send/recv delivers
         if not slab.halos_match_send_recv(plan, a, rank, world):
@@ -323,6 +351,7 @@ def main():
         if runner is not None:
             runner.finish()
         barrier()
+    settle(a)
     launches = _cabi.launch_count() - launches0
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
     nl = torch.tensor([launches], dtype=torch.int64, device=device)
@@ -346,8 +375,10 @@ def main():
         plan.close()
         torch.cuda.empty_cache()
         if not slab_mode:
-            cfg = engine.RunConfig(steps=args.steps, precision=prec, device=local)
-            warm = engine.RunConfig(steps=max(1, args.warmup), precision=prec, device=local)
+            cfg = engine.RunConfig(steps=args.steps, precision=prec, device=local,
+                                   inplace=args.inplace)
+            warm = engine.RunConfig(steps=max(1, args.warmup), precision=prec, device=local,
+                                    inplace=args.inplace)
             engine.run(state, warm)              # allocator / page-lock warm-up, untimed
             barrier()
             t0 = time.perf_counter()
@@ -358,13 +389,19 @@ def main():
             def e2e_once(k):
                 p = KernelPlan(n, n, n, Layout.ROW, prec, mask_flat, params.omega,
                                (U0, 0.0, 0.0), device=local, halo_lo=lo, halo_hi=hi, slab=True)
-                x, y = p.alloc(), p.alloc()
+                x = p.alloc()
                 p.upload(host, x)
-                y.tensor.copy_(x.tensor)
-                p.set_passthrough(True)
-                rr, _ = make_runner(p, x, y)
-                x, y = rr.run(x, y, k)
-                rr.finish()
+                if args.inplace:
+                    rr = slab.open_inplace_runner(p, x, rank, world)
+                    rr.run_inplace(x, k)
+                    rr.normalize(x)
+                else:
+                    y = p.alloc()
+                    y.tensor.copy_(x.tensor)
+                    p.set_passthrough(True)
+                    rr, _ = make_runner(p, x, y)
+                    x, y = rr.run(x, y, k)
+                    rr.finish()
                 p.download(x, host)
                 if rr.ring is not None:
                     rr.ring.close()
@@ -406,7 +443,12 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         key = f"step_kernel_{ {'single': 'f32', 'double': 'f64', 'mixed1': 'f16'}[prec_tok] }_{n}"
-        traffic = json.load(open(tpath)).get(key)
+        table = json.load(open(tpath))
+        traffic = table.get(key)
+        if args.inplace:   # the two halves alternate: per-launch average
+            tag = {'single': 'f32', 'double': 'f64', 'mixed1': 'f16'}[prec_tok]
+            pair = [table.get(f"aa_pull_{tag}_{n}"), table.get(f"aa_local_{tag}_{n}")]
+            traffic = sum(pair) / 2 if all(pair) else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "kernel": kernel_name, "algorithmic_bytes_per_update": bytes_per_update,
@@ -421,7 +463,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": PREC_DTYPE[prec_tok], "data": "synthetic",
-        "config": dict(workload_config(n, nz_global, world, prec_tok, params.omega),
+        "config": dict(workload_config(n, nz_global, world, prec_tok, params.omega, args.inplace),
                        **({"halo_transport": transport,
                            "signal_wait": {1: "stream memory operation", 2: "polling kernel"}[
                                _cabi.lib().mlb_signal_wait_kind()]} if transport else {})),
