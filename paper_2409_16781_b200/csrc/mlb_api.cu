@@ -810,8 +810,6 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     if (p->out_chained)
         p->passthrough = 0;  // see mlb_plan_set_passthrough
 
-    MLB_CUDA(cudaMalloc(&p->d_cls, padded * sizeof(uint32_t)));
-    MLB_CUDA(cudaMalloc(&p->d_mlinks, padded * sizeof(uint32_t)));
     p->n_in = (long long)in_idx.size();
     p->n_out = (long long)out_idx.size();
     if (p->n_in) {
@@ -826,10 +824,9 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
         if (p->out_chained)
             MLB_CUDA(cudaMalloc(&p->d_out_tmp, (size_t)p->lay.itemsize * MLB_Q * p->n_out));
     }
+    // flags -> one kind byte per cell + the dictionary of distinct (class word,
+    // link bits) pairs, in one pass (the class words live in registers)
     const dim3 grid((unsigned)((xp + 127) / 128), ny, nz + 2);
-    mlb::build_cls_kernel<<<grid, 128>>>(p->d_flags, p->d_cls, p->d_mlinks, p->g);
-    MLB_LAUNCHED();
-    // compress to one kind byte per cell + the dictionary of distinct pairs
     unsigned int *d_esc = nullptr;
     MLB_CUDA(cudaMalloc(&p->d_kind, padded));
     MLB_CUDA(cudaMalloc(&p->d_tab, 256 * sizeof(unsigned long long)));
@@ -837,21 +834,27 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     MLB_CUDA(cudaMemset(p->d_tab, 0xff, 256 * sizeof(unsigned long long)));
     MLB_CUDA(cudaMemset(p->d_tab, 0, sizeof(unsigned long long)));  // slot 0 = bulk (0, 0)
     MLB_CUDA(cudaMemset(d_esc, 0, sizeof(unsigned int)));
-    mlb::build_kind_kernel<<<(unsigned)((padded + 255) / 256), 256>>>(
-        p->d_cls, p->d_mlinks, (long long)padded, p->d_tab, p->d_kind, d_esc);
+    mlb::build_kind_kernel<<<grid, 128>>>(p->d_flags, p->g, p->d_tab, p->d_kind, d_esc, nullptr,
+                                          nullptr);
     MLB_LAUNCHED();
     MLB_CUDA(cudaMemcpy(&p->n_escape, d_esc, sizeof(unsigned int), cudaMemcpyDeviceToHost));
+    if (p->n_escape) {
+        // more than 254 distinct pairs: the overflow cells read full-width words.
+        // The table is full now, so a second pass finds the same slots.
+        MLB_CUDA(cudaMalloc(&p->d_cls, padded * sizeof(uint32_t)));
+        MLB_CUDA(cudaMalloc(&p->d_mlinks, padded * sizeof(uint32_t)));
+        MLB_CUDA(cudaMemset(d_esc, 0, sizeof(unsigned int)));
+        mlb::build_kind_kernel<<<grid, 128>>>(p->d_flags, p->g, p->d_tab, p->d_kind, d_esc,
+                                              p->d_cls, p->d_mlinks);
+        MLB_LAUNCHED();
+        MLB_CUDA(cudaMemcpy(&p->n_escape, d_esc, sizeof(unsigned int), cudaMemcpyDeviceToHost));
+    }
     cudaFree(d_esc);
     unsigned long long tab[256];
     MLB_CUDA(cudaMemcpy(tab, p->d_tab, sizeof(tab), cudaMemcpyDeviceToHost));
     p->n_kinds = 0;
     for (int k = 0; k < 255; ++k)
         p->n_kinds += tab[k] != mlb::KIND_EMPTY;
-    if (p->n_escape == 0) {
-        // the usual case: the dictionary covers the geometry, drop the 8 B / cell
-        cudaFree(p->d_cls); cudaFree(p->d_mlinks);
-        p->d_cls = p->d_mlinks = nullptr;
-    }
     cudaFree(p->d_flags);  // only the build reads the raw flag block
     p->d_flags = nullptr;
     p->have_flags = true;

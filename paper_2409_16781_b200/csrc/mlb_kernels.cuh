@@ -48,7 +48,7 @@ struct Geom {
     long long xp, plane, pop;  // row pitch, z-plane, population strides (elements)
 };
 
-// Per-cell class word, built once from the flags (build_cls_kernel):
+// Per-cell class word, computed from the flags (cell_class, inside build_kind_kernel):
 //   bits 0..2   the reference's flag code (boundaries.py:20-24)
 //   bit  2 + i  (i = 1..18) the source cell of direction i is a wall (SOLID or
 //               MOVING_WALL): that link bounces back
@@ -1243,24 +1243,19 @@ __device__ __forceinline__ constexpr int dir_index(int cx, int cy, int cz)
     return -1;
 }
 
-__global__ void build_cls_kernel(const uint8_t *__restrict__ flags,
-                                 uint32_t *__restrict__ cls, uint32_t *__restrict__ mlinks,
-                                 const Geom gm)
+// class word + moving-wall link bits of one padded element of the flag block
+__device__ __forceinline__ void cell_class(const uint8_t *__restrict__ flags, const Geom &gm,
+                                           int x, int y, int sz, uint32_t &cw, uint32_t &mw)
 {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    if (x >= gm.xp)
-        return;
-    const int y = blockIdx.y;
-    const int sz = blockIdx.z;  // storage plane
     const long long d = (long long)sz * gm.plane + (long long)y * gm.xp + x;
-    mlinks[d] = 0u;
+    mw = 0u;
     if (x >= gm.nx) {
-        cls[d] = 1u;  // row padding: solid, never written
+        cw = 1u;  // row padding: solid, never written
         return;
     }
     const uint32_t fl = flags[d];
     if (sz == 0 || sz == gm.nz + 1 || fl == 1 || fl == 2) {
-        cls[d] = fl;  // halo planes are only ever sources; walls have no links
+        cw = fl;  // halo planes are only ever sources; walls have no links
         return;
     }
     // fluid cells - and inlet / outlet cells, whose link bits only the in-place
@@ -1288,8 +1283,8 @@ __global__ void build_cls_kernel(const uint8_t *__restrict__ flags,
                 if (m == 2)
                     mv |= 1u << i;
             }
-    cls[d] = fl | c | (mv ? CLS_MOVING : 0u);
-    mlinks[d] = mv;
+    cw = fl | c | (mv ? CLS_MOVING : 0u);
+    mw = mv;
 }
 
 // Census of the padded flag block: [0] inlet cells, [1] outlet cells (slab
@@ -1318,15 +1313,24 @@ __global__ void flag_census_kernel(const uint8_t *__restrict__ flags, const Geom
 // escape, never a key); kind[d] = the slot.  Slot numbers depend on insertion
 // order, which no result depends on.
 constexpr unsigned long long KIND_EMPTY = ~0ull;
-__global__ void build_kind_kernel(const uint32_t *__restrict__ cls,
-                                  const uint32_t *__restrict__ mlinks, long long n,
+// One pass from the flags to the kind bytes: the class word of a cell lives in
+// registers only.  cls_full / ml_full are NULL on the first pass; if the
+// dictionary overflowed (escapes > 0) the host allocates them and runs the pass
+// again - the table is then full, so every cell finds its old slot or escapes -
+// and the escape cells get their full-width words.
+__global__ void build_kind_kernel(const uint8_t *__restrict__ flags, const Geom gm,
                                   unsigned long long *__restrict__ tab, uint8_t *__restrict__ kind,
-                                  unsigned int *__restrict__ escapes)
+                                  unsigned int *__restrict__ escapes,
+                                  uint32_t *__restrict__ cls_full, uint32_t *__restrict__ ml_full)
 {
-    const long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (d >= n)
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= gm.xp)
         return;
-    const unsigned long long key = ((unsigned long long)mlinks[d] << 32) | cls[d];
+    const int y = blockIdx.y, sz = blockIdx.z;  // storage plane
+    const long long d = (long long)sz * gm.plane + (long long)y * gm.xp + x;
+    uint32_t cw, mw;
+    cell_class(flags, gm, x, y, sz, cw, mw);
+    const unsigned long long key = ((unsigned long long)mw << 32) | cw;
     if (key == 0ull) {
         kind[d] = 0;
         return;
@@ -1342,6 +1346,10 @@ __global__ void build_kind_kernel(const uint32_t *__restrict__ cls,
     }
     kind[d] = (uint8_t)KIND_ESCAPE;
     atomicAdd(escapes, 1u);
+    if (cls_full) {
+        cls_full[d] = cw;
+        ml_full[d] = mw;
+    }
 }
 
 // ---------------------------------------------------------------------------
