@@ -1054,15 +1054,15 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
             n = 0;
 #define MLB_X(i, CX, Z, R)                                                            \
             if (CX > 0) { /* locations x0 .. x0+V-1 take cells x0+1 .. x0+V */        \
-                if (bulk_r) {                                                         \
-                    T o[V];                                                           \
-                    _Pragma("unroll") for (int j = 0; j < V - 1; ++j) o[j] = g[opp(i)][j + 1]; \
-                    o[V - 1] = nb[n];                                                 \
-                    PackIO<TS, V>::store(MLB_T(i, Z, R, x0), o);                      \
-                } else {                                                              \
-                    _Pragma("unroll") for (int j = 1; j < V; ++j)                     \
-                        *MLB_T(i, Z, R, x0 + j - 1) = Store<TS>::down(g[opp(i)][j]);  \
-                }                                                                     \
+                /* straight-line, predicated stores: the lanes at the ends of a warp */ \
+                /* row must not send the whole warp through a second code path       */ \
+                TS *base = MLB_T(i, Z, R, x0);                                        \
+                T o[V];                                                               \
+                _Pragma("unroll") for (int j = 0; j < V - 1; ++j) o[j] = g[opp(i)][j + 1]; \
+                o[V - 1] = nb[n];                                                     \
+                if (bulk_r) PackIO<TS, V>::store(base, o);                            \
+                _Pragma("unroll") for (int j = 0; j < V - 1; ++j)                     \
+                    if (!bulk_r) base[j] = Store<TS>::down(o[j]);                     \
                 if (!bulk_l) *MLB_T(i, Z, R, xl) = Store<TS>::down(g[opp(i)][0]);     \
                 ++n;                                                                  \
             }
@@ -1077,15 +1077,13 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
             n = 0;
 #define MLB_X(i, CX, Z, R)                                                            \
             if (CX < 0) { /* locations x0 .. x0+V-1 take cells x0-1 .. x0+V-2 */      \
-                if (bulk_l) {                                                         \
-                    T o[V];                                                           \
-                    _Pragma("unroll") for (int j = 1; j < V; ++j) o[j] = g[opp(i)][j - 1]; \
-                    o[0] = nb[n];                                                     \
-                    PackIO<TS, V>::store(MLB_T(i, Z, R, x0), o);                      \
-                } else {                                                              \
-                    _Pragma("unroll") for (int j = 0; j < V - 1; ++j)                 \
-                        *MLB_T(i, Z, R, x0 + j + 1) = Store<TS>::down(g[opp(i)][j]);  \
-                }                                                                     \
+                TS *base = MLB_T(i, Z, R, x0);                                        \
+                T o[V];                                                               \
+                _Pragma("unroll") for (int j = 1; j < V; ++j) o[j] = g[opp(i)][j - 1]; \
+                o[0] = nb[n];                                                         \
+                if (bulk_l) PackIO<TS, V>::store(base, o);                            \
+                _Pragma("unroll") for (int j = 1; j < V; ++j)                         \
+                    if (!bulk_l) base[j] = Store<TS>::down(o[j]);                     \
                 if (!bulk_r) *MLB_T(i, Z, R, xr) = Store<TS>::down(g[opp(i)][V - 1]); \
                 ++n;                                                                  \
             }
