@@ -1,0 +1,151 @@
+"""Seeded random geometries through every kernel family, against the oracle,
+bit for bit.  Each case draws its own grid shape (ragged and pack-aligned row
+lengths), flag field (solid and moving grains, inlet / outlet cells wherever
+the reference would accept them), relaxation rate, wall and inlet velocity,
+storage mode, kernel variant and step count; then runs
+  * the two-buffer kernels, strict stores with arbitrary never-written cells,
+  * the two-buffer kernels with pass-through stores (when the library accepts
+    the geometry),
+  * the in-place kernels (when the library accepts the geometry),
+  * the z-slab driver with the fused peer-store exchange (ring closed on the
+    slab itself), two blocks and - where accepted - one block,
+and requires the oracle's bits every time."""
+
+import numpy as np
+import pytest
+
+from oracle.cpu import CpuOracle
+from paper_2409_16781_b200 import boundaries as B
+from paper_2409_16781_b200.fields import Layout, Precision
+
+from .helpers import random_block
+
+pytestmark = pytest.mark.gpu
+
+PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED1}
+SCALAR = [32, 64, 128, 256]
+PACKS = {"f32": [1008, 1016, 1032], "f64": [1008, 1016, 1032],
+         "f16": [2008, 2016, 2032, 3008, 3016, 3032]}
+
+
+def draw_case(seed):
+    r = np.random.default_rng(seed)
+    tag = ["f32", "f64", "f16"][r.integers(3)]
+    aligned = r.random() < 0.7
+    nx = int(r.integers(2, 19)) * 4 if aligned else int(r.integers(5, 40))
+    ny, nz = int(r.integers(3, 9)), int(r.integers(3, 8))
+    grid = B.open_mask(nx, ny, nz)
+    u = r.random(grid.shape)
+    p_solid, p_move = r.choice([0.0, 0.05, 0.25]), r.choice([0.0, 0.03, 0.1])
+    grid[u < p_solid] = B.SOLID
+    grid[u > 1.0 - p_move] = B.MOVING_WALL
+    if r.random() < 0.4:          # a closed box around it
+        grid[0], grid[-1] = B.SOLID, B.SOLID
+        grid[:, 0], grid[:, -1] = B.SOLID, B.MOVING_WALL
+    inlet_u = 0.0
+    if r.random() < 0.5:          # open-boundary cells: anywhere, as index lists allow
+        inlet_u = float(r.uniform(0.01, 0.08))
+        for _ in range(int(r.integers(1, 4))):
+            x = int(r.integers(0, nx))
+            grid[x, r.integers(0, ny), :] = B.INLET
+        for _ in range(int(r.integers(1, 4))):
+            x = int(r.integers(1, nx))      # an outlet cell at x = 0 is rejected by design
+            grid[x, :, r.integers(0, nz)] = B.OUTLET
+    omega = float(r.choice([0.0, r.uniform(0.2, 1.99)], p=[0.05, 0.95]))
+    wall_u = tuple(float(v) for v in r.uniform(-0.06, 0.06, 3))
+    variant = int(r.choice(PACKS[tag] if aligned and r.random() < 0.75 else SCALAR))
+    if tag == "f16" and variant // 1000 == 2 and nx % 4:
+        variant = 128
+    steps = int(r.integers(1, 5))
+    return tag, grid, omega, wall_u, inlet_u, variant, steps
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("MLB_FUZZ_CASES", "120"))))
+def test_random_case_every_kernel_family_bitwise(seed):
+    from paper_2409_16781_b200 import slab
+    from paper_2409_16781_b200.kernels import KernelPlan
+    tag, grid, omega, wall_u, inlet_u, variant, steps = draw_case(seed)
+    prec = PREC[tag]
+    nx, ny, nz = grid.shape
+    mask = B.flatten_mask(grid)
+    rng = np.random.default_rng(1000 + seed)
+    f = random_block(rng, grid.size, prec.storage)
+    sentinel = random_block(rng, grid.size, prec.storage)
+    orc = CpuOracle(nx, ny, nz, mask, omega, wall_u, inlet_u)
+
+    def plan_for(**kw):
+        p = KernelPlan(nx, ny, nz, Layout.ROW, prec, mask, omega, wall_u, inlet_u=inlet_u, **kw)
+        p.set_variant(variant)
+        return p
+
+    # two buffers, strict: arbitrary never-written cells in the second buffer
+    want = orc.run(f.copy(), sentinel.copy(), steps)
+    plan = plan_for()
+    a, b = plan.alloc(), plan.alloc()
+    plan.upload(f, a)
+    plan.upload(sentinel, b)
+    newest, _, _ = plan.run_steps(a, b, steps)
+    got = np.empty_like(f)
+    plan.download(newest, got)
+    np.testing.assert_array_equal(got, want, err_msg=f"strict, case {seed}")
+    np.testing.assert_array_equal(plan.device_flags(), mask)
+
+    # from here on both buffers start identical (engine.py:148)
+    want = orc.run(f.copy(), f.copy(), steps)
+    try:
+        plan.set_passthrough(True)
+        fused = True
+    except ValueError:
+        fused = False             # chained outlet cells: refused by design
+    if fused:
+        plan.upload(f, a)
+        plan.upload(f, b)
+        newest, _, _ = plan.run_steps(a, b, steps)
+        plan.download(newest, got)
+        np.testing.assert_array_equal(got, want, err_msg=f"pass-through, case {seed}")
+
+    # in place, when the library serves this geometry with this variant
+    plan.upload(f, a)
+    a.repr = 0
+    try:
+        plan.run_steps_inplace(a, steps)
+        inplace = True
+    except ValueError:
+        inplace = False
+    if inplace:
+        plan.normalize(a)
+        plan.download(a, got)
+        np.testing.assert_array_equal(got, want, err_msg=f"in place, case {seed}")
+    plan.close()
+
+    # the z-slab driver, ring closed on the slab itself
+    flags3 = mask.reshape(nz, ny, nx)
+    lo, hi = slab.slab_halo_flags(flags3, nx, ny, 0, nz)
+    plan = plan_for(halo_lo=lo, halo_hi=hi, slab=True)
+    if fused:
+        plan.set_passthrough(True)
+    a, b = plan.alloc(), plan.alloc()
+    for blk in (a, b):
+        blk.tensor.fill_(float("nan"))
+        plan.upload(f, blk)
+    ring = slab.PeerRing(plan, [a, b])
+    runner = slab.DistSlab(slab.CudaStepper(plan), nz, overlap=bool(seed % 2), ring=ring)
+    runner.exchange(a)
+    newest, _ = runner.run(a, b, steps)
+    runner.finish()
+    plan.download(newest, got)
+    np.testing.assert_array_equal(got, want, err_msg=f"slab ring, case {seed}")
+    ring.close()
+    if inplace and variant >= 1000:
+        c = plan.alloc()
+        c.tensor.fill_(float("nan"))
+        plan.upload(f, c)
+        ring = slab.PeerRing(plan, [c])
+        runner = slab.DistSlab(slab.CudaStepper(plan), nz, overlap=bool(seed % 2), ring=ring)
+        runner.exchange(c)
+        runner.run_inplace(c, steps)
+        runner.normalize(c)
+        plan.download(c, got)
+        np.testing.assert_array_equal(got, want, err_msg=f"in-place slab, case {seed}")
+        ring.close()
+    plan.close()
