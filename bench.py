@@ -71,6 +71,9 @@ def parse():
                          "planes from inside the fused kernel over CUDA-IPC-mapped peer memory "
                          "(default; falls back to 'nccl' if the mapping cannot be set up), "
                          "'nccl' = torch.distributed send/recv")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: 'weak' = 512^3 cells per GPU (default, what the driver's scaling run "
+                         "measures), 'strong' = the N = 1 domain (512^3) split into N z-slabs")
     ap.add_argument("--inplace", action="store_true",
                     help="the in-place update (one population block per GPU instead of two; same "
                          "arithmetic and traffic)")
@@ -81,17 +84,18 @@ def parse():
     return ap.parse_args()
 
 
-def workload_config(n, nz_global, world, prec, omega, inplace=False):
-    size = f"{n}^3" if world == 1 else f"{n}x{n}x{nz_global}"
+def workload_config(n, nz_global, world, prec, omega, inplace=False, strong=False):
+    size = f"{n}^3" if nz_global == n else f"{n}x{n}x{nz_global}"
     return {
         "workload": f"D3Q19 BGK lid-driven cavity {size} {PREC_NAME[prec]}"
-                    f" (BASELINE.json configs[2]{', z-slab weak scaling' if world > 1 else ''})",
-        "nx": n, "ny": n, "nz_per_gpu": n, "nz_global": nz_global,
+                    f" (BASELINE.json configs[2]"
+                    f"{', z-slab ' + ('strong' if strong else 'weak') + ' scaling' if world > 1 else ''})",
+        "nx": n, "ny": n, "nz_per_gpu": nz_global // world, "nz_global": nz_global,
         "re": RE, "u0": U0, "omega": omega,
         "decomposition": f"{world} z-slab(s), 5-population halos" if world > 1 else "single GPU",
         "blocks_per_gpu": 1 if inplace else 2,
         "l2_policy": f"inputs exceed L2: {'one population block' if inplace else 'two population blocks'} of "
-                     f"{19 * n ** 3 * PREC_BYTES[prec] / 1e9:.1f} GB per GPU vs 126 MB L2",
+                     f"{19 * n * n * (nz_global // world) * PREC_BYTES[prec] / 1e9:.1f} GB per GPU vs 126 MB L2",
     }
 
 
@@ -155,11 +159,12 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------
-def slab_mask(n, rank, world):
-    """This rank's [x, y, z] flag block of the 512 x 512 x (512 world) cavity."""
+def slab_mask(n, nzl, rank, world):
+    """This rank's [x, y, z] flag block (nzl planes) of the cavity that the ranks'
+    slabs stack up to."""
     import numpy as np
     from paper_2409_16781_b200 import boundaries as B
-    m = B.cavity_mask(n, n, n, z_walls=False)
+    m = B.cavity_mask(n, n, nzl, z_walls=False)
     if rank == 0:
         m[:, :, 0] = B.SOLID
     if rank == world - 1:
@@ -257,9 +262,13 @@ def main():
             dist.init_process_group("nccl", device_id=device)
     prec = Precision.from_token(prec_tok)
     itemsize = prec.storage.itemsize
-    nz_global = n * world
+    strong = args.scaling == "strong" and world > 1
+    if strong and n % world:
+        raise SystemExit(f"--scaling strong needs {n} planes to split evenly over {world} ranks")
+    nzl = n // world if strong else n              # planes per rank
+    nz_global = nzl * world
     params = omega_from_reynolds(RE, U0, n)
-    cells_rank = n * n * n
+    cells_rank = n * n * nzl
     cells_all = cells_rank * world
 
     def barrier():
@@ -277,11 +286,11 @@ def main():
                           (U0, 0.0, 0.0), device=local)
         host = state.f_pre.data
     else:
-        m = slab_mask(n, rank, world)
+        m = slab_mask(n, nzl, rank, world)
         mask_flat = B.flatten_mask(m)
-        lo, hi = slab.exchange_flag_halos(mask_flat.reshape(n, n, n), rank, world,
+        lo, hi = slab.exchange_flag_halos(mask_flat.reshape(nzl, n, n), rank, world,
                                           device=None if args.share_gpu else device)
-        plan = KernelPlan(n, n, n, Layout.ROW, prec, mask_flat, params.omega,
+        plan = KernelPlan(n, n, nzl, Layout.ROW, prec, mask_flat, params.omega,
                           (U0, 0.0, 0.0), device=local, halo_lo=lo, halo_hi=hi, slab=True)
         host = pinned_empty((19, cells_rank), prec.storage)
         for q in range(19):
@@ -387,7 +396,7 @@ def main():
             dt = time.perf_counter() - t0
         else:
             def e2e_once(k):
-                p = KernelPlan(n, n, n, Layout.ROW, prec, mask_flat, params.omega,
+                p = KernelPlan(n, n, nzl, Layout.ROW, prec, mask_flat, params.omega,
                                (U0, 0.0, 0.0), device=local, halo_lo=lo, halo_hi=hi, slab=True)
                 x = p.alloc()
                 p.upload(host, x)
@@ -461,9 +470,10 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
         "dtype": PREC_DTYPE[prec_tok], "data": "synthetic",
-        "config": dict(workload_config(n, nz_global, world, prec_tok, params.omega, args.inplace),
+        "config": dict(workload_config(n, nz_global, world, prec_tok, params.omega, args.inplace,
+                                       strong),
                        **({"halo_transport": transport,
                            "signal_wait": {1: "stream memory operation", 2: "polling kernel"}[
                                _cabi.lib().mlb_signal_wait_kind()]} if transport else {})),
