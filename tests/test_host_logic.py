@@ -181,3 +181,18 @@ class TestSlabPartition:
         np.testing.assert_array_equal(hi, g[2])
         lo, hi = slab_halo_flags(g, 3, 2, 3, 5)
         np.testing.assert_array_equal(hi, g[0])
+
+    def test_single_rank_diagnostics_combine_is_the_identity(self):
+        from paper_2409_16781_b200.slab import DIAG_KEYS, combine_diagnostics
+        local = dict(zip(DIAG_KEYS, [3.5, 0.1, -0.2, 0.3, 1.25, 0.07, 0.0, 42.0]))
+        assert combine_diagnostics(local) == local
+
+    def test_distributed_run_needs_a_process_group(self):
+        from paper_2409_16781_b200 import cases, engine
+        state = cases.init(cases.CaseSpec("ldc", 8, 8, 8), Precision.SINGLE)
+        with pytest.raises(ValueError, match="process group"):
+            engine.run(state, engine.RunConfig(steps=1, distributed=True))
+        # auto mode without a process group is the single-GPU path: on this
+        # box that means the CUDA requirement, not a distributed error
+        assert engine._wants_slabs(engine.RunConfig(steps=1)) is False
+        assert engine._wants_slabs(engine.RunConfig(steps=1, distributed=False)) is False
