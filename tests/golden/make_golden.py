@@ -110,6 +110,16 @@ def main():
                                    boundaries.MOVING_WALL, boundaries.INLET,
                                    boundaries.OUTLET], dtype=np.uint8)
 
+    # wake analysis (cases.py:200-228) on a noisy, drifting two-tone series
+    rs = np.random.default_rng(20240917)
+    t = np.arange(3000, dtype=np.float64)
+    series = (0.02 * np.sin(2 * np.pi * t / 173.0) + 0.004 * np.sin(2 * np.pi * t / 41.0)
+              + 3e-6 * t + 0.002 * rs.standard_normal(t.size))
+    out["strouhal_series"] = series
+    out["strouhal_crossings"] = cases.zero_crossing_times(series)
+    st, n = cases.strouhal(series, 16.0, 0.08, sample_every=2)
+    out["strouhal_value"] = np.array([st, n], dtype=np.float64)
+
     path = os.path.join(HERE, "lb2d_golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path)} bytes")

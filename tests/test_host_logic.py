@@ -125,6 +125,44 @@ class TestCases:
             cases.l2_velocity_error(r, (r[1], r[1]))
 
 
+class TestShedding:
+    """The reference's wake analysis helpers (pkg/tests/test_cases.py:199-232)."""
+
+    def test_zero_crossings_of_sine(self):
+        from paper_2409_16781_b200.cases import zero_crossing_times
+        t = np.arange(1000, dtype=np.float64)
+        crossings = zero_crossing_times(np.sin(2 * np.pi * (t + 0.5) / 100.0))
+        assert crossings.size == 19
+        np.testing.assert_allclose(crossings[0], 49.5, rtol=1e-12)
+        np.testing.assert_allclose(np.diff(crossings), 50.0, rtol=1e-12)
+
+    def test_strouhal(self):
+        from paper_2409_16781_b200.cases import strouhal
+        period = 320.0
+        t = np.arange(4000, dtype=np.float64)
+        st, n = strouhal(0.02 * np.sin(2 * np.pi * t / period) + 1e-4 * t / 4000, 20.0, 0.1)
+        assert st == pytest.approx(20.0 / (period * 0.1), rel=1e-2) and n >= 20
+        t4 = np.arange(0, 4000, 4, dtype=np.float64)
+        st, _ = strouhal(np.sin(2 * np.pi * t4 / period), 20.0, 0.1, sample_every=4)
+        assert st == pytest.approx(20.0 / (period * 0.1), rel=1e-2)
+        with pytest.raises(ValueError, match="short"):
+            strouhal(np.zeros(5), 20.0, 0.1)
+        with pytest.raises(ValueError, match="no shedding"):
+            strouhal(np.zeros(100), 20.0, 0.1)
+
+    def test_equal_to_the_reference_on_a_noisy_series(self):
+        # values generated with the unmodified lb2d (tests/golden/make_golden.py)
+        from .conftest import GOLDEN
+        g = np.load(GOLDEN)
+        if "strouhal_series" not in g.files:
+            pytest.skip("golden file predates the shedding vectors")
+        from paper_2409_16781_b200.cases import strouhal, zero_crossing_times
+        np.testing.assert_array_equal(zero_crossing_times(g["strouhal_series"]),
+                                      g["strouhal_crossings"])
+        st, n = strouhal(g["strouhal_series"], 16.0, 0.08, sample_every=2)
+        assert (st, n) == (float(g["strouhal_value"][0]), int(g["strouhal_value"][1]))
+
+
 class TestEngineConfig:
     def test_schedule_and_runconfig_validation(self):
         with pytest.raises(ValueError, match="schedule"):
