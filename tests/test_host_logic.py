@@ -202,6 +202,13 @@ class TestPerfport:
         assert perfport.bandwidth_ceiling_mlups(6551.7, Precision.SINGLE) == pytest.approx(43103.3, rel=1e-5)
         assert perfport.achieved_bandwidth_gbs(37530.0, Precision.SINGLE) == pytest.approx(5704.56)
 
+    def test_c09_roofline_reproduction(self):
+        # the reference's acceptance criterion 9 (test_acceptance.py:215-224): the paper's
+        # V100S row - 1.1 TB/s x AI 1.37 against 1.55 TF/s, 976 GF/s achieved = 63 %
+        peak = perfport.roofline_peak(7.0e12, 1.1e12, 1.37)
+        assert abs(peak - 1.55e12) / 1.55e12 <= 0.05
+        assert abs(perfport.roofline_efficiency(976.0, 1550.0) - 0.63) <= 0.01
+
 
 class TestSlabPartition:
     def test_partition_and_ring(self):
