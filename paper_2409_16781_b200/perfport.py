@@ -83,3 +83,66 @@ def achieved_bandwidth_gbs(mlups_value, precision):
 def bandwidth_ceiling_mlups(bandwidth_gbs, precision):
     """The update rate at which the ideal traffic saturates `bandwidth_gbs`."""
     return bandwidth_gbs * 1e9 / bytes_per_cell(precision) / 1e6
+
+
+# --------------------------------------------------------------------------
+# The reference's sweep protocol (perfport.py:156-184) on the CUDA path.
+class PerfRecord:
+    """Outcome of one benchmark job (fields follow lb2d's PerfRecord, plus the
+    third dimension and the bandwidth view this path is judged by)."""
+
+    FIELDS = ("case", "nx", "ny", "nz", "precision", "layout", "schedule", "inplace", "steps",
+              "seconds", "mlups", "flops_per_cell", "bytes_per_cell", "ai", "gbs", "error")
+
+    def __init__(self, spec, config):
+        nbytes = bytes_per_cell(config.precision)
+        self.case, self.nx, self.ny, self.nz = spec.name, spec.nx, spec.ny, spec.nz
+        self.precision = config.precision.token
+        self.layout = config.layout.token
+        self.schedule = config.schedule.label()
+        self.inplace = bool(config.inplace)
+        self.steps = config.steps
+        self.seconds = self.mlups = self.gbs = 0.0
+        self.flops_per_cell = FLOPS_PER_CELL
+        self.bytes_per_cell = nbytes
+        self.ai = arithmetic_intensity(FLOPS_PER_CELL, nbytes)
+        self.error = ""
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k in self.FIELDS}
+
+    def __repr__(self):
+        return f"PerfRecord({self.as_dict()})"
+
+
+def bench_sweep(jobs, reps=3, progress=None):
+    """Time (CaseSpec, RunConfig) jobs the way the reference does: one
+    discarded warm-up run, then `reps` runs each from a freshly initialised
+    state; the record carries the MEDIAN update-loop time (device time, CUDA
+    events - `RunStats.seconds`).  A job that raises is recorded with its
+    error and the sweep goes on."""
+    import statistics
+
+    from . import cases, engine  # deferred: metric-only users never touch the GPU path
+
+    if reps < 1:
+        raise ValueError("reps must be >= 1")
+    out = []
+    for spec, config in jobs:
+        rec = PerfRecord(spec, config)
+        try:
+            samples = []
+            for attempt in range(reps + 1):          # attempt 0 is the warm-up
+                state = cases.init(spec, config.precision, config.layout)
+                seconds = engine.run(state, config).seconds
+                if attempt:
+                    samples.append(seconds)
+            rec.seconds = statistics.median(samples)
+            rec.mlups = mlups(spec.nx, spec.ny, spec.nz, config.steps, rec.seconds)
+            rec.gbs = achieved_bandwidth_gbs(rec.mlups, config.precision)
+        except Exception as exc:  # noqa: BLE001 - one bad job must not end the sweep
+            rec.error = f"{type(exc).__name__}: {exc}"
+        out.append(rec)
+        if progress is not None:
+            progress(rec)
+    return out

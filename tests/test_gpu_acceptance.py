@@ -167,3 +167,24 @@ def test_c07_vks_shedding_and_symmetry_control():
     print(f"c07: St={st:.4f} crossings={crossings} symmetric-control crossings={crossings_sym}")
     assert 0.1 <= st <= 0.3 and crossings >= 20
     assert crossings_sym < 20 and crossings_sym < crossings
+
+
+def test_bench_sweep_protocol_and_survival():
+    """perfport.bench_sweep (the reference's sweep protocol, perfport.py:156-184,
+    exercised there by test_perfport.py): warm-up discarded, median of reps,
+    a failing job annotated instead of ending the sweep."""
+    from paper_2409_16781_b200 import perfport
+    from paper_2409_16781_b200.engine import RunConfig, Schedule
+    good = (CaseSpec("ldc", 64, 64, 64), RunConfig(steps=20))
+    inplace = (CaseSpec("ldc", 128, 32, 32), RunConfig(steps=20, inplace=True))
+    bad = (CaseSpec("ldc", 16, 16, 16), RunConfig(steps=5, schedule=Schedule("tiled", 64, 1, 1)))
+    seen = []
+    recs = perfport.bench_sweep([good, bad, inplace], reps=3, progress=seen.append)
+    assert [r.case for r in recs] == ["ldc"] * 3 and seen == recs
+    assert recs[0].error == "" and recs[0].mlups > 5.0 and recs[0].seconds > 0.0
+    assert recs[0].bytes_per_cell == 152 and recs[0].flops_per_cell == 195
+    assert recs[0].gbs == pytest.approx(recs[0].mlups * 152e6 / 1e9)
+    assert "exceeds" in recs[1].error and recs[1].mlups == 0.0
+    assert recs[2].error == "" and recs[2].inplace and recs[2].mlups > 5.0
+    with pytest.raises(ValueError, match="reps"):
+        perfport.bench_sweep([good], reps=0)
