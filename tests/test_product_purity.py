@@ -22,6 +22,21 @@ def test_package_never_imports_the_oracle():
                 assert not pat.search(code), f"{name} references the oracle"
 
 
+def test_only_tests_smoke_and_the_bench_cpu_arm_use_the_oracle():
+    pat = re.compile(r"^\s*(from|import)\s+oracle\b", re.M)
+    tools = os.path.join(ROOT, "tools")
+    for name in os.listdir(tools):
+        if name.endswith(".py"):
+            assert not pat.search(open(os.path.join(tools, name)).read()), f"tools/{name}"
+    # bench.py: inside cpu_arm only; __graft_entry__.py: inside smoke only
+    bench = open(os.path.join(ROOT, "bench.py")).read()
+    assert [m.start() for m in pat.finditer(bench)] and all(
+        bench.rfind("\ndef ", 0, m.start()) == bench.find("\ndef cpu_arm") for m in pat.finditer(bench))
+    entry = open(os.path.join(ROOT, "__graft_entry__.py")).read()
+    assert all(entry.rfind("\ndef ", 0, m.start()) == entry.find("\ndef smoke")
+               for m in pat.finditer(entry))
+
+
 def test_no_reference_sources_read_at_run_time():
     for name in ("bench.py", "__graft_entry__.py"):
         assert "/root/reference" not in open(os.path.join(ROOT, name)).read()
