@@ -245,7 +245,8 @@ int mlb_ipc_close(void *d_base);
  * without blocking the host.  mode 0 = a stream memory operation
  * (cuStreamWaitValue32: no SM is occupied) when the driver offers it, else a
  * one-thread polling kernel; 1 = memory operation or error; 2 = polling
- * kernel. */
+ * kernel.  post / wait / read act on the CURRENT device (the one `stream`
+ * belongs to); create selects `device` itself. */
 int mlb_signal_create(int device, void **d_sig);
 int mlb_signal_destroy(void *d_sig);
 int mlb_signal_post(void *d_slot, uint32_t value, void *stream);
