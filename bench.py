@@ -48,9 +48,11 @@ sys.path.insert(0, ROOT)
 NX = NY = NZ_PER_GPU = 512
 RE, U0 = 1000.0, 0.1
 METRIC = "MLUPS (D3Q19 BGK)"
-PREC_NAME = {"single": "fp32", "double": "fp64", "mixed1": "fp16 storage / fp32 compute"}
-PREC_BYTES = {"single": 4, "double": 8, "mixed1": 2}
-PREC_DTYPE = {"single": "f32", "double": "f64", "mixed1": "f16 storage, f32 compute"}
+PREC_NAME = {"single": "fp32", "double": "fp64", "mixed1": "fp16 storage / fp32 compute",
+             "mixed2": "fp32 storage / fp64 compute"}
+PREC_BYTES = {"single": 4, "double": 8, "mixed1": 2, "mixed2": 4}
+PREC_DTYPE = {"single": "f32", "double": "f64", "mixed1": "f16 storage, f32 compute",
+              "mixed2": "f32 storage, f64 compute"}
 
 
 def parse():
@@ -61,7 +63,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--edge", "--n", dest="n", type=int, default=0,
                     help="override the edge length (debug; use --edge under torchrun)")
-    ap.add_argument("--precision", default="single", choices=["single", "double", "mixed1"])
+    ap.add_argument("--precision", default="single", choices=["single", "double", "mixed1", "mixed2"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-slab", action="store_true",
@@ -180,7 +182,8 @@ def cpu_arm(n, prec, steps, warmup, budget_s):
     from paper_2409_16781_b200 import boundaries as B
     from paper_2409_16781_b200.lattice import W, omega_from_reynolds
     cores = os.cpu_count() or 1
-    dtype = {"single": np.float32, "double": np.float64, "mixed1": np.float16}[prec]
+    dtype = {"single": np.float32, "double": np.float64, "mixed1": np.float16,
+             "mixed2": np.float32}[prec]
     omega = omega_from_reynolds(RE, U0, n).omega
 
     def make(nz):
@@ -188,7 +191,8 @@ def cpu_arm(n, prec, steps, warmup, budget_s):
         f = np.empty((19, n * n * nz), dtype=dtype)
         for q in range(19):
             f[q].fill(W[q])
-        return CpuOracle(n, n, nz, mask, omega, (U0, 0.0, 0.0), threads=cores), f, f.copy()
+        return CpuOracle(n, n, nz, mask, omega, (U0, 0.0, 0.0), threads=cores,
+                         compute=np.float64 if prec == "mixed2" else None), f, f.copy()
 
     # calibrate on a thin slice, then size the sample to the time budget
     orc, a, b = make(8)
@@ -451,11 +455,11 @@ def main():
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        key = f"step_kernel_{ {'single': 'f32', 'double': 'f64', 'mixed1': 'f16'}[prec_tok] }_{n}"
+        key = f"step_kernel_{ {'single': 'f32', 'double': 'f64', 'mixed1': 'f16', 'mixed2': 'm2'}[prec_tok] }_{n}"
         table = json.load(open(tpath))
         traffic = table.get(key)
         if args.inplace:   # the two halves alternate: per-launch average
-            tag = {'single': 'f32', 'double': 'f64', 'mixed1': 'f16'}[prec_tok]
+            tag = {'single': 'f32', 'double': 'f64', 'mixed1': 'f16', 'mixed2': 'm2'}[prec_tok]
             pair = [table.get(f"aa_pull_{tag}_{n}"), table.get(f"aa_local_{tag}_{n}")]
             traffic = sum(pair) / 2 if all(pair) else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -35,11 +35,12 @@ extern "C" {
 #define MLB_ABI_VERSION 1
 #define MLB_Q 19
 
-/* dtype codes = the reference's Precision wire codes (fields.py:22-24):
- * single, double, and mixed1 = populations STORED as IEEE binary16 and
- * computed in float (exact upcast on load, round-to-nearest-even on store,
- * kernels.py:435-455).  The reference's mixed2 (code 3) is not built. */
-enum { MLB_F32 = 0, MLB_F64 = 1, MLB_F16 = 2 };
+/* dtype codes = the reference's Precision wire codes (fields.py:22-25):
+ * single, double, mixed1 = populations STORED as IEEE binary16 and computed
+ * in float (exact upcast on load, round-to-nearest-even on store,
+ * kernels.py:435-455), mixed2 = stored as float, computed in double (every
+ * load upcast, kernels.py:80-96; the store rounds to nearest). */
+enum { MLB_F32 = 0, MLB_F64 = 1, MLB_F16 = 2, MLB_F32C64 = 3 };
 /* how the pulls across the slab's z faces are served */
 enum { MLB_Z_PERIODIC = 0, /* whole domain on this GPU: wrap in-kernel      */
        MLB_Z_HALO = 1 };   /* z-slab: read the halo planes (filled by the
@@ -51,7 +52,7 @@ typedef struct mlb_plan mlb_plan;
 
 typedef struct {
     int32_t nx, ny, nz;   /* slab cells                                    */
-    int32_t itemsize;     /* 4, 8 or 2 (storage dtype)                     */
+    int32_t itemsize;     /* 4, 8, 2 or 4 (storage dtype)                  */
     int64_t xp;           /* row pitch, elements                           */
     int64_t plane;        /* elements per z-plane = ny*xp                  */
     int64_t pop;          /* elements per population = (nz+2)*plane        */

@@ -46,7 +46,7 @@ def lib():
     global _lib
     if _lib is None:
         _lib = ctypes.CDLL(build())
-        for suf in ("f32", "f64", "h32"):
+        for suf in ("f32", "f64", "h32", "f32c64"):
             fn = getattr(_lib, f"orc_step_{suf}")
             fn.restype = ctypes.c_int
             fn.argtypes = [ctypes.POINTER(Geom), ctypes.c_void_p, ctypes.c_void_p,
@@ -69,8 +69,10 @@ def lib():
     return _lib
 
 
-def _suffix(dtype):
+def _suffix(dtype, compute=None):
     dtype = np.dtype(dtype)
+    if dtype == np.float32 and compute is not None and np.dtype(compute) == np.float64:
+        return "f32c64"  # single storage, double compute (the reference's MIXED2)
     if dtype == np.float32:
         return "f32"
     if dtype == np.float64:
@@ -85,7 +87,8 @@ def _ptr(a):
 
 
 class _Base:
-    def __init__(self, geom, flags, omega, wall_u, inlet_u, threads):
+    def __init__(self, geom, flags, omega, wall_u, inlet_u, threads, compute=None):
+        self.compute = compute  # None: the storage dtype's own (float16 -> float32)
         self.geom = geom
         self.flags = flags
         self.omega = float(omega)
@@ -100,7 +103,7 @@ class _Base:
 
     def step_range(self, fpre, fpost, z0, z1):
         self._check(fpre, fpost)
-        fn = getattr(lib(), f"orc_step_{_suffix(fpre.dtype)}")
+        fn = getattr(lib(), f"orc_step_{_suffix(fpre.dtype, self.compute)}")
         rc = fn(ctypes.byref(self.geom), _ptr(fpre), _ptr(fpost), _ptr(self.flags),
                 self.omega, self._uw, z0, z1, self.threads)
         if rc:
@@ -108,7 +111,7 @@ class _Base:
 
     def open_pass_range(self, fpost, z0, z1):
         self._check(fpost)
-        fn = getattr(lib(), f"orc_open_pass_{_suffix(fpost.dtype)}")
+        fn = getattr(lib(), f"orc_open_pass_{_suffix(fpost.dtype, self.compute)}")
         rc = fn(ctypes.byref(self.geom), _ptr(fpost), _ptr(self.flags),
                 self.inlet_u, z0, z1)
         if rc:
@@ -145,13 +148,13 @@ class CpuOracle(_Base):
     """Whole periodic domain, dense `(19, nx*ny*nz)` blocks, x fastest."""
 
     def __init__(self, nx, ny, nz, flags, omega, wall_u=(0.0, 0.0, 0.0),
-                 inlet_u=0.0, threads=1):
+                 inlet_u=0.0, threads=1, compute=None):
         flags = np.ascontiguousarray(flags, dtype=np.uint8).reshape(-1)
         n = nx * ny * nz
         if flags.size != n:
             raise ValueError("flag array does not match the grid")
         geom = Geom(nx, ny, nz, nx, nx * ny, n, 0, nz - 1, 0)
-        super().__init__(geom, flags, omega, wall_u, inlet_u, threads)
+        super().__init__(geom, flags, omega, wall_u, inlet_u, threads, compute)
 
     def run(self, fpre, fpost, steps):
         """`steps` x (fused update, open-boundary pass, swap); returns the
@@ -168,12 +171,12 @@ class SlabOracle(_Base):
     0 and nz+1 supply the pulls from lz = -1 and lz = nz."""
 
     def __init__(self, nx, ny, nz, xp, flags, omega, wall_u=(0.0, 0.0, 0.0),
-                 inlet_u=0.0, threads=1):
+                 inlet_u=0.0, threads=1, compute=None):
         flags = np.ascontiguousarray(flags, dtype=np.uint8)
         if flags.shape != (nz + 2, ny, xp):
             raise ValueError("slab flags must have shape (nz+2, ny, xp)")
         geom = Geom(nx, ny, nz, xp, ny * xp, (nz + 2) * ny * xp, 1, 0, nz + 1)
-        super().__init__(geom, flags, omega, wall_u, inlet_u, threads)
+        super().__init__(geom, flags, omega, wall_u, inlet_u, threads, compute)
 
 
 def equilibrium(rho, ux, uy, uz, dtype):

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmlb_d3q19.so")
 ABI_VERSION = 1
 
-MLB_F32, MLB_F64 = 0, 1
+MLB_F32, MLB_F64, MLB_F16, MLB_F32C64 = 0, 1, 2, 3
 IPC_HANDLE_BYTES = 64
 MLB_Z_PERIODIC, MLB_Z_HALO = 0, 1
 MLB_OK, MLB_EINVAL, MLB_ECUDA, MLB_ENOMEM, MLB_EUNSUPPORTED = 0, 1, 2, 3, 4

@@ -84,12 +84,12 @@ int layout_of(int nx, int ny, int nz, int dtype, mlb_layout *out)
 {
     if (nx < 1 || ny < 1 || nz < 1)
         return fail(MLB_EINVAL, "grid %dx%dx%d is empty", nx, ny, nz);
-    if (dtype != MLB_F32 && dtype != MLB_F64 && dtype != MLB_F16)
+    if (dtype != MLB_F32 && dtype != MLB_F64 && dtype != MLB_F16 && dtype != MLB_F32C64)
         return fail(MLB_EINVAL, "unknown dtype code %d (0 = f32, 1 = f64, 2 = f16 storage / "
-                    "f32 compute)", dtype);
+                    "f32 compute, 3 = f32 storage / f64 compute)", dtype);
     if (ny > 65535 || nz > 65535)
         return fail(MLB_EUNSUPPORTED, "ny and nz are limited to 65535 per slab");
-    const int sz = dtype == MLB_F32 ? 4 : dtype == MLB_F64 ? 8 : 2;
+    const int sz = dtype == MLB_F64 ? 8 : dtype == MLB_F16 ? 2 : 4;
     const long long line = 128 / sz;
     out->nx = nx; out->ny = ny; out->nz = nz; out->itemsize = sz;
     out->xp = (nx + line - 1) / line * line;
@@ -183,7 +183,7 @@ void inlet_values(double u_in, T *e)
 int pack_cells(int dtype, int variant)
 {
     const int bytes = 16 >> (variant / 1000 - 1);
-    const int sz = dtype == MLB_F32 ? 4 : dtype == MLB_F64 ? 8 : 2;
+    const int sz = dtype == MLB_F64 ? 8 : dtype == MLB_F16 ? 2 : 4;
     return bytes / sz;
 }
 
@@ -197,6 +197,8 @@ bool variant_exists(int dtype, int variant)
         return false;
     if (dtype == MLB_F16)
         return w == 2 || w == 3;
+    if (dtype == MLB_F32C64)
+        return w == 2;   // 8-byte packs: two floats, two doubles' worth of registers per population
     return w == 1;
 }
 
@@ -214,6 +216,8 @@ int resolve_variant(const mlb_plan *p)
     // cells, which only a pack kernel can handle inside the fused pass (~7 %)
     if (p->dtype == MLB_F64 && (p->n_in || p->n_out) && p->nx % 2 == 0 && p->nx >= 128)
         return 1016;
+    if (p->dtype == MLB_F32C64 && p->nx % 2 == 0 && p->nx >= 128)
+        return 2016;   // 8-byte packs: 36.6 vs 33.4 GLUPS (one cell per thread) at 512^3
     return 128;
 }
 
@@ -342,6 +346,9 @@ int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cuda
     if (p->dtype == MLB_F64)
         return push ? launch_typed<double, 2, 2, true>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push)
                     : launch_typed<double, 2, 2, false>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push);
+    if (p->dtype == MLB_F32C64)
+        return push ? launch_typed<mlb::f32w, 2, 2, true>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push)
+                    : launch_typed<mlb::f32w, 2, 2, false>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push);
     return push ? launch_typed<__half, 4, 2, true>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push)
                 : launch_typed<__half, 4, 2, false>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push);
 }
@@ -448,6 +455,7 @@ int resolve_aa_variant(const mlb_plan *p)
     if (p->dtype == MLB_F32 && p->nx % 4 == 0 && p->nx >= 128) return 1016;
     if (p->dtype == MLB_F64 && p->nx % 2 == 0 && p->nx >= 128) return 1016;
     if (p->dtype == MLB_F16 && p->nx % 4 == 0 && p->nx >= 128) return 2016;
+    if (p->dtype == MLB_F32C64 && p->nx % 2 == 0 && p->nx >= 128) return 2016;
     return 128;
 }
 
@@ -490,6 +498,9 @@ int launch_aa_any(mlb_plan *p, void *f, int kind, cudaStream_t st, const AaRange
     if (p->dtype == MLB_F64)
         return vec ? launch_aa_vec_lx<double, 2>(p, f, kind, lx, r, st)
                    : launch_aa<double>(p, f, kind, r, st);
+    if (p->dtype == MLB_F32C64)
+        return vec ? launch_aa_vec_lx<mlb::f32w, 2>(p, f, kind, lx, r, st)
+                   : launch_aa<mlb::f32w>(p, f, kind, r, st);
     if (vec && variant >= 3000) return launch_aa_vec_lx<__half, 2>(p, f, kind, lx, r, st);
     if (vec) return launch_aa_vec_lx<__half, 4>(p, f, kind, lx, r, st);
     return launch_aa<__half>(p, f, kind, r, st);
@@ -677,7 +688,8 @@ const char *mlb_plan_kernel_name(const mlb_plan *p)
     static thread_local char name[64];
     if (!p) return "";
     const int v = resolve_variant(p);
-    const char *t = p->dtype == MLB_F32 ? "float" : p->dtype == MLB_F64 ? "double" : "__half";
+    const char *t = p->dtype == MLB_F32 ? "float" : p->dtype == MLB_F64 ? "double"
+                  : p->dtype == MLB_F32C64 ? "f32w" : "__half";
     if (v >= 1000)
         snprintf(name, sizeof(name), "mlb::step_vec_kernel<%s, %d, %d, false>", t,
                  pack_cells(p->dtype, v), v % 1000);
@@ -945,6 +957,7 @@ int mlb_open_pass_range(mlb_plan *p, void *d_fpost, int z0, int z1, void *stream
     MLB_CUDA(cudaSetDevice(p->device));
     if (p->dtype == MLB_F32) return launch_open<float>(p, d_fpost, z0, z1, S(stream));
     if (p->dtype == MLB_F64) return launch_open<double>(p, d_fpost, z0, z1, S(stream));
+    if (p->dtype == MLB_F32C64) return launch_open<mlb::f32w>(p, d_fpost, z0, z1, S(stream));
     return launch_open<__half>(p, d_fpost, z0, z1, S(stream));
 }
 
@@ -1170,10 +1183,11 @@ int mlb_macro(const mlb_plan *p, const void *d_f, double *d_rho, double *d_ux, d
     if (int rc = check_plan(p, false)) return rc;
     if (!d_f || !d_rho || !d_ux || !d_uy || !d_uz) return fail(MLB_EINVAL, "NULL buffer");
     MLB_CUDA(cudaSetDevice(p->device));
+    // (the diagnostics read storage only: mixed2 - float in memory - shares the float kernels)
     const int V = p->dtype == MLB_F64 ? 2 : 4;   // cells per pack (16 / 16 / 8 bytes)
     if (p->nx % V == 0) {
         const dim3 grid((p->nx / V + 127) / 128, p->ny, p->nz);
-        if (p->dtype == MLB_F32)
+        if (p->dtype == MLB_F32 || p->dtype == MLB_F32C64)
             mlb::macro_vec_kernel<float, 4><<<grid, 128, 0, S(stream)>>>(
                 static_cast<const float *>(d_f), p->g, d_rho, d_ux, d_uy, d_uz);
         else if (p->dtype == MLB_F64)
@@ -1186,7 +1200,7 @@ int mlb_macro(const mlb_plan *p, const void *d_f, double *d_rho, double *d_ux, d
         return MLB_OK;
     }
     const dim3 grid((p->nx + 127) / 128, p->ny, p->nz);
-    if (p->dtype == MLB_F32)
+    if (p->dtype == MLB_F32 || p->dtype == MLB_F32C64)
         mlb::macro_kernel<float><<<grid, 128, 0, S(stream)>>>(
             static_cast<const float *>(d_f), p->g, d_rho, d_ux, d_uy, d_uz);
     else if (p->dtype == MLB_F64)
@@ -1207,7 +1221,7 @@ int mlb_diagnostics(mlb_plan *p, const void *d_f, double h_out[8], void *stream)
     const bool packs = p->nx % (p->dtype == MLB_F64 ? 2 : 4) == 0;
     const mlb::ClsTab ct = cls_tab(p);
     const int nb = p->diag_blocks, nt = mlb::DIAG_THREADS;
-    if (p->dtype == MLB_F32) {
+    if (p->dtype == MLB_F32 || p->dtype == MLB_F32C64) {
         const float *f = static_cast<const float *>(d_f);
         if (packs) mlb::diag_vec_kernel<float, 4><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
         else mlb::diag_kernel<float><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
@@ -1238,7 +1252,7 @@ int mlb_probe(const mlb_plan *p, const void *d_f, int x, int y, int lz, double *
     if (x < 0 || x >= p->nx || y < 0 || y >= p->ny || lz < 0 || lz >= p->nz)
         return fail(MLB_EINVAL, "probe cell (%d, %d, %d) outside the slab", x, y, lz);
     MLB_CUDA(cudaSetDevice(p->device));
-    if (p->dtype == MLB_F32)
+    if (p->dtype == MLB_F32 || p->dtype == MLB_F32C64)
         mlb::probe_kernel<float><<<1, 1, 0, S(stream)>>>(static_cast<const float *>(d_f),
                                                          p->g, x, y, lz, d_out4);
     else if (p->dtype == MLB_F64)

@@ -36,6 +36,14 @@ template <> struct Store<double> {
     static __host__ __device__ __forceinline__ double up(double v) { return v; }
     static __host__ __device__ __forceinline__ double down(double v) { return v; }
 };
+// MIXED2 (fields.py:25): float in memory, double arithmetic.  The element type
+// is a 4-byte wrapper so that the templates can tell it from plain float.
+struct f32w { float v; };
+template <> struct Store<f32w> {
+    using C = double;
+    static __host__ __device__ __forceinline__ double up(f32w x) { return (double)x.v; }
+    static __host__ __device__ __forceinline__ f32w down(double v) { f32w r; r.v = (float)v; return r; }
+};
 template <> struct Store<__half> {
     using C = float;
     static __host__ __device__ __forceinline__ float up(__half v) { return __half2float(v); }
@@ -661,6 +669,12 @@ template <> struct PackIO<double, 2> {
     { const double2 v = *reinterpret_cast<const double2 *>(p); o[0] = v.x; o[1] = v.y; }
     static __device__ __forceinline__ void store(double *p, const double (&o)[2])
     { *reinterpret_cast<double2 *>(p) = make_double2(o[0], o[1]); }
+};
+template <> struct PackIO<f32w, 2> {
+    static __device__ __forceinline__ void load(const f32w *p, double (&o)[2])
+    { const float2 v = *reinterpret_cast<const float2 *>(p); o[0] = (double)v.x; o[1] = (double)v.y; }
+    static __device__ __forceinline__ void store(f32w *p, const double (&o)[2])
+    { *reinterpret_cast<float2 *>(p) = make_float2((float)o[0], (float)o[1]); }
 };
 template <> struct PackIO<__half, 2> {
     static __device__ __forceinline__ void load(const __half *p, float (&o)[2])

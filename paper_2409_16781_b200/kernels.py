@@ -406,7 +406,7 @@ class KernelPlan:
 
 def _torch_dtype(precision):
     return {Precision.SINGLE: torch.float32, Precision.DOUBLE: torch.float64,
-            Precision.MIXED1: torch.float16}[precision]
+            Precision.MIXED1: torch.float16, Precision.MIXED2: torch.float32}[precision]
 
 
 def pinned_empty(shape, dtype):

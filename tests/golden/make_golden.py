@@ -61,7 +61,8 @@ def main():
 
     # --- cases through the reference engine (D2Q9, ROW layout) -------------
     ldc = cases.CaseSpec("ldc", 24, 24, re=100.0, u0=0.1)
-    for tag, prec in (("f64", Precision.DOUBLE), ("f32", Precision.SINGLE)):
+    for tag, prec in (("f64", Precision.DOUBLE), ("f32", Precision.SINGLE),
+                      ("m2", Precision.MIXED2)):
         for k, v in run_case(ldc, prec, 100).items():
             out[f"ldc24_{tag}_{k}"] = v
     tgv = cases.CaseSpec("tgv", 16, 16, re=50.0, u0=0.04)

@@ -22,15 +22,16 @@ from .helpers import random_block
 
 pytestmark = pytest.mark.gpu
 
-PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED1}
+PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED1,
+        "m2": Precision.MIXED2}
 SCALAR = [32, 64, 128, 256]
 PACKS = {"f32": [1008, 1016, 1032], "f64": [1008, 1016, 1032],
-         "f16": [2008, 2016, 2032, 3008, 3016, 3032]}
+         "f16": [2008, 2016, 2032, 3008, 3016, 3032], "m2": [2008, 2016, 2032]}
 
 
 def draw_case(seed):
     r = np.random.default_rng(seed)
-    tag = ["f32", "f64", "f16"][r.integers(3)]
+    tag = ["f32", "f64", "f16", "m2"][r.integers(4)]
     aligned = r.random() < 0.7
     nx = int(r.integers(2, 19)) * 4 if aligned else int(r.integers(5, 40))
     ny, nz = int(r.integers(3, 9)), int(r.integers(3, 8))
@@ -71,7 +72,8 @@ def test_random_case_every_kernel_family_bitwise(seed):
     rng = np.random.default_rng(1000 + seed)
     f = random_block(rng, grid.size, prec.storage)
     sentinel = random_block(rng, grid.size, prec.storage)
-    orc = CpuOracle(nx, ny, nz, mask, omega, wall_u, inlet_u)
+    orc = CpuOracle(nx, ny, nz, mask, omega, wall_u, inlet_u,
+                    compute=np.float64 if prec is Precision.MIXED2 else None)
 
     def plan_for(**kw):
         p = KernelPlan(nx, ny, nz, Layout.ROW, prec, mask, omega, wall_u, inlet_u=inlet_u, **kw)

@@ -17,7 +17,8 @@ from .helpers import geometries3d, random_block
 
 pytestmark = pytest.mark.gpu
 
-PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED1}
+PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED1,
+        "m2": Precision.MIXED2}
 WALL_GEOMS = ["porous", "cavity", "cavity_oblique_lid", "cavity16", "periodic", "periodic8", "wide"]
 
 
@@ -25,12 +26,13 @@ def make(grid, prec, omega, wall_u):
     from paper_2409_16781_b200.kernels import KernelPlan
     nx, ny, nz = grid.shape
     plan = KernelPlan(nx, ny, nz, Layout.ROW, prec, B.flatten_mask(grid), omega, wall_u)
-    orc = CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u)
+    orc = CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u,
+                    compute=np.float64 if prec is Precision.MIXED2 else None)
     return plan, orc
 
 
 @pytest.mark.parametrize("steps", [1, 2, 5, 8])
-@pytest.mark.parametrize("tag", ["f64", "f32", "f16"])
+@pytest.mark.parametrize("tag", ["f64", "f32", "f16", "m2"])
 @pytest.mark.parametrize("geom", WALL_GEOMS)
 def test_inplace_equals_oracle_bitwise(geom, tag, steps, rng):
     grid, wall_u, _ = geometries3d()[geom]
@@ -50,7 +52,7 @@ def test_inplace_equals_oracle_bitwise(geom, tag, steps, rng):
 
 
 PACK_VARIANTS = {"f32": [1008, 1016, 1032], "f64": [1008, 1016, 1032],
-                 "f16": [2008, 2016, 2032, 3008, 3016, 3032]}
+                 "f16": [2008, 2016, 2032, 3008, 3016, 3032], "m2": [2008, 2016, 2032]}
 
 
 @pytest.mark.parametrize("steps", [1, 2, 7])

@@ -17,10 +17,12 @@ from .helpers import (extrude_mask, from_xyzq, geometries3d, lift_2d,
 
 pytestmark = pytest.mark.gpu
 
-PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED1}
+PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED1,
+        "m2": Precision.MIXED2}
 VARIANTS = {"f32": [32, 64, 128, 256, 512, 1008, 1016, 1032],
             "f64": [32, 64, 128, 256, 512, 1008, 1016, 1032],
-            "f16": [32, 128, 512, 2008, 2016, 2032, 3008, 3016, 3032]}
+            "f16": [32, 128, 512, 2008, 2016, 2032, 3008, 3016, 3032],
+            "m2": [32, 128, 512, 2008, 2016, 2032]}
 
 
 def make_plan(grid, prec, omega, wall_u, inlet_u=0.0, **kw):
@@ -30,12 +32,15 @@ def make_plan(grid, prec, omega, wall_u, inlet_u=0.0, **kw):
                       wall_u, inlet_u=inlet_u, **kw)
 
 
-def make_oracle(grid, omega, wall_u, inlet_u=0.0):
+def make_oracle(grid, omega, wall_u, inlet_u=0.0, prec=None):
     nx, ny, nz = grid.shape
-    return CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u, inlet_u)
+    # the oracle computes in the storage dtype's own compute type unless told
+    # otherwise: MIXED2 is float storage with double arithmetic
+    compute = np.float64 if prec is Precision.MIXED2 else None
+    return CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u, inlet_u, compute=compute)
 
 
-@pytest.mark.parametrize("tag", ["f64", "f32", "f16"])
+@pytest.mark.parametrize("tag", ["f64", "f32", "f16", "m2"])
 @pytest.mark.parametrize("geom", list(geometries3d()))
 def test_one_step_bitwise(geom, tag, rng):
     grid, wall_u, inlet_u = geometries3d()[geom]
@@ -45,7 +50,7 @@ def test_one_step_bitwise(geom, tag, rng):
     post0 = random_block(rng, n, prec.storage)  # never-written cells must survive
     omega = 1.41
     want = post0.copy()
-    make_oracle(grid, omega, wall_u, inlet_u).step(f, want)
+    make_oracle(grid, omega, wall_u, inlet_u, prec).step(f, want)
     got = post0.copy()
     make_plan(grid, prec, omega, wall_u, inlet_u).step(f, got)  # host-block call
     np.testing.assert_array_equal(got, want)
@@ -64,7 +69,7 @@ def test_one_step_matches_naive_oracle(geom, rng):
     np.testing.assert_allclose(to_xyzq(got, nx, ny, nz), want, rtol=1e-12, atol=1e-15)
 
 
-@pytest.mark.parametrize("tag", ["f64", "f32", "f16"])
+@pytest.mark.parametrize("tag", ["f64", "f32", "f16", "m2"])
 @pytest.mark.parametrize("geom", list(geometries3d()))
 def test_multi_step_with_open_pass_bitwise(geom, tag, rng):
     grid, wall_u, inlet_u = geometries3d()[geom]
@@ -72,7 +77,7 @@ def test_multi_step_with_open_pass_bitwise(geom, tag, rng):
     f = random_block(rng, grid.size, prec.storage)
     omega, steps = 0.9, 7
     a, b = f.copy(), f.copy()
-    want = make_oracle(grid, omega, wall_u, inlet_u).run(a, b, steps)
+    want = make_oracle(grid, omega, wall_u, inlet_u, prec).run(a, b, steps)
     plan = make_plan(grid, prec, omega, wall_u, inlet_u)
     da, db = plan.alloc(), plan.alloc()
     plan.upload(f, da)
@@ -120,7 +125,7 @@ def test_kernel_variants_never_change_bits(geom, tag, variant, passthrough, rng)
         sentinel[:, non_fluid] = f[:, non_fluid]
     omega, steps = 1.6, 3
     a, b = f.copy(), sentinel.copy()
-    orc = make_oracle(grid, omega, wall_u, inlet_u)
+    orc = make_oracle(grid, omega, wall_u, inlet_u, prec)
     want = orc.run(a, b, steps)
     plan = make_plan(grid, prec, omega, wall_u, inlet_u)
     plan.set_variant(variant)

@@ -21,7 +21,9 @@ class TestFields:
         assert Precision.from_code(0) is Precision.SINGLE
         assert Precision.MIXED1.storage == np.float16 and Precision.MIXED1.compute == np.float32
         assert Precision.from_code(2) is Precision.MIXED1  # the reference's wire code
-        for bad in ("mixed2", "half"):
+        assert Precision.MIXED2.storage == np.float32 and Precision.MIXED2.compute == np.float64
+        assert Precision.from_code(3) is Precision.MIXED2 and Precision.from_token("mixed2").code == 3
+        for bad in ("mixed3", "half"):
             with pytest.raises(ValueError, match="precision"):
                 Precision.from_token(bad)
 

@@ -32,7 +32,7 @@ def oracle_for(grid, omega, wall_u, inlet_u=0.0, threads=2):
 class TestBridgeToLb2d:
     @pytest.mark.parametrize("case,tag,tol", [
         ("ldc24", "f64", 1e-13), ("tgv16", "f64", 1e-13), ("vks48", "f64", 1e-13),
-        ("ldc24", "f32", 1e-5)])
+        ("ldc24", "f32", 1e-5), ("ldc24", "m2", 1e-6)])
     @pytest.mark.parametrize("nz", [1, 4])
     def test_engine_runs(self, case, tag, tol, nz, golden):
         """LDC, TGV and channel+disk (inlet/outlet pass included) through
@@ -42,7 +42,8 @@ class TestBridgeToLb2d:
         wu = golden[p + "wall_u"]
         orc = CpuOracle(nx, ny, nz, extrude_mask(golden[p + "mask"], nx, ny, nz),
                         float(golden[p + "omega"]), (wu[0], wu[1], 0.0),
-                        float(golden[p + "inlet_u"]), threads=4)
+                        float(golden[p + "inlet_u"]), threads=4,
+                        compute=np.float64 if tag == "m2" else None)
         f0 = lift_2d(golden[p + "f0"], nz)
         got = orc.run(f0.copy(), f0.copy(), steps)
         want = golden[p + "f"].astype(np.float64)
@@ -56,6 +57,13 @@ class TestBridgeToLb2d:
             assert np.abs(ux[:, :, z] - golden[p + "ux"]).max() <= tol * max(1.0, 1 / scale) * scale + tol
             assert np.abs(uy[:, :, z] - golden[p + "uy"]).max() <= tol * max(1.0, 1 / scale) * scale + tol
         assert np.abs(uz).max() <= (1e-15 if tag == "f64" else 1e-7)
+        if tag == "m2":
+            # lb2d's mixed2 run (float planes, double arithmetic) is closer to its
+            # double run than its single run is: the mode does what it says
+            d64 = golden["ldc24_f64_f"]
+            e_m2 = np.abs(golden["ldc24_m2_f"].astype(np.float64) - d64).max()
+            e_f32 = np.abs(golden["ldc24_f32_f"].astype(np.float64) - d64).max()
+            assert e_m2 < e_f32
 
     @pytest.mark.parametrize("geom", ["cavity", "channel", "periodic"])
     def test_one_step_on_reference_kernel_geometries(self, geom, golden):
@@ -201,6 +209,39 @@ class TestMixed1Storage:
         f16 = random_block(rng, grid.size, np.float16)
         for got, want in zip(orc.macro(f16), orc.macro(f16.astype(np.float64))):
             np.testing.assert_array_equal(got, want)
+
+
+class TestMixed2Storage:
+    @pytest.mark.parametrize("geom", ["cavity_oblique_lid", "channel40", "periodic8"])
+    def test_float_storage_is_the_double_kernel_between_two_casts(self, geom, rng):
+        """The reference's MIXED2 (fields.py:25): its kernel, compiled for
+        float64, upcasts every load (`one * fpre[...]`, kernels.py:80-96) and the
+        store into the float32 plane rounds to nearest.  The oracle's
+        float-storage / double-compute instantiation must equal the double
+        kernel between an exact upcast and one rounding, step after step,
+        never-written cells included."""
+        grid, wall_u, inlet_u = geometries3d()[geom]
+        nx, ny, nz = grid.shape
+        mask = B.flatten_mask(grid)
+        m2 = CpuOracle(nx, ny, nz, mask, 1.3, wall_u, inlet_u, compute=np.float64)
+        dbl = CpuOracle(nx, ny, nz, mask, 1.3, wall_u, inlet_u)
+        a, b = random_block(rng, grid.size, np.float32), random_block(rng, grid.size, np.float32)
+        a64, b64 = a.astype(np.float64), b.astype(np.float64)
+        for _ in range(4):
+            m2.step(a, b)
+            m2.open_pass(b)
+            dbl.step(a64, b64)
+            dbl.open_pass(b64)
+            b64 = b64.astype(np.float32).astype(np.float64)   # the store's rounding + the next load
+            np.testing.assert_array_equal(b, b64.astype(np.float32))
+            a, b, a64, b64 = b, a, b64, a64
+        # and it is NOT the float kernel
+        s = CpuOracle(nx, ny, nz, mask, 1.3, wall_u, inlet_u)
+        x = random_block(rng, grid.size, np.float32)
+        y1, y2 = x.copy(), x.copy()
+        s.step(x, y1)
+        m2.step(x, y2)
+        assert not np.array_equal(y1, y2)
 
 
 # ---- 3. the independent naive oracle on 3-D geometries ----------------------

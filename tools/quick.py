@@ -12,12 +12,12 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 peak = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"]
 mask = B.flatten_mask(B.cavity_mask(n, n, n))
-for prec in (Precision.SINGLE, Precision.DOUBLE, Precision.MIXED1):
+for prec in (Precision.SINGLE, Precision.DOUBLE, Precision.MIXED1, Precision.MIXED2):
     for mode in ("ab", "inplace"):
         plan = KernelPlan(n, n, n, Layout.ROW, prec, mask, 1.53, (0.1, 0, 0))
         if os.environ.get("MLB_VARIANT"):
             v = int(os.environ["MLB_VARIANT"])
-            plan.set_variant(v if prec is not Precision.MIXED1 else v + 1000)
+            plan.set_variant(v if prec in (Precision.SINGLE, Precision.DOUBLE) else v + 1000)
         a = plan.alloc()
         for q in range(19):
             a.tensor[q].fill_(float(W[q]))
