@@ -112,7 +112,7 @@ def test_distslab_overlap_path_single_rank(geom, rng):
 
 
 @pytest.mark.parametrize("overlap", [True, False])
-@pytest.mark.parametrize("tag", ["f64", "f32", "f16"])
+@pytest.mark.parametrize("tag", ["f64", "f32", "f16", "m2"])
 @pytest.mark.parametrize("geom", ["cavity_oblique_lid", "channel", "periodic", "cavity16",
                                   "channel40", "open_chain", "open_unfusable"])
 def test_peer_ring_single_rank(geom, tag, overlap, rng):
@@ -122,7 +122,8 @@ def test_peer_ring_single_rank(geom, tag, overlap, rng):
     pass-through stores, fused and list-driven open-boundary pass."""
     from paper_2409_16781_b200 import slab
     grid, wall_u, inlet_u = geometries3d()[geom]
-    prec = {"f64": Precision.DOUBLE, "f32": Precision.SINGLE, "f16": Precision.MIXED1}[tag]
+    prec = {"f64": Precision.DOUBLE, "f32": Precision.SINGLE, "f16": Precision.MIXED1,
+            "m2": Precision.MIXED2}[tag]
     f = random_block(rng, grid.size, prec.storage)
     steps, omega = 5, 1.4
     want = single_domain(grid, prec, omega, wall_u, inlet_u, f, steps)
