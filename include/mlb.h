@@ -65,6 +65,12 @@ int mlb_abi_version(void);
 /* number of CUDA kernel launches issued by this library in this process */
 int64_t mlb_launch_count(void);
 
+/* The plans' device memory (flag tables, lists, scratch) is pooled inside the
+ * library: destroying a plan keeps its blocks for the next one of the same
+ * shape (cudaMalloc / cudaFree stall the device; up to 6 GB are held back).
+ * mlb_trim returns the idle blocks to the driver. */
+int mlb_trim(void);
+
 int mlb_layout_query(int nx, int ny, int nz, int dtype, mlb_layout *out);
 
 /* ---- plan: replaces KernelPlan.__init__ (kernels.py:408-443) -------------

@@ -22,7 +22,7 @@ MLB_OK, MLB_EINVAL, MLB_ECUDA, MLB_ENOMEM, MLB_EUNSUPPORTED = 0, 1, 2, 3, 4
 
 #: every symbol include/mlb.h declares; tests check the .so exports them all
 SYMBOLS = (
-    "mlb_last_error", "mlb_abi_version", "mlb_launch_count", "mlb_layout_query",
+    "mlb_last_error", "mlb_abi_version", "mlb_launch_count", "mlb_trim", "mlb_layout_query",
     "mlb_plan_create", "mlb_plan_destroy", "mlb_plan_get_layout",
     "mlb_plan_set_physics", "mlb_plan_set_variant", "mlb_plan_set_passthrough",
     "mlb_plan_kernel_name", "mlb_plan_set_flags",
@@ -66,6 +66,7 @@ def lib():
         "mlb_last_error": (ctypes.c_char_p, []),
         "mlb_abi_version": (i, []),
         "mlb_launch_count": (ctypes.c_int64, []),
+        "mlb_trim": (i, []),
         "mlb_layout_query": (i, [i, i, i, i, ctypes.POINTER(Layout)]),
         "mlb_plan_create": (i, [ctypes.POINTER(vp), i, i, i, i, d, dp3, d, i, i]),
         "mlb_plan_destroy": (i, [vp]),

@@ -8,6 +8,9 @@
 #include "mlb_kernels.cuh"
 
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <unordered_map>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -44,6 +47,82 @@ int fail(int code, const char *fmt, ...)
     } while (0)
 
 inline cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
+
+// Device memory of the plans (flag tables, index lists, reduction scratch, signal
+// words) comes from a small process-wide pool: cudaMalloc / cudaFree synchronise
+// the device and were measured to stall for 0.1 - 1.4 s now and then with tens of
+// GB of populations resident - a large, erratic part of a short run's end-to-end
+// time (plan setup + teardown are inside engine.run).  Freed blocks are kept,
+// keyed by (device, size), and handed out again to the next plan of the same
+// shape; at most POOL_CAP bytes are held back, mlb_trim() returns them all.
+class DevicePool {
+public:
+    cudaError_t alloc(void **out, size_t bytes)
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            auto it = free_.find({dev, bytes});
+            if (it != free_.end()) {
+                *out = it->second;
+                free_.erase(it);
+                cached_ -= bytes;
+                live_[*out] = {dev, bytes};
+                return cudaSuccess;
+            }
+        }
+        cudaError_t e = cudaMalloc(out, bytes);
+        if (e != cudaSuccess) {       // give the pool's idle memory back and retry once
+            trim();
+            e = cudaMalloc(out, bytes);
+        }
+        if (e == cudaSuccess) {
+            std::lock_guard<std::mutex> g(mu_);
+            live_[*out] = {dev, bytes};
+        }
+        return e;
+    }
+    void release(void *p)
+    {
+        if (!p) return;
+        std::lock_guard<std::mutex> g(mu_);
+        auto it = live_.find(p);
+        if (it == live_.end()) {      // not ours
+            cudaFree(p);
+            return;
+        }
+        const Key k = it->second;
+        live_.erase(it);
+        if (cached_ + k.second > POOL_CAP) {
+            cudaFree(p);
+            return;
+        }
+        free_.insert({k, p});
+        cached_ += k.second;
+    }
+    void trim()
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        for (auto &kv : free_)
+            cudaFree(kv.second);
+        free_.clear();
+        cached_ = 0;
+    }
+
+private:
+    using Key = std::pair<int, size_t>;
+    static constexpr size_t POOL_CAP = 6ull << 30;
+    std::mutex mu_;
+    std::multimap<Key, void *> free_;
+    std::unordered_map<void *, Key> live_;
+    size_t cached_ = 0;
+};
+DevicePool g_pool;
+
+template <typename T>
+cudaError_t pool_alloc(T **out, size_t bytes) { return g_pool.alloc(reinterpret_cast<void **>(out), bytes); }
+inline void pool_free(void *p) { g_pool.release(p); }
 
 }  // namespace
 
@@ -625,8 +704,8 @@ int mlb_plan_create(mlb_plan **out, int nx, int ny, int nz, int dtype, double om
     }
     cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
     p->diag_blocks = p->sms * 8;
-    cudaError_t e = cudaMalloc(&p->d_partials, sizeof(double) * mlb::DIAG_N * p->diag_blocks);
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_diag, sizeof(double) * mlb::DIAG_N);
+    cudaError_t e = pool_alloc(&p->d_partials, sizeof(double) * mlb::DIAG_N * p->diag_blocks);
+    if (e == cudaSuccess) e = pool_alloc(&p->d_diag, sizeof(double) * mlb::DIAG_N);
     if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&p->ev1);
     if (e != cudaSuccess) {
@@ -642,9 +721,9 @@ int mlb_plan_destroy(mlb_plan *p)
     if (!p)
         return MLB_OK;
     cudaSetDevice(p->device);
-    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_mlinks); cudaFree(p->d_in);
-    cudaFree(p->d_kind); cudaFree(p->d_tab);
-    cudaFree(p->d_out); cudaFree(p->d_out_tmp); cudaFree(p->d_partials); cudaFree(p->d_diag);
+    pool_free(p->d_flags); pool_free(p->d_cls); pool_free(p->d_mlinks); pool_free(p->d_in);
+    pool_free(p->d_kind); pool_free(p->d_tab);
+    pool_free(p->d_out); pool_free(p->d_out_tmp); pool_free(p->d_partials); pool_free(p->d_diag);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
     delete p;
@@ -724,9 +803,9 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     const uint8_t *src_lo = h_lo ? h_lo : h_flags + (size_t)(nz - 1) * dense_plane;
     const uint8_t *src_hi = h_hi ? h_hi : h_flags;
 
-    cudaFree(p->d_flags); cudaFree(p->d_cls); cudaFree(p->d_mlinks); cudaFree(p->d_in);
-    cudaFree(p->d_kind); cudaFree(p->d_tab);
-    cudaFree(p->d_out); cudaFree(p->d_out_tmp);
+    pool_free(p->d_flags); pool_free(p->d_cls); pool_free(p->d_mlinks); pool_free(p->d_in);
+    pool_free(p->d_kind); pool_free(p->d_tab);
+    pool_free(p->d_out); pool_free(p->d_out_tmp);
     p->d_flags = nullptr; p->d_cls = p->d_mlinks = nullptr; p->d_in = p->d_out = nullptr;
     p->d_kind = nullptr; p->d_tab = nullptr;
     p->d_out_tmp = nullptr;
@@ -735,7 +814,7 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
 
     // the padded flag block on the device, straight from the caller's dense
     // array (row padding = solid, never written); no padded host copy
-    MLB_CUDA(cudaMalloc(&p->d_flags, padded));
+    MLB_CUDA(pool_alloc(&p->d_flags, padded));
     if (xp != nx)
         MLB_CUDA(cudaMemset(p->d_flags, 1, padded));
     if (xp == nx)
@@ -753,7 +832,7 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     // needed only if there are any) and invalid codes.  A cavity or a periodic
     // box never walks its flags on the host.
     unsigned long long *d_census = nullptr, census[3] = {0, 0, 0};
-    MLB_CUDA(cudaMalloc(&d_census, sizeof(census)));
+    MLB_CUDA(pool_alloc(&d_census, sizeof(census)));
     MLB_CUDA(cudaMemset(d_census, 0, sizeof(census)));
     {
         const dim3 cgrid((unsigned)((xp + 255) / 256), ny, nz + 2);
@@ -761,7 +840,7 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
         MLB_LAUNCHED();
     }
     MLB_CUDA(cudaMemcpy(census, d_census, sizeof(census), cudaMemcpyDeviceToHost));
-    cudaFree(d_census);
+    pool_free(d_census);
 
     std::vector<long long> in_idx, out_idx;
     p->in_zoff.assign(nz + 1, 0);
@@ -825,24 +904,24 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     p->n_in = (long long)in_idx.size();
     p->n_out = (long long)out_idx.size();
     if (p->n_in) {
-        MLB_CUDA(cudaMalloc(&p->d_in, sizeof(long long) * p->n_in));
+        MLB_CUDA(pool_alloc(&p->d_in, sizeof(long long) * p->n_in));
         MLB_CUDA(cudaMemcpy(p->d_in, in_idx.data(), sizeof(long long) * p->n_in,
                             cudaMemcpyHostToDevice));
     }
     if (p->n_out) {
-        MLB_CUDA(cudaMalloc(&p->d_out, sizeof(long long) * p->n_out));
+        MLB_CUDA(pool_alloc(&p->d_out, sizeof(long long) * p->n_out));
         MLB_CUDA(cudaMemcpy(p->d_out, out_idx.data(), sizeof(long long) * p->n_out,
                             cudaMemcpyHostToDevice));
         if (p->out_chained)
-            MLB_CUDA(cudaMalloc(&p->d_out_tmp, (size_t)p->lay.itemsize * MLB_Q * p->n_out));
+            MLB_CUDA(pool_alloc(&p->d_out_tmp, (size_t)p->lay.itemsize * MLB_Q * p->n_out));
     }
     // flags -> one kind byte per cell + the dictionary of distinct (class word,
     // link bits) pairs, in one pass (the class words live in registers)
     const dim3 grid((unsigned)((xp + 127) / 128), ny, nz + 2);
     unsigned int *d_esc = nullptr;
-    MLB_CUDA(cudaMalloc(&p->d_kind, padded));
-    MLB_CUDA(cudaMalloc(&p->d_tab, 256 * sizeof(unsigned long long)));
-    MLB_CUDA(cudaMalloc(&d_esc, sizeof(unsigned int)));
+    MLB_CUDA(pool_alloc(&p->d_kind, padded));
+    MLB_CUDA(pool_alloc(&p->d_tab, 256 * sizeof(unsigned long long)));
+    MLB_CUDA(pool_alloc(&d_esc, sizeof(unsigned int)));
     MLB_CUDA(cudaMemset(p->d_tab, 0xff, 256 * sizeof(unsigned long long)));
     MLB_CUDA(cudaMemset(p->d_tab, 0, sizeof(unsigned long long)));  // slot 0 = bulk (0, 0)
     MLB_CUDA(cudaMemset(d_esc, 0, sizeof(unsigned int)));
@@ -853,21 +932,21 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     if (p->n_escape) {
         // more than 254 distinct pairs: the overflow cells read full-width words.
         // The table is full now, so a second pass finds the same slots.
-        MLB_CUDA(cudaMalloc(&p->d_cls, padded * sizeof(uint32_t)));
-        MLB_CUDA(cudaMalloc(&p->d_mlinks, padded * sizeof(uint32_t)));
+        MLB_CUDA(pool_alloc(&p->d_cls, padded * sizeof(uint32_t)));
+        MLB_CUDA(pool_alloc(&p->d_mlinks, padded * sizeof(uint32_t)));
         MLB_CUDA(cudaMemset(d_esc, 0, sizeof(unsigned int)));
         mlb::build_kind_kernel<<<grid, 128>>>(p->d_flags, p->g, p->d_tab, p->d_kind, d_esc,
                                               p->d_cls, p->d_mlinks);
         MLB_LAUNCHED();
         MLB_CUDA(cudaMemcpy(&p->n_escape, d_esc, sizeof(unsigned int), cudaMemcpyDeviceToHost));
     }
-    cudaFree(d_esc);
+    pool_free(d_esc);
     unsigned long long tab[256];
     MLB_CUDA(cudaMemcpy(tab, p->d_tab, sizeof(tab), cudaMemcpyDeviceToHost));
     p->n_kinds = 0;
     for (int k = 0; k < 255; ++k)
         p->n_kinds += tab[k] != mlb::KIND_EMPTY;
-    cudaFree(p->d_flags);  // only the build reads the raw flag block
+    pool_free(p->d_flags);  // only the build reads the raw flag block
     p->d_flags = nullptr;
     p->have_flags = true;
     return MLB_OK;
@@ -1364,7 +1443,7 @@ int mlb_signal_create(int device, void **d_sig)
 {
     if (!d_sig) return fail(MLB_EINVAL, "NULL argument");
     MLB_CUDA(cudaSetDevice(device));
-    MLB_CUDA(cudaMalloc(d_sig, MLB_SIGNAL_BYTES));
+    MLB_CUDA(g_pool.alloc(d_sig, MLB_SIGNAL_BYTES));
     MLB_CUDA(cudaMemset(*d_sig, 0, MLB_SIGNAL_BYTES));
     MLB_CUDA(cudaDeviceSynchronize());
     return MLB_OK;
@@ -1372,7 +1451,7 @@ int mlb_signal_create(int device, void **d_sig)
 
 int mlb_signal_destroy(void *d_sig)
 {
-    if (d_sig) MLB_CUDA(cudaFree(d_sig));
+    pool_free(d_sig);
     return MLB_OK;
 }
 
@@ -1400,6 +1479,12 @@ int mlb_signal_wait(const void *d_slot, uint32_t value, int mode, void *stream)
     signal_wait_kernel<<<1, 1, 0, S(stream)>>>(static_cast<const volatile unsigned int *>(d_slot),
                                                  value);
     MLB_LAUNCHED();
+    return MLB_OK;
+}
+
+int mlb_trim(void)
+{
+    g_pool.trim();
     return MLB_OK;
 }
 
