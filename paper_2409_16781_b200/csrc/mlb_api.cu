@@ -721,6 +721,9 @@ int mlb_plan_destroy(mlb_plan *p)
     if (!p)
         return MLB_OK;
     cudaSetDevice(p->device);
+    // cudaFree used to wait for work still using the tables; a pooled block can be
+    // handed to the next plan at once, so wait here
+    cudaDeviceSynchronize();
     pool_free(p->d_flags); pool_free(p->d_cls); pool_free(p->d_mlinks); pool_free(p->d_in);
     pool_free(p->d_kind); pool_free(p->d_tab);
     pool_free(p->d_out); pool_free(p->d_out_tmp); pool_free(p->d_partials); pool_free(p->d_diag);
@@ -803,6 +806,8 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     const uint8_t *src_lo = h_lo ? h_lo : h_flags + (size_t)(nz - 1) * dense_plane;
     const uint8_t *src_hi = h_hi ? h_hi : h_flags;
 
+    if (p->have_flags)
+        MLB_CUDA(cudaDeviceSynchronize());   // earlier launches may still read the old tables
     pool_free(p->d_flags); pool_free(p->d_cls); pool_free(p->d_mlinks); pool_free(p->d_in);
     pool_free(p->d_kind); pool_free(p->d_tab);
     pool_free(p->d_out); pool_free(p->d_out_tmp);
@@ -1451,6 +1456,7 @@ int mlb_signal_create(int device, void **d_sig)
 
 int mlb_signal_destroy(void *d_sig)
 {
+    if (d_sig) MLB_CUDA(cudaDeviceSynchronize());
     pool_free(d_sig);
     return MLB_OK;
 }
