@@ -87,7 +87,9 @@ int mlb_plan_set_physics(mlb_plan *plan, double omega, const double wall_u[3],
 /* kernel variant used by mlb_step (tuning knob, never changes bits): 0 =
  * default; 32..512 = one cell per thread with that block width; W*1000 + LX
  * = packs of consecutive cells, LX = 8 / 16 / 32 packs per warp row, W = 1:
- * 16-byte packs (fp32 / fp64), W = 2 / 3: 8- / 4-byte packs (fp16 storage) */
+ * 16-byte packs (fp32 / fp64), W = 2: 8-byte packs (fp32: two cells, for even
+ * rows that 4 does not divide; fp16 storage: four cells; mixed2: two cells),
+ * W = 3: 4-byte packs (fp16 storage) */
 int mlb_plan_set_variant(mlb_plan *plan, int variant);
 /* name of the fused kernel mlb_step will launch for this plan (for reports) */
 const char *mlb_plan_kernel_name(const mlb_plan *plan);

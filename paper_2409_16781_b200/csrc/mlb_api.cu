@@ -278,6 +278,8 @@ bool variant_exists(int dtype, int variant)
         return w == 2 || w == 3;
     if (dtype == MLB_F32C64)
         return w == 2;   // 8-byte packs: two floats, two doubles' worth of registers per population
+    if (dtype == MLB_F32)
+        return w == 1 || w == 2;   // 16-byte packs, or 8-byte packs (even rows that 4 does not divide)
     return w == 1;
 }
 
@@ -289,6 +291,8 @@ int resolve_variant(const mlb_plan *p)
         return p->variant;
     if (p->dtype == MLB_F32 && p->nx % 4 == 0 && p->nx >= 128)
         return 1016;
+    if (p->dtype == MLB_F32 && p->nx % 2 == 0 && p->nx >= 128)
+        return 2016;
     if (p->dtype == MLB_F16 && p->nx % 4 == 0 && p->nx >= 128)
         return 2008;
     // fp64: the scalar kernel is ~2 % faster, unless there are open-boundary
@@ -405,8 +409,11 @@ int launch_typed(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cud
     if (PUSH)
         fill_push<TS>(p, *push, ph);
     const int lx = variant % 1000, n = z1 - z0;
-    if (variant >= 3000) return launch_vec<TS, V2, PUSH>(p, a, ph, lx, n, st);
-    if (variant >= 1000) return launch_vec<TS, V1, PUSH>(p, a, ph, lx, n, st);
+    if (variant >= 1000) {
+        // the pack width the variant means for this dtype: one of the two built
+        if (pack_cells(p->dtype, variant) == V1) return launch_vec<TS, V1, PUSH>(p, a, ph, lx, n, st);
+        return launch_vec<TS, V2, PUSH>(p, a, ph, lx, n, st);
+    }
     return launch_scalar<TS, PUSH>(p, a, ph, variant, n, st);
 }
 
@@ -420,8 +427,8 @@ int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cuda
     // pack widths per dtype: W = 1 -> 16-byte packs (fp32 / fp64); fp16 storage
     // has W = 2 (4 halves) and W = 3 (2 halves)
     if (p->dtype == MLB_F32)
-        return push ? launch_typed<float, 4, 4, true>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push)
-                    : launch_typed<float, 4, 4, false>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push);
+        return push ? launch_typed<float, 4, 2, true>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push)
+                    : launch_typed<float, 4, 2, false>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push);
     if (p->dtype == MLB_F64)
         return push ? launch_typed<double, 2, 2, true>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push)
                     : launch_typed<double, 2, 2, false>(p, fpre, fpost, z0, z1, st, fuse_open, variant, push);
@@ -532,6 +539,7 @@ int resolve_aa_variant(const mlb_plan *p)
     if (p->variant != 0)
         return p->variant;
     if (p->dtype == MLB_F32 && p->nx % 4 == 0 && p->nx >= 128) return 1016;
+    if (p->dtype == MLB_F32 && p->nx % 2 == 0 && p->nx >= 128) return 2016;
     if (p->dtype == MLB_F64 && p->nx % 2 == 0 && p->nx >= 128) return 1016;
     if (p->dtype == MLB_F16 && p->nx % 4 == 0 && p->nx >= 128) return 2016;
     if (p->dtype == MLB_F32C64 && p->nx % 2 == 0 && p->nx >= 128) return 2016;
@@ -571,9 +579,12 @@ int launch_aa_any(mlb_plan *p, void *f, int kind, cudaStream_t st, const AaRange
                     p->dtype);
     const bool vec = kind != 2 && aa_uses_packs(p, variant);
     const int lx = variant % 1000;
-    if (p->dtype == MLB_F32)
+    if (p->dtype == MLB_F32) {
+        if (vec && pack_cells(p->dtype, variant) == 2)
+            return launch_aa_vec_lx<float, 2>(p, f, kind, lx, r, st);
         return vec ? launch_aa_vec_lx<float, 4>(p, f, kind, lx, r, st)
                    : launch_aa<float>(p, f, kind, r, st);
+    }
     if (p->dtype == MLB_F64)
         return vec ? launch_aa_vec_lx<double, 2>(p, f, kind, lx, r, st)
                    : launch_aa<double>(p, f, kind, r, st);

@@ -664,6 +664,12 @@ template <> struct PackIO<float, 4> {
     static __device__ __forceinline__ void store(float *p, const float (&o)[4])
     { *reinterpret_cast<float4 *>(p) = make_float4(o[0], o[1], o[2], o[3]); }
 };
+template <> struct PackIO<float, 2> {   // 8-byte packs: rows whose length is even but not a multiple of 4
+    static __device__ __forceinline__ void load(const float *p, float (&o)[2])
+    { const float2 v = *reinterpret_cast<const float2 *>(p); o[0] = v.x; o[1] = v.y; }
+    static __device__ __forceinline__ void store(float *p, const float (&o)[2])
+    { *reinterpret_cast<float2 *>(p) = make_float2(o[0], o[1]); }
+};
 template <> struct PackIO<double, 2> {
     static __device__ __forceinline__ void load(const double *p, double (&o)[2])
     { const double2 v = *reinterpret_cast<const double2 *>(p); o[0] = v.x; o[1] = v.y; }

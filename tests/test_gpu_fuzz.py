@@ -25,7 +25,7 @@ pytestmark = pytest.mark.gpu
 PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED1,
         "m2": Precision.MIXED2}
 SCALAR = [32, 64, 128, 256]
-PACKS = {"f32": [1008, 1016, 1032], "f64": [1008, 1016, 1032],
+PACKS = {"f32": [1008, 1016, 1032, 2008, 2016, 2032], "f64": [1008, 1016, 1032],
          "f16": [2008, 2016, 2032, 3008, 3016, 3032], "m2": [2008, 2016, 2032]}
 
 

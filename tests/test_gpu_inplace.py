@@ -51,7 +51,7 @@ def test_inplace_equals_oracle_bitwise(geom, tag, steps, rng):
     np.testing.assert_array_equal(got, want)
 
 
-PACK_VARIANTS = {"f32": [1008, 1016, 1032], "f64": [1008, 1016, 1032],
+PACK_VARIANTS = {"f32": [1008, 1016, 1032, 2008, 2016], "f64": [1008, 1016, 1032],
                  "f16": [2008, 2016, 2032, 3008, 3016, 3032], "m2": [2008, 2016, 2032]}
 
 

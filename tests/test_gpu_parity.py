@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED1,
         "m2": Precision.MIXED2}
-VARIANTS = {"f32": [32, 64, 128, 256, 512, 1008, 1016, 1032],
+VARIANTS = {"f32": [32, 64, 128, 256, 512, 1008, 1016, 1032, 2008, 2016, 2032],
             "f64": [32, 64, 128, 256, 512, 1008, 1016, 1032],
             "f16": [32, 128, 512, 2008, 2016, 2032, 3008, 3016, 3032],
             "m2": [32, 128, 512, 2008, 2016, 2032]}
@@ -142,6 +142,35 @@ def test_kernel_variants_never_change_bits(geom, tag, variant, passthrough, rng)
     newest, _, _ = plan.run_steps(da, db, steps)
     got = np.empty_like(f)
     plan.download(newest, got)
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("tag,variant", [("f32", 2008), ("f32", 2016), ("f64", 1008), ("m2", 2032),
+                                         ("f16", 3016)])
+def test_two_cell_packs_on_rows_that_four_does_not_divide(tag, variant, rng):
+    """nx = 14: even, not a multiple of 4 - the 8-byte (fp32, mixed2), 16-byte
+    (fp64) and 4-byte (fp16) packs of two cells serve it, two blocks and in
+    place, inlet / outlet cells included."""
+    grid, wall_u, inlet_u = geometries3d()["channel"]
+    assert grid.shape[0] % 4 == 2
+    prec = PREC[tag]
+    f = random_block(rng, grid.size, prec.storage)
+    want = make_oracle(grid, 1.7, wall_u, inlet_u, prec).run(f.copy(), f.copy(), 5)
+    plan = make_plan(grid, prec, 1.7, wall_u, inlet_u)
+    plan.set_variant(variant)
+    plan.set_passthrough(True)
+    a, b = plan.alloc(), plan.alloc()
+    plan.upload(f, a)
+    plan.upload(f, b)
+    newest, _, _ = plan.run_steps(a, b, 5)
+    got = np.empty_like(f)
+    plan.download(newest, got)
+    np.testing.assert_array_equal(got, want)
+    c = plan.alloc()
+    plan.upload(f, c)
+    plan.run_steps_inplace(c, 5)
+    plan.normalize(c)
+    plan.download(c, got)
     np.testing.assert_array_equal(got, want)
 
 
