@@ -373,7 +373,9 @@ int launch_vec(mlb_plan *p, const mlb::StepArgs<TS> &a, const mlb::PushArgs<TS> 
     if (p->nx % V != 0)
         return fail(MLB_EINVAL, "this vectorised kernel needs nx %% %d == 0", V);
     const int rows = 128 / lx;  // rows per 128-thread block
-    const dim3 grid((p->nx / V + lx - 1) / lx, (p->ny + rows - 1) / rows, nplanes);
+    // pass-through launches cover the padded row (see step_vec_kernel)
+    const long long cols = a.passthrough ? p->lay.xp : p->nx;
+    const dim3 grid((unsigned)((cols / V + lx - 1) / lx), (p->ny + rows - 1) / rows, nplanes);
     if (lx == 8) mlb::step_vec_kernel<TS, V, 8, PUSH><<<grid, 128, 0, st>>>(a, ph);
     else if (lx == 16) mlb::step_vec_kernel<TS, V, 16, PUSH><<<grid, 128, 0, st>>>(a, ph);
     else mlb::step_vec_kernel<TS, V, 32, PUSH><<<grid, 128, 0, st>>>(a, ph);
@@ -387,7 +389,8 @@ int launch_scalar(mlb_plan *p, const mlb::StepArgs<TS> &a, const mlb::PushArgs<T
 {
     while (bx > 32 && bx / 2 >= p->nx)
         bx /= 2;
-    const dim3 grid((p->nx + bx - 1) / bx, p->ny, nplanes);
+    const long long cols = a.passthrough ? p->lay.xp : p->nx;   // pass-through covers the padded row
+    const dim3 grid((unsigned)((cols + bx - 1) / bx), p->ny, nplanes);
     switch (bx) {
     case 32: mlb::step_kernel<TS, 32, PUSH><<<grid, 32, 0, st>>>(a, ph); break;
     case 64: mlb::step_kernel<TS, 64, PUSH><<<grid, 64, 0, st>>>(a, ph); break;
@@ -500,7 +503,9 @@ int launch_aa_vec(mlb_plan *p, void *f, int kind, const AaRange &r, cudaStream_t
     fill_aa<TS>(p, f, r, a);
     const int rows = 128 / LX;
     const int n = (r.z1 < 0 ? p->nz : r.z1) - r.z0;
-    const dim3 grid((p->nx / V + LX - 1) / LX, (p->ny + rows - 1) / rows, n);
+    // the local half covers the padded row (it rewrites the padding: whole last lines)
+    const long long cols = kind == 1 ? p->lay.xp : p->nx;
+    const dim3 grid((unsigned)((cols / V + LX - 1) / LX), (p->ny + rows - 1) / rows, n);
     const bool remote = r.below || r.above;
     if (kind == 0) {
         // pull half: results for crossing directions go into the neighbours' planes

@@ -403,7 +403,8 @@ template <typename TS, int BX, bool PUSH>
 __global__ void __launch_bounds__(BX) step_kernel(const StepArgs<TS> a, const PushArgs<TS> ph)
 {
     const int x = blockIdx.x * BX + threadIdx.x;
-    if (x >= a.g.nx)
+    // pass-through mode also rewrites the row padding: whole last lines (see step_vec_kernel)
+    if (x >= (a.passthrough ? (int)a.g.xp : a.g.nx))
         return;
     step_cell<TS, PUSH>(a, ph, x, blockIdx.y, a.z0 + blockIdx.z);
 }
@@ -757,10 +758,14 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
     const int x0 = (blockIdx.x * LX + (lane % LX)) * V;
     const int y = blockIdx.y * (4 * RPW) + warp * RPW + lane / LX;
     const int lz = a.z0 + blockIdx.z;
-    if (x0 >= gm.nx || y >= gm.ny)
+    const int xp = (int)gm.xp, plane = (int)gm.plane;
+    // Pass-through mode also rewrites the row padding (kind 1: "solid", holds
+    // whatever the block was allocated with, read by nobody): the last line of a
+    // row whose length is not a multiple of 128 bytes is then stored whole instead
+    // of leaving a partial sector for L2 to complete with a DRAM read.
+    if (x0 >= (a.passthrough ? xp : gm.nx) || y >= gm.ny)
         return;
 
-    const int xp = (int)gm.xp, plane = (int)gm.plane;
     const int zc = (lz + 1) * plane;
     const int zm = ((lz == 0) ? gm.zlo_src : lz) * plane;
     const int zq = ((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) * plane;
@@ -1153,7 +1158,8 @@ __global__ void __launch_bounds__(128, 4) aa_local_vec_kernel(const AAArgs<TS> a
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int x0 = (blockIdx.x * LX + (lane % LX)) * V;
     const int y = blockIdx.y * (4 * RPW) + warp * RPW + lane / LX;
-    if (x0 >= gm.nx || y >= gm.ny)
+    // the row padding is rewritten too (always valid in place): whole last lines
+    if (x0 >= (int)gm.xp || y >= gm.ny)
         return;
     const int lz = a.z0 + (int)blockIdx.z;
     const int d = (lz + 1) * (int)gm.plane + y * (int)gm.xp + x0;
