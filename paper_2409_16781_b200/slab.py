@@ -100,7 +100,8 @@ class CudaStepper:
 class PeerRing:
     """The ring neighbours' blocks and step counters, mapped into this process.
 
-    `blocks` are this rank's two population blocks (DeviceFields of `plan`);
+    `blocks` are this rank's population blocks (DeviceFields of `plan`): two
+    for the two-buffer update, one for the in-place update;
     every rank passes its own and learns the others' through one object
     all-gather of CUDA IPC handles (64 bytes each) - control plane only.
     With world == 1 the ring closes on the rank's own blocks.
@@ -171,7 +172,7 @@ class PeerRing:
         for k, b in enumerate(self.blocks):
             if b is block:
                 return k
-        raise ValueError("block is not one of the ring's two population blocks")
+        raise ValueError("block is not one of the ring's population blocks")
 
     def targets(self, k):
         """((below ptr, nz), (above ptr, nz)) for pushes out of local block k."""
