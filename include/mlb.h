@@ -104,6 +104,13 @@ const char *mlb_plan_kernel_name(const mlb_plan *plan);
  * is itself an outlet cell: there the reference's result depends on the
  * stale content of the never-written cell. */
 int mlb_plan_set_passthrough(mlb_plan *plan, int on);
+/* L2 prefetch distance of the pack kernels (two-buffer and in-place), in cells
+ * of launch order: while a block's own pulls are in flight, one lane per
+ * 128-byte line issues `prefetch.global.L2` for the lines that the cells this
+ * far ahead will read.  No result depends on it (the reference has no
+ * counterpart; it replaces the cache blocking of kernels.py:258-279 tiles).
+ * -1 = auto (default: the cells whose populations make ~10 MB), 0 = off. */
+int mlb_plan_set_prefetch(mlb_plan *plan, long long cells);
 
 /* Flags: the reference's `mask` argument (kernels.py:408, a (N,) uint8 array
  * in cell order).  h_flags is dense [nz][ny][nx] HOST memory.  h_halo_lo /

@@ -25,6 +25,7 @@ SYMBOLS = (
     "mlb_last_error", "mlb_abi_version", "mlb_launch_count", "mlb_trim", "mlb_layout_query",
     "mlb_plan_create", "mlb_plan_destroy", "mlb_plan_get_layout",
     "mlb_plan_set_physics", "mlb_plan_set_variant", "mlb_plan_set_passthrough",
+    "mlb_plan_set_prefetch",
     "mlb_plan_kernel_name", "mlb_plan_set_flags",
     "mlb_plan_get_flags", "mlb_plan_geometry_stats", "mlb_upload", "mlb_download", "mlb_step",
     "mlb_step_range", "mlb_step_open_range", "mlb_open_pass", "mlb_open_pass_range",
@@ -74,6 +75,7 @@ def lib():
         "mlb_plan_set_physics": (i, [vp, d, dp3, d]),
         "mlb_plan_set_variant": (i, [vp, i]),
         "mlb_plan_set_passthrough": (i, [vp, i]),
+        "mlb_plan_set_prefetch": (i, [vp, ctypes.c_longlong]),
         "mlb_plan_kernel_name": (ctypes.c_char_p, [vp]),
         "mlb_plan_set_flags": (i, [vp, vp, vp, vp]),
         "mlb_plan_get_flags": (i, [vp, vp]),

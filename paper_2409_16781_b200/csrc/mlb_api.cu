@@ -129,6 +129,7 @@ inline void pool_free(void *p) { g_pool.release(p); }
 struct mlb_plan {
     int nx = 0, ny = 0, nz = 0, dtype = 0, device = 0, z_mode = 0, variant = 0;
     int passthrough = 0;
+    long long prefetch = -1;  // L2 prefetch distance in cells, -1 = auto (prefetch_distance)
     double omega = 1.0, wall_u[3] = {0, 0, 0}, inlet_u = 0.0;
     mlb_layout lay{};
     mlb::Geom g{};
@@ -321,6 +322,20 @@ bool can_fuse_open(const mlb_plan *p, int variant)
     return true;
 }
 
+// how far ahead the pack kernels prefetch into L2 (prefetch_ahead), as planes + rows
+// (mlb_plan_set_prefetch).  Auto = the cells whose 19 populations make ~10 MB:
+// measured on B200 at 512^3 and 256^3 the optimum sits at that many BYTES for
+// every storage type (fp32 128 Ki cells, fp64 64 Ki, fp16 192-256 Ki); twice as
+// far is already slower than no prefetch (the prefetched lines plus the dirty
+// lines of the stores outgrow the L2 share they can hold on to).
+void prefetch_distance(const mlb_plan *p, int &dz, int &dy)
+{
+    const long long cells = p->prefetch >= 0 ? p->prefetch : (512ll << 10) / p->lay.itemsize;
+    const long long rows = cells / p->nx;
+    dz = (int)(rows / p->ny);
+    dy = (int)(rows % p->ny);
+}
+
 template <typename TS>
 void fill_args(mlb_plan *p, const void *fpre, void *fpost, int z0, bool fuse_open,
                mlb::StepArgs<TS> &a)
@@ -335,6 +350,7 @@ void fill_args(mlb_plan *p, const void *fpre, void *fpost, int z0, bool fuse_ope
     a.z0 = z0;
     a.passthrough = p->passthrough;
     a.fuse_open = fuse_open ? 1 : 0;
+    prefetch_distance(p, a.pf_dz, a.pf_dy);
     T cv[MLB_Q];
     inlet_values<T>(p->inlet_u, cv);  // compute dtype, then storage dtype (engine.py:167-171)
     for (int q = 0; q < MLB_Q; ++q)
@@ -466,6 +482,7 @@ void fill_aa(mlb_plan *p, void *f, const AaRange &r, mlb::AAArgs<TS> &a)
     for (int q = 0; q < MLB_Q; ++q)
         a.inlet[q] = mlb::Store<TS>::down(cv[q]);
     a.z0 = r.z0;
+    prefetch_distance(p, a.pf_dz, a.pf_dy);
     const long long plane = p->lay.plane;
     for (int j = 0; j < 5; ++j) {
         // slab below: its top plane lz = nz_below-1 (storage nz_below), c_z = +1 populations
@@ -805,6 +822,16 @@ int mlb_plan_set_passthrough(mlb_plan *p, int on)
                     "that cell's STALE value in fpost (numpy evaluates the right-hand side "
                     "first, engine.py:179-180), which pass-through would refresh");
     p->passthrough = on ? 1 : 0;
+    return MLB_OK;
+}
+
+int mlb_plan_set_prefetch(mlb_plan *p, long long cells)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (cells < -1)
+        return fail(MLB_EINVAL, "prefetch distance %lld: must be -1 (auto), 0 (off) or a number "
+                    "of cells", cells);
+    p->prefetch = cells;
     return MLB_OK;
 }
 

@@ -108,6 +108,8 @@ struct StepArgs {
     int passthrough;  // 1: non-fluid cells are rewritten with fpre's value (see step_cell)
     int fuse_open;    // 1 (pack kernels, pass-through only): apply the open-boundary pass
                       // (engine.py:156-180) to the cells of the pack before storing
+    int pf_dz, pf_dy; // pack kernels: L2-prefetch the lines of the cells pf_dz planes + pf_dy
+                      // rows ahead (both 0 = off), see prefetch_ahead
     TS inlet[Q];      // equilibrium(1, u_in, 0, 0), storage dtype
     T omega;
     T k[Q];        // moving-wall terms 6 w_i (c_i . u_w), compute dtype
@@ -442,6 +444,7 @@ struct AAArgs {
     T k[Q];
     TS inlet[Q];  // equilibrium(1, u_in, 0, 0), storage dtype (open boundaries, pack kernels)
     int z0;       // first slab plane this launch updates (blockIdx.z = 0)
+    int pf_dz, pf_dy;  // L2 prefetch distance of the pack kernels (prefetch_ahead)
     // z-slabs (REMOTE kernels): the pull half writes each result into the location
     // it was pulled from - and for a boundary plane's crossing directions that
     // location belongs to the ring neighbour.  It is READ from the local halo plane
@@ -739,6 +742,11 @@ __device__ __forceinline__ void pull_pack(const TS *__restrict__ row, int x0, in
     }
 }
 
+__device__ __forceinline__ void l2_prefetch(const void *p)
+{
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // direction table: X(i, c_x, plane offset, row offset)
 #define MLB_DIRS(X)                                                              \
     X(1, 1, zc, rc)   X(2, 0, zc, rm)   X(3, -1, zc, rc)  X(4, 0, zc, rq)        \
@@ -746,6 +754,36 @@ __device__ __forceinline__ void pull_pack(const TS *__restrict__ row, int x0, in
     X(9, 0, zm, rc)   X(10, 0, zq, rc)  X(11, 1, zm, rc)  X(12, -1, zm, rc)      \
     X(13, -1, zq, rc) X(14, 1, zq, rc)  X(15, 0, zm, rm)  X(16, 0, zm, rq)       \
     X(17, 0, zq, rq)  X(18, 0, zq, rm)
+
+// L2 prefetch, one lane per 128-byte line: the lines that the cells `dz` planes
+// and `dy` rows further on in launch order (about one wave of resident blocks
+// later) will pull (PULL) or find in their own slots (!PULL: the local half of
+// the in-place update).  Every value is read exactly once, so this moves no
+// extra bytes; it turns that block's DRAM round trip into an L2 hit without
+// holding registers for it.  Distances much beyond one wave lose: the
+// prefetched lines and the dirty lines of the stores then outgrow L2.
+template <typename TS, int V, int LX, bool PULL, typename PTR>
+__device__ __forceinline__ void prefetch_ahead(PTR const (&base)[Q], const Geom &gm, int dz,
+                                               int dy, int x0, int y, int lz, int lane)
+{
+    if ((dz | dy) == 0)
+        return;
+    constexpr int LPL = 128 / (V * (int)sizeof(TS));   // lanes per line
+    int yp = y + dy, lp = lz + dz;
+    if (yp >= gm.ny) { yp -= gm.ny; ++lp; }
+    if ((lane % LX) % LPL != 0 || lp >= gm.nz)
+        return;
+    const int xp = (int)gm.xp, plane = (int)gm.plane;
+    const int rc = yp * xp, rm = (yp == 0 ? gm.ny - 1 : yp - 1) * xp,
+              rq = (yp == gm.ny - 1 ? 0 : yp + 1) * xp;
+    const int zc = (lp + 1) * plane + x0;
+    const int zm = PULL ? ((lp == 0) ? gm.zlo_src : lp) * plane + x0 : zc;
+    const int zq = PULL ? ((lp == gm.nz - 1) ? gm.zhi_src : lp + 2) * plane + x0 : zc;
+    l2_prefetch(base[0] + (zc + rc));
+#define MLB_X(i, CX, Z, R) l2_prefetch(base[i] + ((Z) + (PULL ? (R) : rc)));
+    MLB_DIRS(MLB_X)
+#undef MLB_X
+}
 
 template <typename TS, int V, int LX, bool PUSH>
 __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
@@ -783,6 +821,8 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
 #define MLB_X(i, CX, Z, R) pull_pack<TS, V, CX>(a.pre[i] + ((Z) + (R)), x0, xl, xr, g[i]);
     MLB_DIRS(MLB_X)
 #undef MLB_X
+
+    prefetch_ahead<TS, V, LX, true>(a.pre, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
 
     // class words: all zero for a pack of bulk cells (the usual case), else from
     // the dictionary.  (A separate code path for bulk packs was measured and is
@@ -969,6 +1009,7 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
 #define MLB_X(i, CX, Z, R) pull_pack<TS, V, CX>(a.f[i] + ((Z) + (R)), x0, xl, xr, g[i]);
     MLB_DIRS(MLB_X)
 #undef MLB_X
+    prefetch_ahead<TS, V, LX, true>(a.f, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
 
     const bool bulk = valid && kpack == 0u;
     const bool bulk_r = __shfl_down_sync(FULL, (int)bulk, 1) != 0 && seg != LX - 1
@@ -1169,6 +1210,7 @@ __global__ void __launch_bounds__(128, 4) aa_local_vec_kernel(const AAArgs<TS> a
 #pragma unroll
     for (int i = 0; i < Q; ++i)
         PackIO<TS, V>::load(a.f[opp(i)] + d, g[i]);
+    prefetch_ahead<TS, V, LX, false>(a.f, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
     uint32_t c[V];
 #pragma unroll
     for (int j = 0; j < V; ++j)

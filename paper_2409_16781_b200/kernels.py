@@ -242,6 +242,11 @@ class KernelPlan:
         self.passthrough = bool(on)
         _cabi.check(self._lib.mlb_plan_set_passthrough(self._plan, int(self.passthrough)))
 
+    def set_prefetch(self, cells):
+        """L2 prefetch distance of the pack kernels in cells (-1 auto, 0 off);
+        a performance knob only - results never depend on it (include/mlb.h)."""
+        _cabi.check(self._lib.mlb_plan_set_prefetch(self._plan, int(cells)))
+
     # -- host <-> device ---------------------------------------------------
     def _check_host(self, a):
         n = self.nx * self.ny * self.nz

@@ -145,6 +145,46 @@ def test_kernel_variants_never_change_bits(geom, tag, variant, passthrough, rng)
     np.testing.assert_array_equal(got, want)
 
 
+@pytest.mark.parametrize("cells", [0, 5, "row+1", "plane", "2planes+3rows", 10 ** 9, -1])
+@pytest.mark.parametrize("tag", ["f32", "f64", "f16", "m2"])
+@pytest.mark.parametrize("geom", ["cavity16", "channel40", "periodic8", "wide"])
+def test_prefetch_distance_never_changes_bits(geom, tag, cells, rng):
+    """The L2 prefetch of the pack kernels (mlb_plan_set_prefetch) is a pure
+    performance knob like the reference's tile shape (test_kernels.py:107-126):
+    any distance - off, inside a row, across rows and planes, beyond the
+    domain, auto - same bits as the oracle, two blocks and in place."""
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    nx, ny = grid.shape[0], grid.shape[1]
+    cells = {"row+1": nx + 1, "plane": nx * ny, "2planes+3rows": 2 * nx * ny + 3 * nx}.get(cells, cells)
+    prec = PREC[tag]
+    f = random_block(rng, grid.size, prec.storage)
+    want = make_oracle(grid, 1.6, wall_u, inlet_u, prec).run(f.copy(), f.copy(), 4)
+    plan = make_plan(grid, prec, 1.6, wall_u, inlet_u)
+    plan.set_variant({"f32": 1016, "f64": 1016, "f16": 2008, "m2": 2016}[tag])
+    plan.set_prefetch(cells)
+    plan.set_passthrough(True)
+    a, b = plan.alloc(), plan.alloc()
+    plan.upload(f, a)
+    plan.upload(f, b)
+    newest, _, _ = plan.run_steps(a, b, 4)
+    got = np.empty_like(f)
+    plan.download(newest, got)
+    np.testing.assert_array_equal(got, want)
+    c = plan.alloc()
+    plan.upload(f, c)
+    plan.run_steps_inplace(c, 4)
+    plan.normalize(c)
+    plan.download(c, got)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_prefetch_distance_is_validated():
+    grid, wall_u, inlet_u = geometries3d()["cavity16"]
+    plan = make_plan(grid, Precision.SINGLE, 1.0, wall_u, inlet_u)
+    with pytest.raises(ValueError, match="prefetch"):
+        plan.set_prefetch(-2)
+
+
 @pytest.mark.parametrize("tag,variant", [("f32", 2008), ("f32", 2016), ("f64", 1008), ("m2", 2032),
                                          ("f16", 3016)])
 def test_two_cell_packs_on_rows_that_four_does_not_divide(tag, variant, rng):

@@ -18,6 +18,8 @@ for prec in (Precision.SINGLE, Precision.DOUBLE, Precision.MIXED1, Precision.MIX
         if os.environ.get("MLB_VARIANT"):
             v = int(os.environ["MLB_VARIANT"])
             plan.set_variant(v if prec in (Precision.SINGLE, Precision.DOUBLE) else v + 1000)
+        if os.environ.get("MLB_PREFETCH"):
+            plan.set_prefetch(int(os.environ["MLB_PREFETCH"]))
         a = plan.alloc()
         for q in range(19):
             a.tensor[q].fill_(float(W[q]))
