@@ -152,6 +152,7 @@ struct PushArgs {
 template <typename L> struct Alg;
 template <> struct Alg<float> {
     using S = float;
+    static constexpr bool packed = false;
     static __device__ __forceinline__ float cst(float v) { return v; }
     static __device__ __forceinline__ float add(float a, float b) { return a + b; }
     static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
@@ -162,6 +163,7 @@ template <> struct Alg<float> {
 };
 template <> struct Alg<double> {
     using S = double;
+    static constexpr bool packed = false;
     static __device__ __forceinline__ double cst(double v) { return v; }
     static __device__ __forceinline__ double add(double a, double b) { return a + b; }
     static __device__ __forceinline__ double sub(double a, double b) { return a - b; }
@@ -172,6 +174,11 @@ template <> struct Alg<double> {
 };
 template <> struct Alg<float2> {
     using S = float;
+#ifdef MLB_SCALAR_SUMS   // A/B builds only: every sum that consumes a product per element
+    static constexpr bool packed = false;
+#else
+    static constexpr bool packed = true;
+#endif
     static __device__ __forceinline__ float2 cst(float v) { return make_float2(v, v); }
     static __device__ __forceinline__ float2 add(float2 a, float2 b) { return __fadd2_rn(a, b); }
     static __device__ __forceinline__ float2 sub(float2 a, float2 b)
@@ -183,10 +190,19 @@ template <> struct Alg<float2> {
     // skips the product's rounding (found as a 1-half-ulp parity failure, once
     // in ~20 000 values).  Scalar adds are not contracted (-fmad=false holds
     // for them), so sums that consume a product are done per element.
+    // The DIFFERENCE a - m is safe as FFMA2(m, -1, a) (exact product, one
+    // rounding; ptxas leaves that form alone - FFMA2(m, +1, a) it rewrites to
+    // an add and then contracts).  So the packed collide turns its sums of
+    // products into differences of the exactly negated product (a + c*x =
+    // a - (-c)*x, same bits: rounding to nearest is symmetric), see collide.
     static __device__ __forceinline__ float2 addm(float2 a, float2 m)
     { return make_float2(a.x + m.x, a.y + m.y); }
     static __device__ __forceinline__ float2 subm(float2 a, float2 m)
+#ifdef MLB_SCALAR_SUMS
     { return make_float2(a.x - m.x, a.y - m.y); }
+#else
+    { return __ffma2_rn(m, make_float2(-1.0f, -1.0f), a); }
+#endif
     static __device__ __forceinline__ float2 rcp0(float2 r)
     { return make_float2(r.x != 0.0f ? 1.0f / r.x : 0.0f, r.y != 0.0f ? 1.0f / r.y : 0.0f); }
 };
@@ -219,17 +235,29 @@ __device__ __forceinline__ void collide(L (&g)[Q], const typename Alg<L>::S omeg
     const L ux = A::mul(mx, inv), uy = A::mul(my, inv), uz = A::mul(mz, inv);
     // (addm / subm: a sum one of whose operands is a product, see Alg<float2>)
     const L usq = A::addm(A::addm(A::mul(ux, ux), A::mul(uy, uy)), A::mul(uz, uz));
-    const L um = A::subm(one, A::mul(c15, usq));
+    // (packed lanes: per element, so that every FFMA2 in the library keeps the one
+    // checkable form (m, -1, a) - ptxas would write this one as (m, -R, 1))
+    L um;
+    if constexpr (A::packed) um = A::addm(one, A::mul(A::cst(S(-1.5)), usq));
+    else um = A::subm(one, A::mul(c15, usq));
     const L wr0 = A::mul(w0, rho), wrs = A::mul(ws, rho), wrd = A::mul(wd, rho);
     const L a = A::add(ux, uy), b = A::sub(ux, uy), c = A::add(ux, uz), d = A::sub(ux, uz),
             h = A::add(uy, uz), kk = A::sub(uy, uz);
 
+    // packed lanes: um + 4.5 cu^2 and p + 3 cu as differences of the negated
+    // products (see Alg<float2>::subm) - same values, bit for bit
+    const L nc3 = A::cst(S(-3.0)), nc45 = A::cst(S(-4.5));
 #define MLB_PAIR(cu, wr, ip, im)                                               \
     {                                                                          \
-        const L q_ = A::mul(c45, A::mul((cu), (cu)));                          \
         const L t_ = A::mul(c3, (cu));                                         \
-        const L p_ = A::addm(um, q_);                                          \
-        const L ep_ = A::mul((wr), A::addm(p_, t_));                           \
+        L p_, ep_;                                                             \
+        if constexpr (A::packed) {                                             \
+            p_ = A::subm(um, A::mul(nc45, A::mul((cu), (cu))));                \
+            ep_ = A::mul((wr), A::subm(p_, A::mul(nc3, (cu))));                \
+        } else {                                                               \
+            p_ = A::addm(um, A::mul(c45, A::mul((cu), (cu))));                 \
+            ep_ = A::mul((wr), A::addm(p_, t_));                               \
+        }                                                                      \
         const L em_ = A::mul((wr), A::subm(p_, t_));                           \
         g[ip] = A::subm(g[ip], A::mul(omega, A::subm(g[ip], ep_)));            \
         g[im] = A::subm(g[im], A::mul(omega, A::subm(g[im], em_)));            \

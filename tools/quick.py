@@ -13,6 +13,8 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 peak = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"]
 mask = B.flatten_mask(B.cavity_mask(n, n, n))
 for prec in (Precision.SINGLE, Precision.DOUBLE, Precision.MIXED1, Precision.MIXED2):
+    if os.environ.get("MLB_PRECS") and prec.token not in os.environ["MLB_PRECS"].split(","):
+        continue
     for mode in ("ab", "inplace"):
         plan = KernelPlan(n, n, n, Layout.ROW, prec, mask, 1.53, (0.1, 0, 0))
         if os.environ.get("MLB_VARIANT"):
