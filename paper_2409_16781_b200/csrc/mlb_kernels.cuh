@@ -144,9 +144,12 @@ struct PushArgs {
 //                   issue slot for two independent round-to-nearest results.
 //                   a - b is FFMA2(b, -1, a): the product is exact, the sum is
 //                   rounded once - bit-identical to the scalar subtraction.
-//                   The 68 sums that consume a product stay scalar (addm / subm
-//                   below: ptxas would contract them), so a cell's 195 unfused
-//                   operations cost ~132 slots instead of 195.
+//                   ptxas contracts a packed multiply followed by a packed ADD
+//                   (see addm below), so the packed collide writes its sums
+//                   of products as differences of the exactly negated product
+//                   (um + 4.5 cu^2 = um - (-4.5) cu^2); only 3 sums per cell
+//                   stay scalar, and a cell's 195 unfused operations cost
+//                   ~100 issue slots instead of 195.
 // Every element of every result is the same correctly rounded value the
 // scalar code (and the CPU oracle) produces.
 template <typename L> struct Alg;
@@ -185,11 +188,11 @@ template <> struct Alg<float2> {
     { return __ffma2_rn(b, make_float2(-1.0f, -1.0f), a); }
     static __device__ __forceinline__ float2 mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
     // a + m / a - m where m is the result of a mul().  ptxas 12.9 contracts a
-    // packed multiply followed by a packed add / subtract into FFMA2 - even
-    // for mul.rn.f32x2 + add.rn.f32x2 in PTX, even with --fmad=false - which
+    // packed multiply followed by a packed add into FFMA2 - even for
+    // mul.rn.f32x2 + add.rn.f32x2 in PTX, even with --fmad=false - which
     // skips the product's rounding (found as a 1-half-ulp parity failure, once
     // in ~20 000 values).  Scalar adds are not contracted (-fmad=false holds
-    // for them), so sums that consume a product are done per element.
+    // for them), so the few true sums of a product are done per element.
     // The DIFFERENCE a - m is safe as FFMA2(m, -1, a) (exact product, one
     // rounding; ptxas leaves that form alone - FFMA2(m, +1, a) it rewrites to
     // an add and then contracts).  So the packed collide turns its sums of
@@ -325,6 +328,49 @@ __host__ __device__ constexpr int opp(int i)
          : (i <= 16 ? i + 2 : i - 2);
 }
 
+__device__ __forceinline__ void l2_prefetch(const void *p)
+{
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// direction table: X(i, c_x, plane offset, row offset)
+#define MLB_DIRS(X)                                                              \
+    X(1, 1, zc, rc)   X(2, 0, zc, rm)   X(3, -1, zc, rc)  X(4, 0, zc, rq)        \
+    X(5, 1, zc, rm)   X(6, -1, zc, rm)  X(7, -1, zc, rq)  X(8, 1, zc, rq)        \
+    X(9, 0, zm, rc)   X(10, 0, zq, rc)  X(11, 1, zm, rc)  X(12, -1, zm, rc)      \
+    X(13, -1, zq, rc) X(14, 1, zq, rc)  X(15, 0, zm, rm)  X(16, 0, zm, rq)       \
+    X(17, 0, zq, rq)  X(18, 0, zq, rm)
+
+// L2 prefetch, one lane per 128-byte line: the lines that the cells `dz` planes
+// and `dy` rows further on in launch order (about one wave of resident blocks
+// later) will pull (PULL) or find in their own slots (!PULL: the local half of
+// the in-place update).  Every value is read exactly once, so this moves no
+// extra bytes; it turns that block's DRAM round trip into an L2 hit without
+// holding registers for it.  Distances much beyond one wave lose: the
+// prefetched lines and the dirty lines of the stores then outgrow L2.
+template <typename TS, int V, int LX, bool PULL, typename PTR>
+__device__ __forceinline__ void prefetch_ahead(PTR const (&base)[Q], const Geom &gm, int dz,
+                                               int dy, int x0, int y, int lz, int lane)
+{
+    if ((dz | dy) == 0)
+        return;
+    constexpr int LPL = 128 / (V * (int)sizeof(TS));   // lanes per line
+    int yp = y + dy, lp = lz + dz;
+    if (yp >= gm.ny) { yp -= gm.ny; ++lp; }
+    if ((lane % LX) % LPL != 0 || lp >= gm.nz)
+        return;
+    const int xp = (int)gm.xp, plane = (int)gm.plane;
+    const int rc = yp * xp, rm = (yp == 0 ? gm.ny - 1 : yp - 1) * xp,
+              rq = (yp == gm.ny - 1 ? 0 : yp + 1) * xp;
+    const int zc = (lp + 1) * plane + x0;
+    const int zm = PULL ? ((lp == 0) ? gm.zlo_src : lp) * plane + x0 : zc;
+    const int zq = PULL ? ((lp == gm.nz - 1) ? gm.zhi_src : lp + 2) * plane + x0 : zc;
+    l2_prefetch(base[0] + (zc + rc));
+#define MLB_X(i, CX, Z, R) l2_prefetch(base[i] + ((Z) + (PULL ? (R) : rc)));
+    MLB_DIRS(MLB_X)
+#undef MLB_X
+}
+
 // ---------------------------------------------------------------------------
 // Fused pull-stream + bounce-back + BGK collide, one thread per cell
 // (kernels.py:76-245 `cell`, :247-279 `fused`).  blockIdx = (x tile, y, plane).
@@ -375,6 +421,7 @@ __device__ __forceinline__ void step_cell(const StepArgs<TS> &a, const PushArgs<
     MLB_PULL(13, zq, rc, dq) MLB_PULL(14, zq, rc, dm) MLB_PULL(15, zm, rm, dc)
     MLB_PULL(16, zm, rq, dc) MLB_PULL(17, zq, rq, dc) MLB_PULL(18, zq, rm, dc)
 #undef MLB_PULL
+    prefetch_ahead<TS, 1, 32, true>(a.pre, gm, a.pf_dz, a.pf_dy, x, y, lz, threadIdx.x & 31);
 
     // Non-fluid destination.  Strict mode: never written (kernels.py:79-80;
     // the stores of the warp then leave 28-of-32-byte sectors at every wall,
@@ -768,49 +815,6 @@ __device__ __forceinline__ void pull_pack(const TS *__restrict__ row, int x0, in
         for (int j = 0; j < V - 1; ++j) o[j] = w[j + 1];
         o[V - 1] = Store<TS>::up(row[xr]);
     }
-}
-
-__device__ __forceinline__ void l2_prefetch(const void *p)
-{
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
-// direction table: X(i, c_x, plane offset, row offset)
-#define MLB_DIRS(X)                                                              \
-    X(1, 1, zc, rc)   X(2, 0, zc, rm)   X(3, -1, zc, rc)  X(4, 0, zc, rq)        \
-    X(5, 1, zc, rm)   X(6, -1, zc, rm)  X(7, -1, zc, rq)  X(8, 1, zc, rq)        \
-    X(9, 0, zm, rc)   X(10, 0, zq, rc)  X(11, 1, zm, rc)  X(12, -1, zm, rc)      \
-    X(13, -1, zq, rc) X(14, 1, zq, rc)  X(15, 0, zm, rm)  X(16, 0, zm, rq)       \
-    X(17, 0, zq, rq)  X(18, 0, zq, rm)
-
-// L2 prefetch, one lane per 128-byte line: the lines that the cells `dz` planes
-// and `dy` rows further on in launch order (about one wave of resident blocks
-// later) will pull (PULL) or find in their own slots (!PULL: the local half of
-// the in-place update).  Every value is read exactly once, so this moves no
-// extra bytes; it turns that block's DRAM round trip into an L2 hit without
-// holding registers for it.  Distances much beyond one wave lose: the
-// prefetched lines and the dirty lines of the stores then outgrow L2.
-template <typename TS, int V, int LX, bool PULL, typename PTR>
-__device__ __forceinline__ void prefetch_ahead(PTR const (&base)[Q], const Geom &gm, int dz,
-                                               int dy, int x0, int y, int lz, int lane)
-{
-    if ((dz | dy) == 0)
-        return;
-    constexpr int LPL = 128 / (V * (int)sizeof(TS));   // lanes per line
-    int yp = y + dy, lp = lz + dz;
-    if (yp >= gm.ny) { yp -= gm.ny; ++lp; }
-    if ((lane % LX) % LPL != 0 || lp >= gm.nz)
-        return;
-    const int xp = (int)gm.xp, plane = (int)gm.plane;
-    const int rc = yp * xp, rm = (yp == 0 ? gm.ny - 1 : yp - 1) * xp,
-              rq = (yp == gm.ny - 1 ? 0 : yp + 1) * xp;
-    const int zc = (lp + 1) * plane + x0;
-    const int zm = PULL ? ((lp == 0) ? gm.zlo_src : lp) * plane + x0 : zc;
-    const int zq = PULL ? ((lp == gm.nz - 1) ? gm.zhi_src : lp + 2) * plane + x0 : zc;
-    l2_prefetch(base[0] + (zc + rc));
-#define MLB_X(i, CX, Z, R) l2_prefetch(base[i] + ((Z) + (PULL ? (R) : rc)));
-    MLB_DIRS(MLB_X)
-#undef MLB_X
 }
 
 template <typename TS, int V, int LX, bool PUSH>
