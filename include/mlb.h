@@ -104,11 +104,13 @@ const char *mlb_plan_kernel_name(const mlb_plan *plan);
  * is itself an outlet cell: there the reference's result depends on the
  * stale content of the never-written cell. */
 int mlb_plan_set_passthrough(mlb_plan *plan, int on);
-/* L2 prefetch distance of the pack kernels (two-buffer and in-place), in cells
- * of launch order: while a block's own pulls are in flight, one lane per
- * 128-byte line issues `prefetch.global.L2` for the lines that the cells this
- * far ahead will read.  No result depends on it (the reference has no
- * counterpart; it replaces the cache blocking of kernels.py:258-279 tiles).
+/* L2 prefetch distance of the step kernels, in cells of launch order: while a
+ * block's own pulls are in flight, it prefetches into L2 what the cells this
+ * far ahead will read - the pack kernels (two-buffer and in-place) with one
+ * `prefetch.global.L2` per 128-byte line, the one-cell-per-thread kernel with
+ * one `cp.async.bulk.prefetch.L2` per population and row.  No result depends
+ * on it (the reference has no counterpart; it takes the place of the cache
+ * blocking of the kernels.py:258-279 tiles).
  * -1 = auto (default: the cells whose populations make ~10 MB), 0 = off. */
 int mlb_plan_set_prefetch(mlb_plan *plan, long long cells);
 

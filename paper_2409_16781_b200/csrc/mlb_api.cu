@@ -336,6 +336,14 @@ void prefetch_distance(const mlb_plan *p, int &dz, int &dy)
     dy = (int)(rows % p->ny);
 }
 
+// pack kernels: one lane per line (0, default) or the bulk form (1; MLB_PF_BULK=1 for
+// A/B runs: measured slower at 512^3 for fp32 / fp16 / mixed2 packs)
+int prefetch_bulk()
+{
+    static const int v = std::getenv("MLB_PF_BULK") ? std::atoi(std::getenv("MLB_PF_BULK")) : 0;
+    return v;
+}
+
 template <typename TS>
 void fill_args(mlb_plan *p, const void *fpre, void *fpost, int z0, bool fuse_open,
                mlb::StepArgs<TS> &a)
@@ -351,6 +359,7 @@ void fill_args(mlb_plan *p, const void *fpre, void *fpost, int z0, bool fuse_ope
     a.passthrough = p->passthrough;
     a.fuse_open = fuse_open ? 1 : 0;
     prefetch_distance(p, a.pf_dz, a.pf_dy);
+    a.pf_bulk = prefetch_bulk();
     T cv[MLB_Q];
     inlet_values<T>(p->inlet_u, cv);  // compute dtype, then storage dtype (engine.py:167-171)
     for (int q = 0; q < MLB_Q; ++q)
@@ -433,6 +442,14 @@ int launch_typed(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cud
         if (pack_cells(p->dtype, variant) == V1) return launch_vec<TS, V1, PUSH>(p, a, ph, lx, n, st);
         return launch_vec<TS, V2, PUSH>(p, a, ph, lx, n, st);
     }
+    // one cell per thread: 19 per-line prefetches per 32 cells cost too many issue
+    // slots there, so these kernels use the bulk form - one instruction per
+    // population and row (measured at 511^3, fraction of the HBM peak: fp32 0.966
+    // without -> 0.982, fp64 1.006 -> 1.014, fp32 storage / fp64 arithmetic 0.837
+    // -> 0.888) - except with fp16 storage, where any prefetch loses (0.62 -> 0.57)
+    a.pf_bulk = 1;
+    if (sizeof(TS) == 2)
+        a.pf_dz = a.pf_dy = 0;
     return launch_scalar<TS, PUSH>(p, a, ph, variant, n, st);
 }
 
@@ -483,6 +500,7 @@ void fill_aa(mlb_plan *p, void *f, const AaRange &r, mlb::AAArgs<TS> &a)
         a.inlet[q] = mlb::Store<TS>::down(cv[q]);
     a.z0 = r.z0;
     prefetch_distance(p, a.pf_dz, a.pf_dy);
+    a.pf_bulk = prefetch_bulk();
     const long long plane = p->lay.plane;
     for (int j = 0; j < 5; ++j) {
         // slab below: its top plane lz = nz_below-1 (storage nz_below), c_z = +1 populations

@@ -110,6 +110,7 @@ struct StepArgs {
                       // (engine.py:156-180) to the cells of the pack before storing
     int pf_dz, pf_dy; // pack kernels: L2-prefetch the lines of the cells pf_dz planes + pf_dy
                       // rows ahead (both 0 = off), see prefetch_ahead
+    int pf_bulk;      // 1: as bulk row prefetches (prefetch_rows), 0: one lane per line
     TS inlet[Q];      // equilibrium(1, u_in, 0, 0), storage dtype
     T omega;
     T k[Q];        // moving-wall terms 6 w_i (c_i . u_w), compute dtype
@@ -373,6 +374,41 @@ __device__ __forceinline__ void prefetch_ahead(PTR const (&base)[Q], const Geom 
 #undef MLB_X
 }
 
+// The same prefetch as ONE bulk instruction per population and row group
+// (cp.async.bulk.prefetch.L2, sm_90+): the rows a block works on are contiguous
+// in memory across the whole x extent, so thread i < 19 of the block at
+// blockIdx.x == 0 prefetches, for population i, the `nrows` full rows starting at
+// row yb (+ the pull's row / plane shift) for all the blocks that share them.
+// Rows that wrap around the y edge are left out (they are walls or one row in ny).
+constexpr int SEL_zc = 0, SEL_zm = 1, SEL_zq = 2, SEL_rc = 0, SEL_rm = 1, SEL_rq = 2;
+template <typename TS, bool PULL, typename PTR>
+__device__ __forceinline__ void prefetch_rows(PTR const (&base)[Q], const Geom &gm, int dz, int dy,
+                                              int yb, int nrows, int lz, int i)
+{
+    int r0 = yb + dy, lp = lz + dz;
+    if (r0 >= gm.ny) { r0 -= gm.ny; ++lp; }
+    if (lp >= gm.nz)
+        return;
+    int zsel = 0, rsel = 0;
+    if (PULL) {
+#define MLB_X(ii, CX, Z, R) if (i == ii) { zsel = SEL_##Z; rsel = SEL_##R; }
+        MLB_DIRS(MLB_X)
+#undef MLB_X
+    }
+    r0 += rsel == SEL_rm ? -1 : rsel == SEL_rq ? 1 : 0;
+    if (r0 < 0) { r0 = 0; --nrows; }
+    if (r0 + nrows > gm.ny) nrows = gm.ny - r0;
+    if (nrows <= 0)
+        return;
+    const int zp = zsel == SEL_zc ? lp + 1
+                 : zsel == SEL_zm ? (lp == 0 ? gm.zlo_src : lp)
+                                  : (lp == gm.nz - 1 ? gm.zhi_src : lp + 2);
+    const TS *p = base[i] + ((long long)zp * gm.plane + (long long)r0 * gm.xp);
+    const unsigned bytes = (unsigned)(nrows * (int)gm.xp * (int)sizeof(TS));  // whole lines
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(__cvta_generic_to_global(p)),
+                 "r"(bytes));
+}
+
 // ---------------------------------------------------------------------------
 // Fused pull-stream + bounce-back + BGK collide, one thread per cell
 // (kernels.py:76-245 `cell`, :247-279 `fused`).  blockIdx = (x tile, y, plane).
@@ -423,11 +459,10 @@ __device__ __forceinline__ void step_cell(const StepArgs<TS> &a, const PushArgs<
     MLB_PULL(13, zq, rc, dq) MLB_PULL(14, zq, rc, dm) MLB_PULL(15, zm, rm, dc)
     MLB_PULL(16, zm, rq, dc) MLB_PULL(17, zq, rq, dc) MLB_PULL(18, zq, rm, dc)
 #undef MLB_PULL
-    // one cell per thread: 19 prefetches per 32 cells are an issue cost that only the
-    // float64-arithmetic kernels can afford (511^3: fp32 storage / fp64 arithmetic
-    // 0.76 -> 0.82 of the HBM peak, fp64 unchanged; fp32 0.97 -> 0.87 if enabled)
-    if constexpr (sizeof(T) == 8)
-        prefetch_ahead<TS, 1, 32, true>(a.pre, gm, a.pf_dz, a.pf_dy, x, y, lz, threadIdx.x & 31);
+    // one cell per thread: the bulk form, one instruction per population and row
+    // (19 per-line prefetches per 32 cells cost too many issue slots here)
+    if (blockIdx.x == 0 && threadIdx.x < Q && (a.pf_dz | a.pf_dy) != 0)
+        prefetch_rows<TS, true>(a.pre, gm, a.pf_dz, a.pf_dy, y, 1, lz, threadIdx.x);
 
     // Non-fluid destination.  Strict mode: never written (kernels.py:79-80;
     // the stores of the warp then leave 28-of-32-byte sectors at every wall,
@@ -526,6 +561,7 @@ struct AAArgs {
     TS inlet[Q];  // equilibrium(1, u_in, 0, 0), storage dtype (open boundaries, pack kernels)
     int z0;       // first slab plane this launch updates (blockIdx.z = 0)
     int pf_dz, pf_dy;  // L2 prefetch distance of the pack kernels (prefetch_ahead)
+    int pf_bulk;
     // z-slabs (REMOTE kernels): the pull half writes each result into the location
     // it was pulled from - and for a boundary plane's crossing directions that
     // location belongs to the ring neighbour.  It is READ from the local halo plane
@@ -860,7 +896,12 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
     MLB_DIRS(MLB_X)
 #undef MLB_X
 
-    prefetch_ahead<TS, V, LX, true>(a.pre, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
+    if (a.pf_bulk) {
+        if (blockIdx.x == 0 && threadIdx.x < Q && (a.pf_dz | a.pf_dy) != 0)
+            prefetch_rows<TS, true>(a.pre, gm, a.pf_dz, a.pf_dy, blockIdx.y * (4 * RPW), 4 * RPW, lz,
+                                    threadIdx.x);
+    } else
+        prefetch_ahead<TS, V, LX, true>(a.pre, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
 
     // class words: all zero for a pack of bulk cells (the usual case), else from
     // the dictionary.  (A separate code path for bulk packs was measured and is
@@ -1047,7 +1088,12 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
 #define MLB_X(i, CX, Z, R) pull_pack<TS, V, CX>(a.f[i] + ((Z) + (R)), x0, xl, xr, g[i]);
     MLB_DIRS(MLB_X)
 #undef MLB_X
-    prefetch_ahead<TS, V, LX, true>(a.f, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
+    if (a.pf_bulk) {
+        if (blockIdx.x == 0 && threadIdx.x < Q && (a.pf_dz | a.pf_dy) != 0)
+            prefetch_rows<TS, true>(a.f, gm, a.pf_dz, a.pf_dy, blockIdx.y * (4 * RPW), 4 * RPW, lz,
+                                    threadIdx.x);
+    } else
+        prefetch_ahead<TS, V, LX, true>(a.f, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
 
     const bool bulk = valid && kpack == 0u;
     const bool bulk_r = __shfl_down_sync(FULL, (int)bulk, 1) != 0 && seg != LX - 1
@@ -1248,7 +1294,12 @@ __global__ void __launch_bounds__(128, 4) aa_local_vec_kernel(const AAArgs<TS> a
 #pragma unroll
     for (int i = 0; i < Q; ++i)
         PackIO<TS, V>::load(a.f[opp(i)] + d, g[i]);
-    prefetch_ahead<TS, V, LX, false>(a.f, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
+    if (a.pf_bulk) {
+        if (blockIdx.x == 0 && threadIdx.x < Q && (a.pf_dz | a.pf_dy) != 0)
+            prefetch_rows<TS, false>(a.f, gm, a.pf_dz, a.pf_dy, blockIdx.y * (4 * RPW), 4 * RPW, lz,
+                                     threadIdx.x);
+    } else
+        prefetch_ahead<TS, V, LX, false>(a.f, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
     uint32_t c[V];
 #pragma unroll
     for (int j = 0; j < V; ++j)
