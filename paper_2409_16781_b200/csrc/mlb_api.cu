@@ -301,7 +301,10 @@ int resolve_variant(const mlb_plan *p)
     if (p->dtype == MLB_F64 && (p->n_in || p->n_out) && p->nx % 2 == 0 && p->nx >= 128)
         return 1016;
     if (p->dtype == MLB_F32C64 && p->nx % 2 == 0 && p->nx >= 128)
-        return 2016;   // 8-byte packs: 36.6 vs 33.4 GLUPS (one cell per thread) at 512^3
+        return 2016;   // 8-byte packs: 36.6 vs 33.4 GLUPS (one cell per thread) at 512^3.  (With its
+                       // bulk L2 prefetch the one-cell-per-thread kernel is 3 % ahead in 200-step
+                       // runs - 0.936 vs 0.907 of the HBM peak - but 1 % behind in the 300-step
+                       // bench at the power cap, 37.9 vs 38.2 GLUPS: packs stay the default.)
     return 128;
 }
 

@@ -19,7 +19,7 @@ for prec in (Precision.SINGLE, Precision.DOUBLE, Precision.MIXED1, Precision.MIX
         plan = KernelPlan(n, n, n, Layout.ROW, prec, mask, 1.53, (0.1, 0, 0))
         if os.environ.get("MLB_VARIANT"):
             v = int(os.environ["MLB_VARIANT"])
-            plan.set_variant(v if prec in (Precision.SINGLE, Precision.DOUBLE) else v + 1000)
+            plan.set_variant(v if v < 1000 or prec in (Precision.SINGLE, Precision.DOUBLE) else v + 1000)
         if os.environ.get("MLB_PREFETCH"):
             plan.set_prefetch(int(os.environ["MLB_PREFETCH"]))
         a = plan.alloc()
