@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define MLB_ABI_VERSION 1
+#define MLB_ABI_VERSION 2
 #define MLB_Q 19
 
 /* dtype codes = the reference's Precision wire codes (fields.py:22-25):
@@ -62,6 +62,9 @@ typedef struct {
 
 const char *mlb_last_error(void);
 int mlb_abi_version(void);
+/* first 16 hex digits of the SHA-256 of the sources (mlb_api.cu, mlb_kernels.cuh,
+ * mlb.h) this binary was built from: ties recorded profiles to the code that ran */
+const char *mlb_build_id(void);
 /* number of CUDA kernel launches issued by this library in this process */
 int64_t mlb_launch_count(void);
 
@@ -72,6 +75,17 @@ int64_t mlb_launch_count(void);
 int mlb_trim(void);
 
 int mlb_layout_query(int nx, int ny, int nz, int dtype, mlb_layout *out);
+
+/* Population blocks owned by the library: plain cudaMalloc memory of
+ * `bytes` (mlb_layout.bytes) on `device` - what CUDA IPC can export for the
+ * z-slab exchange whatever allocator the host framework runs (torch's
+ * expandable segments / cudaMallocAsync pools cannot be exported).  The
+ * reference's counterpart is PopulationField's numpy block (fields.py:108-146):
+ * the caller still owns the block and says when it dies; the library only
+ * provides the memory.  Freed blocks are pooled (MLB_BLOCK_POOL_GB, default 24;
+ * mlb_trim returns them); mlb_block_free waits for the device to go idle. */
+int mlb_block_alloc(int device, int64_t bytes, void **d_out);
+int mlb_block_free(void *d_ptr);
 
 /* ---- plan: replaces KernelPlan.__init__ (kernels.py:408-443) -------------
  * omega and wall_u are cast once to the compute dtype, as the reference
@@ -113,6 +127,13 @@ int mlb_plan_set_passthrough(mlb_plan *plan, int on);
  * blocking of the kernels.py:258-279 tiles).
  * -1 = auto (default: the cells whose populations make ~10 MB), 0 = off. */
 int mlb_plan_set_prefetch(mlb_plan *plan, long long cells);
+/* CUDA graphs in mlb_run_steps / mlb_run_steps_inplace: on small domains a step
+ * takes microseconds and the loop is launch-bound (the reference's loop pays
+ * Python overhead per step at the same place, engine.py:244-249), so runs of up
+ * to 32 steps are captured once - the very launches the plain loop makes - and
+ * replayed.  -1 = auto (default: domains up to 4 Mi cells), 0 = never, 1 =
+ * always; the environment variable MLB_GRAPH overrides.  Never changes bits. */
+int mlb_plan_set_graph(mlb_plan *plan, int mode);
 
 /* Flags: the reference's `mask` argument (kernels.py:408, a (N,) uint8 array
  * in cell order).  h_flags is dense [nz][ny][nx] HOST memory.  h_halo_lo /
@@ -241,6 +262,40 @@ int mlb_step_push_range(mlb_plan *plan, const void *d_fpre, void *d_fpost,
                         int z0, int z1, void *d_below_post, int nz_below,
                         void *d_above_post, int nz_above, void *stream);
 
+/* ---- the z-slab loop in one call ---------------------------------------------
+ * engine.run's loop body (engine.py:244-249) for one rank of a z-slab ring over
+ * peer memory, `nsteps` times, with nothing but launches between steps:
+ *   stream:     fork -> interior planes [1, nz-1) -> join
+ *   hi_stream:  wait until both neighbours have posted step t-1, boundary planes
+ *               0 and nz-1 (mlb_step_push_range: the crossing populations also go
+ *               into the neighbours' halo planes), post step t to both neighbours
+ * (overlap == 0, nz < 3 or hi_stream == stream: everything on `stream`).
+ * below[k] / above[k]: the ring neighbours' blocks that correspond to the local
+ * block k (0 = d_a, 1 = d_b), mapped with mlb_ipc_open - with a single slab the
+ * local blocks themselves.  post_* are the slots of the NEIGHBOURS' signal
+ * blocks this rank posts into, wait_* this rank's own two counters.  `t` is the
+ * number of steps posted so far: in/out, shared with mlb_signal_* callers.
+ * The newest populations end in d_a when nsteps is even, d_b when odd.  The
+ * call only enqueues; *host_us (may be NULL) is the host time per step spent
+ * enqueuing, averaged over the first steps (before the launch queue can fill).
+ * The _inplace form advances ONE block (mlb_step_inplace_range per plane
+ * range; below[0] / above[0] only) and flips *repr once per step. */
+typedef struct {
+    void *below[2];
+    void *above[2];
+    int32_t nz_below, nz_above;
+    void *post_below, *post_above;
+    const void *wait_below, *wait_above;
+    uint32_t t;
+    int32_t wait_mode;   /* as mlb_signal_wait */
+    int32_t overlap;     /* boundary planes first, on hi_stream */
+} mlb_ring;
+int mlb_slab_run_steps(mlb_plan *plan, void *d_a, void *d_b, int nsteps, mlb_ring *ring,
+                       void *stream, void *hi_stream, double *host_us);
+int mlb_slab_run_steps_inplace(mlb_plan *plan, void *d_f, int nsteps, int *repr,
+                               mlb_ring *ring, void *stream, void *hi_stream,
+                               double *host_us);
+
 /* ---- peer memory: CUDA IPC mapping + stream-ordered signals ---------------
  * One process per GPU: a rank exports its population blocks and its signal
  * words (mlb_ipc_export: handle of the enclosing cudaMalloc allocation + the
@@ -251,6 +306,8 @@ int mlb_step_push_range(mlb_plan *plan, const void *d_fpre, void *d_fpost,
  * cache by handle bytes.  Not for allocations of the same process. */
 #define MLB_IPC_HANDLE_BYTES 64
 #define MLB_SIGNAL_BYTES 256   /* 64 uint32 slots, zero-initialised */
+#define MLB_SLOT_FROM_BELOW 0     /* byte offsets of a rank's two step counters */
+#define MLB_SLOT_FROM_ABOVE 128   /* inside its signal block                    */
 int mlb_ipc_export(const void *d_ptr, unsigned char handle[MLB_IPC_HANDLE_BYTES],
                    int64_t *offset);
 int mlb_ipc_open(int device, const unsigned char handle[MLB_IPC_HANDLE_BYTES],
@@ -263,8 +320,10 @@ int mlb_ipc_close(void *d_base);
  * without blocking the host.  mode 0 = a stream memory operation
  * (cuStreamWaitValue32: no SM is occupied) when the driver offers it, else a
  * one-thread polling kernel; 1 = memory operation or error; 2 = polling
- * kernel.  post / wait / read act on the CURRENT device (the one `stream`
- * belongs to); create selects `device` itself. */
+ * kernel.  post / wait act on the device `stream` belongs to (the legacy
+ * default stream: the current device), destroy on the device that holds the
+ * block; create selects `device` itself.  No call changes the caller's
+ * current device. */
 int mlb_signal_create(int device, void **d_sig);
 int mlb_signal_destroy(void *d_sig);
 int mlb_signal_post(void *d_slot, uint32_t value, void *stream);

@@ -13,7 +13,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmlb_d3q19.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 MLB_F32, MLB_F64, MLB_F16, MLB_F32C64 = 0, 1, 2, 3
 IPC_HANDLE_BYTES = 64
@@ -22,7 +22,7 @@ MLB_OK, MLB_EINVAL, MLB_ECUDA, MLB_ENOMEM, MLB_EUNSUPPORTED = 0, 1, 2, 3, 4
 
 #: every symbol include/mlb.h declares; tests check the .so exports them all
 SYMBOLS = (
-    "mlb_last_error", "mlb_abi_version", "mlb_launch_count", "mlb_trim", "mlb_layout_query",
+    "mlb_last_error", "mlb_abi_version", "mlb_build_id", "mlb_launch_count", "mlb_trim", "mlb_layout_query",
     "mlb_plan_create", "mlb_plan_destroy", "mlb_plan_get_layout",
     "mlb_plan_set_physics", "mlb_plan_set_variant", "mlb_plan_set_passthrough",
     "mlb_plan_set_prefetch",
@@ -37,6 +37,8 @@ SYMBOLS = (
     "mlb_signal_create", "mlb_signal_destroy", "mlb_signal_post", "mlb_signal_wait",
     "mlb_signal_wait_kind", "mlb_signal_read", "mlb_macro", "mlb_diagnostics", "mlb_probe",
     "mlb_step_host",
+    "mlb_block_alloc", "mlb_block_free", "mlb_plan_set_graph",
+    "mlb_slab_run_steps", "mlb_slab_run_steps_inplace",
 )
 
 
@@ -45,6 +47,16 @@ class Layout(ctypes.Structure):
                 ("itemsize", ctypes.c_int32), ("xp", ctypes.c_int64),
                 ("plane", ctypes.c_int64), ("pop", ctypes.c_int64),
                 ("total", ctypes.c_int64), ("bytes", ctypes.c_int64)]
+
+
+class Ring(ctypes.Structure):
+    """mlb_ring (include/mlb.h): one rank's view of the z-slab ring."""
+    _fields_ = [("below", ctypes.c_void_p * 2), ("above", ctypes.c_void_p * 2),
+                ("nz_below", ctypes.c_int32), ("nz_above", ctypes.c_int32),
+                ("post_below", ctypes.c_void_p), ("post_above", ctypes.c_void_p),
+                ("wait_below", ctypes.c_void_p), ("wait_above", ctypes.c_void_p),
+                ("t", ctypes.c_uint32), ("wait_mode", ctypes.c_int32),
+                ("overlap", ctypes.c_int32)]
 
 
 _lib = None
@@ -66,6 +78,7 @@ def lib():
     sig = {
         "mlb_last_error": (ctypes.c_char_p, []),
         "mlb_abi_version": (i, []),
+        "mlb_build_id": (ctypes.c_char_p, []),
         "mlb_launch_count": (ctypes.c_int64, []),
         "mlb_trim": (i, []),
         "mlb_layout_query": (i, [i, i, i, i, ctypes.POINTER(Layout)]),
@@ -109,6 +122,13 @@ def lib():
         "mlb_diagnostics": (i, [vp, vp, dp3, vp]),
         "mlb_probe": (i, [vp, vp, i, i, i, vp, vp]),
         "mlb_step_host": (i, [vp, vp, vp, vp, vp, vp]),
+        "mlb_block_alloc": (i, [i, ctypes.c_int64, ctypes.POINTER(vp)]),
+        "mlb_block_free": (i, [vp]),
+        "mlb_plan_set_graph": (i, [vp, i]),
+        "mlb_slab_run_steps": (i, [vp, vp, vp, i, ctypes.POINTER(Ring), vp, vp,
+                                   ctypes.POINTER(d)]),
+        "mlb_slab_run_steps_inplace": (i, [vp, vp, i, ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(Ring), vp, vp, ctypes.POINTER(d)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -131,6 +151,11 @@ def check(rc):
     if rc == MLB_ENOMEM:
         raise MemoryError(msg)
     raise RuntimeError(msg)
+
+
+def build_id():
+    """Hash of the sources the loaded library was built from."""
+    return lib().mlb_build_id().decode()
 
 
 def launch_count():

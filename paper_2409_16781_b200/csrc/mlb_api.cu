@@ -8,6 +8,7 @@
 #include "mlb_kernels.cuh"
 
 #include <atomic>
+#include <chrono>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -48,6 +49,35 @@ int fail(int code, const char *fmt, ...)
 
 inline cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
 
+// Entry points work on the plan's device and leave the caller's current device
+// as they found it (a process may drive several GPUs, or keep torch's current
+// device elsewhere).
+struct DeviceGuard {
+    int prev = -1;
+    bool switched = false;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev)
+    {
+        err = cudaGetDevice(&prev);
+        if (err == cudaSuccess && prev != dev) {
+            err = cudaSetDevice(dev);
+            switched = err == cudaSuccess;
+        }
+    }
+    ~DeviceGuard()
+    {
+        if (switched)
+            cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard &) = delete;
+    DeviceGuard &operator=(const DeviceGuard &) = delete;
+};
+#define MLB_ON_DEVICE(dev)                                                      \
+    DeviceGuard guard_(dev);                                                    \
+    if (guard_.err != cudaSuccess)                                              \
+        return fail(MLB_ECUDA, "cudaSetDevice(%d): %s", (int)(dev),             \
+                    cudaGetErrorString(guard_.err))
+
 // Device memory of the plans (flag tables, index lists, reduction scratch, signal
 // words) comes from a small process-wide pool: cudaMalloc / cudaFree synchronise
 // the device and were measured to stall for 0.1 - 1.4 s now and then with tens of
@@ -57,6 +87,7 @@ inline cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
 // shape; at most POOL_CAP bytes are held back, mlb_trim() returns them all.
 class DevicePool {
 public:
+    explicit DevicePool(size_t cap) : cap_(cap) {}
     cudaError_t alloc(void **out, size_t bytes)
     {
         int dev = 0;
@@ -94,7 +125,7 @@ public:
         }
         const Key k = it->second;
         live_.erase(it);
-        if (cached_ + k.second > POOL_CAP) {
+        if (cached_ + k.second > cap_) {
             cudaFree(p);
             return;
         }
@@ -112,13 +143,25 @@ public:
 
 private:
     using Key = std::pair<int, size_t>;
-    static constexpr size_t POOL_CAP = 6ull << 30;
+    const size_t cap_;
     std::mutex mu_;
     std::multimap<Key, void *> free_;
     std::unordered_map<void *, Key> live_;
     size_t cached_ = 0;
 };
-DevicePool g_pool;
+DevicePool g_pool(6ull << 30);
+// Population blocks handed out by mlb_block_alloc: plain cudaMalloc memory (what
+// CUDA IPC can export, whatever allocator the host framework is configured with).
+// A short run allocates and frees tens of GB around a few milliseconds of work,
+// so up to MLB_BLOCK_POOL_GB (default 24) of freed blocks are kept for the next
+// caller; an allocation that fails returns them to the driver and retries.
+size_t block_pool_cap()
+{
+    const char *e = std::getenv("MLB_BLOCK_POOL_GB");
+    const double gb = e ? std::atof(e) : 24.0;
+    return gb <= 0.0 ? 0 : (size_t)(gb * (double)(1ull << 30));
+}
+DevicePool g_blocks(block_pool_cap());
 
 template <typename T>
 cudaError_t pool_alloc(T **out, size_t bytes) { return g_pool.alloc(reinterpret_cast<void **>(out), bytes); }
@@ -156,6 +199,24 @@ struct mlb_plan {
     int diag_blocks = 0;
     double *d_partials = nullptr, *d_diag = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // bumped by every setter that changes what a launch looks like: a captured
+    // graph of step launches is only replayed while it still matches
+    unsigned long long epoch = 0;
+    // CUDA graph of a run of steps (mlb_run_steps / mlb_run_steps_inplace on small,
+    // launch-bound domains): captured once on the library's own stream, replayed on
+    // the caller's
+    int graph_mode = -1;            // -1 auto (small domains), 0 never, 1 always
+    cudaStream_t cap_stream = nullptr;
+    struct GraphCache {
+        cudaGraphExec_t exec = nullptr;
+        void *a = nullptr, *b = nullptr;
+        unsigned long long epoch = 0;
+        int steps = 0, repr = 0;
+        long long nodes = 0;
+    } gc;
+    // z-slab schedule (mlb_slab_run_steps): fork / join between the main and the
+    // boundary stream
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -721,6 +782,10 @@ extern "C" {
 
 const char *mlb_last_error(void) { return g_err; }
 int mlb_abi_version(void) { return MLB_ABI_VERSION; }
+#ifndef MLB_BUILD_ID
+#define MLB_BUILD_ID "unknown"
+#endif
+const char *mlb_build_id(void) { return MLB_BUILD_ID; }
 int64_t mlb_launch_count(void) { return g_launches.load(); }
 
 int mlb_layout_query(int nx, int ny, int nz, int dtype, mlb_layout *out)
@@ -745,7 +810,7 @@ int mlb_plan_create(mlb_plan **out, int nx, int ny, int nz, int dtype, double om
     MLB_CUDA(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev)
         return fail(MLB_EINVAL, "device %d out of range (%d visible)", device, ndev);
-    MLB_CUDA(cudaSetDevice(device));
+    MLB_ON_DEVICE(device);
     mlb_plan *p = new (std::nothrow) mlb_plan;
     if (!p)
         return fail(MLB_ENOMEM, "out of host memory");
@@ -762,6 +827,8 @@ int mlb_plan_create(mlb_plan **out, int nx, int ny, int nz, int dtype, double om
     if (e == cudaSuccess) e = pool_alloc(&p->d_diag, sizeof(double) * mlb::DIAG_N);
     if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&p->ev1);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         mlb_plan_destroy(p);
         return fail(MLB_ECUDA, "plan setup: %s", cudaGetErrorString(e));
@@ -774,7 +841,7 @@ int mlb_plan_destroy(mlb_plan *p)
 {
     if (!p)
         return MLB_OK;
-    cudaSetDevice(p->device);
+    DeviceGuard guard_(p->device);
     // cudaFree used to wait for work still using the tables; a pooled block can be
     // handed to the next plan at once, so wait here
     cudaDeviceSynchronize();
@@ -783,6 +850,10 @@ int mlb_plan_destroy(mlb_plan *p)
     pool_free(p->d_out); pool_free(p->d_out_tmp); pool_free(p->d_partials); pool_free(p->d_diag);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
+    if (p->gc.exec) cudaGraphExecDestroy(p->gc.exec);
+    if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     delete p;
     return MLB_OK;
 }
@@ -801,6 +872,7 @@ int mlb_plan_set_physics(mlb_plan *p, double omega, const double wall_u[3], doub
     // omega = 0 is legal kernel input (pure streaming, test_kernels.py:152-164)
     if (!(omega >= 0.0 && omega < 2.0))
         return fail(MLB_EINVAL, "relaxation rate omega=%g outside [0, 2)", omega);
+    ++p->epoch;
     p->omega = omega;
     for (int i = 0; i < 3; ++i)
         p->wall_u[i] = wall_u ? wall_u[i] : 0.0;
@@ -816,6 +888,7 @@ int mlb_plan_set_variant(mlb_plan *p, int variant)
                     "512} (one cell per thread), or W*1000 + {8,16,32} with W = 1 (16-byte packs, "
                     "fp32/fp64), 2 or 3 (8- / 4-byte packs, fp16 storage)", variant);
     p->variant = variant;
+    ++p->epoch;
     return MLB_OK;
 }
 
@@ -843,6 +916,7 @@ int mlb_plan_set_passthrough(mlb_plan *p, int on)
                     "that cell's STALE value in fpost (numpy evaluates the right-hand side "
                     "first, engine.py:179-180), which pass-through would refresh");
     p->passthrough = on ? 1 : 0;
+    ++p->epoch;
     return MLB_OK;
 }
 
@@ -853,6 +927,7 @@ int mlb_plan_set_prefetch(mlb_plan *p, long long cells)
         return fail(MLB_EINVAL, "prefetch distance %lld: must be -1 (auto), 0 (off) or a number "
                     "of cells", cells);
     p->prefetch = cells;
+    ++p->epoch;
     return MLB_OK;
 }
 
@@ -862,7 +937,7 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     if (int rc = check_plan(p, false)) return rc;
     if (!h_flags)
         return fail(MLB_EINVAL, "h_flags is NULL");
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     const int nx = p->nx, ny = p->ny, nz = p->nz;
     const long long xp = p->lay.xp, plane = p->lay.plane;
     const size_t padded = (size_t)(nz + 2) * plane;
@@ -880,6 +955,7 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     p->d_out_tmp = nullptr;
     p->have_flags = false;
     p->n_in = p->n_out = 0;
+    ++p->epoch;
 
     // the padded flag block on the device, straight from the caller's dense
     // array (row padding = solid, never written); no padded host copy
@@ -1025,7 +1101,7 @@ int mlb_plan_get_flags(const mlb_plan *p, uint8_t *h_flags)
 {
     if (int rc = check_plan(p, true)) return rc;
     if (!h_flags) return fail(MLB_EINVAL, "h_flags is NULL");
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     // from what the kernels read - kind byte -> dictionary (or the full-width
     // word for escape cells) -> low bits: proves the codes the kernel tests
     const size_t padded = (size_t)(p->nz + 2) * p->lay.plane;
@@ -1063,7 +1139,7 @@ int mlb_upload(const mlb_plan *p, const void *h_dense, void *d_f, void *stream)
 {
     if (int rc = check_plan(p, false)) return rc;
     if (!h_dense || !d_f) return fail(MLB_EINVAL, "NULL buffer");
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     return copy_dense(p, h_dense, d_f, true, S(stream));
 }
 
@@ -1071,7 +1147,7 @@ int mlb_download(const mlb_plan *p, const void *d_f, void *h_dense, void *stream
 {
     if (int rc = check_plan(p, false)) return rc;
     if (!h_dense || !d_f) return fail(MLB_EINVAL, "NULL buffer");
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     return copy_dense(p, d_f, h_dense, false, S(stream));
 }
 
@@ -1085,7 +1161,7 @@ int mlb_step_range(mlb_plan *p, const void *d_fpre, void *d_fpost, int z0, int z
     if (z0 < 0 || z1 > p->nz || z0 > z1)
         return fail(MLB_EINVAL, "plane range [%d, %d) outside [0, %d)", z0, z1, p->nz);
     if (z0 == z1) return MLB_OK;
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     return launch_step(p, d_fpre, d_fpost, z0, z1, S(stream));
 }
 
@@ -1102,7 +1178,7 @@ int mlb_open_pass_range(mlb_plan *p, void *d_fpost, int z0, int z1, void *stream
     if (z0 < 0 || z1 > p->nz || z0 > z1)
         return fail(MLB_EINVAL, "plane range [%d, %d) outside [0, %d)", z0, z1, p->nz);
     if (p->n_in == 0 && p->n_out == 0) return MLB_OK;
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     if (p->dtype == MLB_F32) return launch_open<float>(p, d_fpost, z0, z1, S(stream));
     if (p->dtype == MLB_F64) return launch_open<double>(p, d_fpost, z0, z1, S(stream));
     if (p->dtype == MLB_F32C64) return launch_open<mlb::f32w>(p, d_fpost, z0, z1, S(stream));
@@ -1120,7 +1196,7 @@ int mlb_step_open_range(mlb_plan *p, const void *d_fpre, void *d_fpost, int z0, 
         if (z0 < 0 || z1 > p->nz || z0 > z1)
             return fail(MLB_EINVAL, "plane range [%d, %d) outside [0, %d)", z0, z1, p->nz);
         if (z0 == z1) return MLB_OK;
-        MLB_CUDA(cudaSetDevice(p->device));
+        MLB_ON_DEVICE(p->device);
         return launch_step(p, d_fpre, d_fpost, z0, z1, S(stream), true);
     }
     if (int rc = mlb_step_range(p, d_fpre, d_fpost, z0, z1, stream)) return rc;
@@ -1133,18 +1209,135 @@ int mlb_open_pass(mlb_plan *p, void *d_fpost, void *stream)
     return mlb_open_pass_range(p, d_fpost, 0, p->nz, stream);
 }
 
+// ---- CUDA graphs for launch-bound domains ------------------------------------
+// Below a few million cells a step takes tens of microseconds or less and the
+// loop is bound by launch latency, not by HBM (the reference's loop has the same
+// problem with Python overhead, engine.py:244-249 / SURVEY "timing semantics").
+// mlb_run_steps / mlb_run_steps_inplace then capture a run of steps - the very
+// launches the plain loop makes: same kernels, same arguments, same order, so
+// the same bits - into a CUDA graph once, and replay it.
+namespace {
+
+constexpr int GRAPH_STEPS = 32;                  // steps per replayed graph
+constexpr long long GRAPH_AUTO_CELLS = 4ll << 20;  // auto: domains up to this many cells
+
+int one_step(mlb_plan *p, void *pre, void *post, void *stream)
+{
+    return mlb_step_open_range(p, pre, post, 0, p->nz, stream);
+}
+
+bool graph_wanted(const mlb_plan *p, int nsteps)
+{
+    static const int env = std::getenv("MLB_GRAPH") ? std::atoi(std::getenv("MLB_GRAPH")) : -1;
+    const int mode = env >= 0 ? env : p->graph_mode;
+    if (mode == 0 || nsteps < 8)
+        return false;
+    return mode == 1 || (long long)p->nx * p->ny * p->nz <= GRAPH_AUTO_CELLS;
+}
+
+// A graph exec that advances `steps` (even) steps from blocks (a, b) - or, in
+// place (b == NULL), from representation `repr` of block a.  NULL if the capture
+// cannot be done (the caller then launches directly).
+cudaGraphExec_t graph_for(mlb_plan *p, void *a, void *b, int steps, int repr)
+{
+    mlb_plan::GraphCache &gc = p->gc;
+    if (gc.exec && gc.a == a && gc.b == b && gc.epoch == p->epoch && gc.steps == steps
+        && gc.repr == repr)
+        return gc.exec;
+    if (gc.exec) {
+        cudaGraphExecDestroy(gc.exec);
+        gc.exec = nullptr;
+    }
+    if (!p->cap_stream
+        && cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return nullptr;
+    }
+    if (cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return nullptr;
+    }
+    const long long launches0 = g_launches.load();
+    int rc = MLB_OK;
+    if (b) {
+        void *pre = a, *post = b;
+        for (int t = 0; t < steps && rc == MLB_OK; ++t) {
+            rc = one_step(p, pre, post, p->cap_stream);
+            void *tmp = pre; pre = post; post = tmp;
+        }
+    } else {
+        int r = repr;
+        for (int t = 0; t < steps && rc == MLB_OK; ++t, r ^= 1)
+            rc = launch_aa_any(p, a, r, p->cap_stream);
+    }
+    const long long nodes = g_launches.load() - launches0;
+    g_launches.fetch_sub(nodes);   // captured, not launched: replays are counted
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(p->cap_stream, &graph);
+    if (rc != MLB_OK || e != cudaSuccess || !graph) {
+        (void)cudaGetLastError();
+        if (graph) cudaGraphDestroy(graph);
+        return nullptr;
+    }
+    cudaGraphExec_t exec = nullptr;
+    if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+        (void)cudaGetLastError();
+        exec = nullptr;
+    }
+    cudaGraphDestroy(graph);
+    if (exec) {
+        gc.exec = exec; gc.a = a; gc.b = b; gc.epoch = p->epoch; gc.steps = steps;
+        gc.repr = repr; gc.nodes = nodes;
+    }
+    return exec;
+}
+
+// replays of a captured run; returns the number of steps done (a multiple of 2,
+// so blocks / representation are back where they started)
+int run_graphed(mlb_plan *p, void *a, void *b, int nsteps, int repr, cudaStream_t st, int *done)
+{
+    *done = 0;
+    if (!graph_wanted(p, nsteps))
+        return MLB_OK;
+    const int unit = nsteps >= GRAPH_STEPS ? GRAPH_STEPS : (nsteps & ~1);
+    cudaGraphExec_t exec = graph_for(p, a, b, unit, repr);
+    if (!exec)
+        return MLB_OK;
+    for (int n = nsteps / unit; n > 0; --n) {
+        MLB_CUDA(cudaGraphLaunch(exec, st));
+        g_launches.fetch_add(p->gc.nodes, std::memory_order_relaxed);
+        *done += unit;
+    }
+    return MLB_OK;
+}
+
+}  // namespace
+
+int mlb_plan_set_graph(mlb_plan *p, int mode)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (mode < -1 || mode > 1)
+        return fail(MLB_EINVAL, "graph mode %d: must be -1 (auto), 0 (never) or 1 (always)", mode);
+    p->graph_mode = mode;
+    return MLB_OK;
+}
+
 int mlb_run_steps(mlb_plan *p, void *d_a, void *d_b, int nsteps, void *stream, float *ms)
 {
     if (int rc = check_plan(p, true)) return rc;
     if (p->z_mode != MLB_Z_PERIODIC)
         return fail(MLB_EUNSUPPORTED, "mlb_run_steps needs an MLB_Z_PERIODIC plan; a slab's "
-                    "halo exchange happens between steps, outside this library");
+                    "halo exchange happens between steps (mlb_slab_run_steps)");
     if (nsteps < 0) return fail(MLB_EINVAL, "nsteps < 0");
-    MLB_CUDA(cudaSetDevice(p->device));
+    if (!d_a || !d_b) return fail(MLB_EINVAL, "NULL population block");
+    if (d_a == d_b) return fail(MLB_EINVAL, "fpre and fpost must be distinct blocks");
+    MLB_ON_DEVICE(p->device);
     if (ms) MLB_CUDA(cudaEventRecord(p->ev0, S(stream)));
-    void *pre = d_a, *post = d_b;
-    for (int t = 0; t < nsteps; ++t) {
-        if (int rc = mlb_step_open_range(p, pre, post, 0, p->nz, stream)) return rc;
+    int done = 0;
+    if (int rc = run_graphed(p, d_a, d_b, nsteps, 0, S(stream), &done)) return rc;
+    void *pre = d_a, *post = d_b;   // `done` is even: the blocks are where they started
+    for (int t = done; t < nsteps; ++t) {
+        if (int rc = one_step(p, pre, post, stream)) return rc;
         void *tmp = pre; pre = post; post = tmp;
     }
     if (ms) {
@@ -1177,9 +1370,11 @@ int mlb_run_steps_inplace(mlb_plan *p, void *d_f, int nsteps, int *repr, void *s
 {
     if (int rc = check_inplace(p, d_f, repr)) return rc;
     if (nsteps < 0) return fail(MLB_EINVAL, "nsteps < 0");
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     if (ms) MLB_CUDA(cudaEventRecord(p->ev0, S(stream)));
-    for (int t = 0; t < nsteps; ++t) {
+    int done = 0;
+    if (int rc = run_graphed(p, d_f, nullptr, nsteps, *repr, S(stream), &done)) return rc;
+    for (int t = done; t < nsteps; ++t) {
         if (int rc = launch_aa_any(p, d_f, *repr, S(stream))) return rc;
         *repr ^= 1;
     }
@@ -1195,7 +1390,7 @@ int mlb_inplace_normalize(mlb_plan *p, void *d_f, int *repr, void *stream)
 {
     if (int rc = check_inplace(p, d_f, repr)) return rc;
     if (*repr == 0) return MLB_OK;
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     if (int rc = launch_aa_any(p, d_f, 2, S(stream))) return rc;
     *repr = 0;
     return MLB_OK;
@@ -1225,7 +1420,7 @@ int mlb_step_inplace_range(mlb_plan *p, void *d_f, int repr, int z0, int z1, voi
                     "cell has its x-1 neighbour in the same pack; this geometry has %lld inlet "
                     "and %lld outlet cells", p->n_in, p->n_out);
     if (z0 == z1) return MLB_OK;
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     AaRange r;
     r.z0 = z0; r.z1 = z1;
     r.below = d_below; r.nz_below = nz_below;
@@ -1240,7 +1435,7 @@ int mlb_inplace_swap_slab(mlb_plan *p, void *d_f, void *d_above, int nz_above, v
     if (p->z_mode != MLB_Z_HALO)
         return fail(MLB_EUNSUPPORTED, "mlb_inplace_swap_slab is the z-slab form; a whole domain "
                     "uses mlb_inplace_normalize");
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     AaRange r;
     r.above = d_above; r.nz_above = nz_above;
     return launch_aa_any(p, d_f, 2, S(stream), r);
@@ -1274,7 +1469,7 @@ int mlb_halo_copy(const mlb_plan *p, void *d_dst, const void *d_src, int src_nz,
     if (!d_dst || !d_src) return fail(MLB_EINVAL, "NULL population block");
     if (src_nz < 1 || (face != 0 && face != 1))
         return fail(MLB_EINVAL, "bad src_nz %d / face %d", src_nz, face);
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     return halo_copy_impl(p, d_dst, p->nz, d_src, src_nz, face, S(stream));
 }
 
@@ -1285,7 +1480,7 @@ int mlb_halo_push(const mlb_plan *p, const void *d_src, void *d_dst, int dst_nz,
     if (!d_dst || !d_src) return fail(MLB_EINVAL, "NULL population block");
     if (dst_nz < 1 || (face != 0 && face != 1))
         return fail(MLB_EINVAL, "bad dst_nz %d / face %d", dst_nz, face);
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     return halo_copy_impl(p, d_dst, dst_nz, d_src, p->nz, face, S(stream));
 }
 
@@ -1309,7 +1504,7 @@ int mlb_step_push_range(mlb_plan *p, const void *d_fpre, void *d_fpost, int z0, 
     if (z0 == 0 && d_below_post) { t.below = d_below_post; t.nz_below = nz_below; }
     if (z1 == p->nz && d_above_post) { t.above = d_above_post; t.nz_above = nz_above; }
     const bool any = t.below || t.above;
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     const bool open_cells = p->in_zoff[z1] > p->in_zoff[z0] || p->out_zoff[z1] > p->out_zoff[z0];
     const bool fuse = can_fuse_open(p, resolve_variant(p));
     if (!open_cells || fuse)
@@ -1325,12 +1520,140 @@ int mlb_step_push_range(mlb_plan *p, const void *d_fpre, void *d_fpost, int z0, 
     return MLB_OK;
 }
 
+// ---- the z-slab time-step loop, one call ---------------------------------------
+// What slab.DistSlab schedules per step, without a host interpreter in the loop:
+//   main:  record fork                         interior planes [1, nz-1)   wait join
+//   hi:    wait fork, wait both counters >= t-1, plane 0 (+ push down),
+//          plane nz-1 (+ push up), post t into both neighbours, record join
+extern "C++" {
+namespace {
+
+int check_ring(const mlb_plan *p, const mlb_ring *r, int nblocks)
+{
+    if (!r) return fail(MLB_EINVAL, "ring is NULL");
+    for (int k = 0; k < nblocks; ++k)
+        if (!r->below[k] || !r->above[k])
+            return fail(MLB_EINVAL, "ring: neighbour block %d is NULL", k);
+    if (r->nz_below < 1 || r->nz_above < 1)
+        return fail(MLB_EINVAL, "ring: neighbour slab plane counts must be >= 1");
+    if (!r->post_below || !r->post_above || !r->wait_below || !r->wait_above)
+        return fail(MLB_EINVAL, "ring: NULL signal slot");
+    if (r->wait_mode < 0 || r->wait_mode > 2)
+        return fail(MLB_EINVAL, "ring: wait mode must be 0 (auto), 1 or 2");
+    if (p->z_mode != MLB_Z_HALO)
+        return fail(MLB_EUNSUPPORTED, "the slab loop needs an MLB_Z_HALO plan");
+    return MLB_OK;
+}
+
+struct HostClock {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    double us() const
+    {
+        return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0)
+            .count();
+    }
+};
+
+// one step of the schedule; `boundary(z0, z1, st)` / `interior(st)` enqueue the launches
+template <typename FB, typename FI>
+int slab_step(mlb_plan *p, mlb_ring *r, cudaStream_t main, cudaStream_t hi, FB boundary,
+              FI interior)
+{
+    const uint32_t t = r->t + 1;
+    const bool overlap = r->overlap && p->nz >= 3 && hi != nullptr && hi != main;
+    cudaStream_t bs = overlap ? hi : main;
+    if (overlap) {
+        MLB_CUDA(cudaEventRecord(p->ev_fork, main));
+        MLB_CUDA(cudaStreamWaitEvent(hi, p->ev_fork, 0));
+    }
+    if (int rc = mlb_signal_wait(r->wait_below, t - 1, r->wait_mode, bs)) return rc;
+    if (int rc = mlb_signal_wait(r->wait_above, t - 1, r->wait_mode, bs)) return rc;
+    if (overlap) {
+        if (int rc = boundary(0, 1, bs)) return rc;
+        if (int rc = boundary(p->nz - 1, p->nz, bs)) return rc;
+    } else {
+        if (int rc = boundary(0, p->nz, bs)) return rc;
+    }
+    if (int rc = mlb_signal_post(r->post_below, t, bs)) return rc;
+    if (int rc = mlb_signal_post(r->post_above, t, bs)) return rc;
+    r->t = t;
+    if (overlap) {
+        if (int rc = interior(main)) return rc;
+        MLB_CUDA(cudaEventRecord(p->ev_join, hi));
+        MLB_CUDA(cudaStreamWaitEvent(main, p->ev_join, 0));
+    }
+    return MLB_OK;
+}
+
+}  // namespace
+}  // extern "C++"
+
+int mlb_slab_run_steps(mlb_plan *p, void *d_a, void *d_b, int nsteps, mlb_ring *ring,
+                       void *stream, void *hi_stream, double *host_us)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (int rc = check_ring(p, ring, 2)) return rc;
+    if (!d_a || !d_b || d_a == d_b) return fail(MLB_EINVAL, "need two distinct population blocks");
+    if (nsteps < 0) return fail(MLB_EINVAL, "nsteps < 0");
+    MLB_ON_DEVICE(p->device);
+    void *blk[2] = {d_a, d_b};
+    HostClock clock;
+    double first = 0.0;
+    int counted = 0;
+    for (int s = 0; s < nsteps; ++s) {
+        const int ipre = s & 1, ipost = ipre ^ 1;
+        void *pre = blk[ipre], *post = blk[ipost];
+        auto boundary = [&](int z0, int z1, cudaStream_t st) {
+            return mlb_step_push_range(p, pre, post, z0, z1, ring->below[ipost], ring->nz_below,
+                                       ring->above[ipost], ring->nz_above, st);
+        };
+        auto interior = [&](cudaStream_t st) {
+            return mlb_step_open_range(p, pre, post, 1, p->nz - 1, st);
+        };
+        if (int rc = slab_step(p, ring, S(stream), S(hi_stream), boundary, interior)) return rc;
+        if (s < 32) { first = clock.us(); counted = s + 1; }   // before the launch queue can fill
+    }
+    if (host_us) *host_us = counted ? first / counted : 0.0;
+    return MLB_OK;
+}
+
+int mlb_slab_run_steps_inplace(mlb_plan *p, void *d_f, int nsteps, int *repr, mlb_ring *ring,
+                               void *stream, void *hi_stream, double *host_us)
+{
+    if (int rc = check_plan(p, true)) return rc;
+    if (int rc = check_ring(p, ring, 1)) return rc;
+    if (!d_f || !repr) return fail(MLB_EINVAL, "NULL argument");
+    if (*repr != 0 && *repr != 1)
+        return fail(MLB_EINVAL, "representation must be 0 (normal) or 1 (shifted), got %d", *repr);
+    if (nsteps < 0) return fail(MLB_EINVAL, "nsteps < 0");
+    MLB_ON_DEVICE(p->device);
+    HostClock clock;
+    double first = 0.0;
+    int counted = 0;
+    for (int s = 0; s < nsteps; ++s) {
+        const int rp = *repr;
+        auto boundary = [&](int z0, int z1, cudaStream_t st) {
+            return mlb_step_inplace_range(p, d_f, rp, z0, z1, ring->below[0], ring->nz_below,
+                                          ring->above[0], ring->nz_above, st);
+        };
+        auto interior = [&](cudaStream_t st) {
+            return mlb_step_inplace_range(p, d_f, rp, 1, p->nz - 1, ring->below[0],
+                                          ring->nz_below, ring->above[0], ring->nz_above, st);
+        };
+        if (int rc = slab_step(p, ring, S(stream), S(hi_stream), boundary, interior)) return rc;
+        *repr ^= 1;
+        if (s < 32) { first = clock.us(); counted = s + 1; }
+    }
+    if (host_us) *host_us = counted ? first / counted : 0.0;
+    return MLB_OK;
+}
+
 int mlb_macro(const mlb_plan *p, const void *d_f, double *d_rho, double *d_ux, double *d_uy,
               double *d_uz, void *stream)
 {
     if (int rc = check_plan(p, false)) return rc;
     if (!d_f || !d_rho || !d_ux || !d_uy || !d_uz) return fail(MLB_EINVAL, "NULL buffer");
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     // (the diagnostics read storage only: mixed2 - float in memory - shares the float kernels)
     const int V = p->dtype == MLB_F64 ? 2 : 4;   // cells per pack (16 / 16 / 8 bytes)
     if (p->nx % V == 0) {
@@ -1365,7 +1688,7 @@ int mlb_diagnostics(mlb_plan *p, const void *d_f, double h_out[8], void *stream)
 {
     if (int rc = check_plan(p, true)) return rc;
     if (!d_f || !h_out) return fail(MLB_EINVAL, "NULL buffer");
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     const bool packs = p->nx % (p->dtype == MLB_F64 ? 2 : 4) == 0;
     const mlb::ClsTab ct = cls_tab(p);
     const int nb = p->diag_blocks, nt = mlb::DIAG_THREADS;
@@ -1399,7 +1722,7 @@ int mlb_probe(const mlb_plan *p, const void *d_f, int x, int y, int lz, double *
     if (!d_f || !d_out4) return fail(MLB_EINVAL, "NULL buffer");
     if (x < 0 || x >= p->nx || y < 0 || y >= p->ny || lz < 0 || lz >= p->nz)
         return fail(MLB_EINVAL, "probe cell (%d, %d, %d) outside the slab", x, y, lz);
-    MLB_CUDA(cudaSetDevice(p->device));
+    MLB_ON_DEVICE(p->device);
     if (p->dtype == MLB_F32 || p->dtype == MLB_F32C64)
         mlb::probe_kernel<float><<<1, 1, 0, S(stream)>>>(static_cast<const float *>(d_f),
                                                          p->g, x, y, lz, d_out4);
@@ -1494,7 +1817,7 @@ int mlb_ipc_export(const void *d_ptr, unsigned char handle[MLB_IPC_HANDLE_BYTES]
 int mlb_ipc_open(int device, const unsigned char handle[MLB_IPC_HANDLE_BYTES], void **d_base)
 {
     if (!handle || !d_base) return fail(MLB_EINVAL, "NULL argument");
-    MLB_CUDA(cudaSetDevice(device));
+    MLB_ON_DEVICE(device);
     cudaIpcMemHandle_t h;
     std::memcpy(&h, handle, sizeof(h));
     MLB_CUDA(cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess));
@@ -1511,7 +1834,7 @@ int mlb_ipc_close(void *d_base)
 int mlb_signal_create(int device, void **d_sig)
 {
     if (!d_sig) return fail(MLB_EINVAL, "NULL argument");
-    MLB_CUDA(cudaSetDevice(device));
+    MLB_ON_DEVICE(device);
     MLB_CUDA(g_pool.alloc(d_sig, MLB_SIGNAL_BYTES));
     MLB_CUDA(cudaMemset(*d_sig, 0, MLB_SIGNAL_BYTES));
     MLB_CUDA(cudaDeviceSynchronize());
@@ -1555,6 +1878,49 @@ int mlb_signal_wait(const void *d_slot, uint32_t value, int mode, void *stream)
 int mlb_trim(void)
 {
     g_pool.trim();
+    g_blocks.trim();
+    return MLB_OK;
+}
+
+int mlb_block_alloc(int device, int64_t bytes, void **d_out)
+{
+    if (!d_out) return fail(MLB_EINVAL, "NULL argument");
+    *d_out = nullptr;
+    if (bytes <= 0) return fail(MLB_EINVAL, "block of %lld bytes", (long long)bytes);
+    int ndev = 0;
+    MLB_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return fail(MLB_EINVAL, "device %d out of range (%d visible)", device, ndev);
+    MLB_ON_DEVICE(device);
+    cudaError_t e = g_blocks.alloc(d_out, (size_t)bytes);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        g_pool.trim();                 // the plans' idle tables too, then once more
+        e = g_blocks.alloc(d_out, (size_t)bytes);
+    }
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return fail(MLB_ENOMEM, "cudaMalloc of a %.2f GB population block on device %d: %s",
+                    (double)bytes / 1e9, device, cudaGetErrorString(e));
+    }
+    return MLB_OK;
+}
+
+int mlb_block_free(void *d_ptr)
+{
+    if (!d_ptr) return MLB_OK;
+    cudaPointerAttributes at;
+    int dev = -1;
+    if (cudaPointerGetAttributes(&at, d_ptr) == cudaSuccess && at.type == cudaMemoryTypeDevice)
+        dev = at.device;
+    else
+        (void)cudaGetLastError();
+    if (dev < 0) return fail(MLB_EINVAL, "not a device allocation");
+    MLB_ON_DEVICE(dev);
+    // a pooled block may be handed to the next caller at once: whatever still
+    // uses it must be over (the wait cudaFree implies)
+    MLB_CUDA(cudaDeviceSynchronize());
+    g_blocks.release(d_ptr);
     return MLB_OK;
 }
 

@@ -374,9 +374,23 @@ def run(state, config, on_output=None, on_checkpoint=None, probe=None):
     if _wants_slabs(config):
         return _run_slabs(state, config, on_output, on_checkpoint, probe)
     own = state.session is None
-    sess = open_session(state, config)
+    if not own and state.session.inplace != bool(config.inplace):
+        raise ValueError(
+            f"state is resident with inplace={state.session.inplace} but the run asks for "
+            f"inplace={bool(config.inplace)}: close the session first (state.session.close())")
     if not own:
-        sess.upload()  # the host arrays are the truth at the start of a run
+        tile = config.schedule.resolve(state.nx, state.ny, state.nz, state.layout)
+        if tile is not None and tuple(tile) != tuple(state.session.plan.tile):
+            raise ValueError(
+                f"state is resident with tile {state.session.plan.tile} but the run asks for "
+                f"{tuple(tile)}: close the session first (state.session.close())")
+    sess = open_session(state, config)
+    if not own and not sess.host_stale:
+        # A resident state whose host arrays are current: the caller may have
+        # edited them, so they are the truth at the start of a run (as in the
+        # reference).  When the DEVICE holds the newest populations (steps were
+        # advanced since the last sync) it is the truth and nothing is uploaded.
+        sess.upload()
     plan = sess.plan
     dev = plan.device
     end_t = state.t + config.steps
@@ -414,6 +428,14 @@ def run(state, config, on_output=None, on_checkpoint=None, probe=None):
                     on_checkpoint(state)
         sess.sync_host()
         torch.cuda.current_stream(dev).synchronize()
+    except BaseException:
+        # leave the host arrays at the step `state.t` names (the reference's
+        # diverged populations are visible in state.f_pre at the reported step)
+        try:
+            sess.sync_host()
+        except Exception:
+            pass
+        raise
     finally:
         if own:
             sess.close(sync=False)
@@ -436,6 +458,26 @@ def _wants_slabs(config):
         raise ValueError("RunConfig(distributed=True) needs an initialised torch.distributed "
                          "process group with more than one rank (launch with torchrun)")
     return on
+
+
+def _same_job_on_every_rank(state, config):
+    """The slab run treats the ranks' states as ONE global domain.  A process
+    group may exist for other reasons (a sweep with one simulation per rank):
+    decompose only if every rank holds the same problem, else raise on all."""
+    import hashlib
+    import torch.distributed as dist
+    p = state.params
+    card = (state.nx, state.ny, state.nz, state.t, state.precision.token,
+            None if p is None else float(p.omega), tuple(float(v) for v in state.wall_u),
+            float(state.inlet_u), int(config.steps), bool(config.inplace),
+            hashlib.blake2b(np.ascontiguousarray(state.mask), digest_size=16).hexdigest())
+    cards = [None] * dist.get_world_size()
+    dist.all_gather_object(cards, card)
+    if any(c != cards[0] for c in cards):
+        raise ValueError(
+            "engine.run found a torch.distributed process group but the ranks hold different "
+            "problems (shape, step, physics or mask differ), so this is not one z-decomposed "
+            "domain: pass RunConfig(distributed=False) to run one simulation per rank")
 
 
 def _run_slabs(state, config, on_output, on_checkpoint, probe):
@@ -461,6 +503,7 @@ def _run_slabs(state, config, on_output, on_checkpoint, probe):
     if state.params.has_source:
         raise ValueError("the fused kernel runs the zero-source path only")
     rank, world = dist.get_rank(), dist.get_world_size()
+    _same_job_on_every_rank(state, config)
     nx, ny, nz = state.nx, state.ny, state.nz
     z0, z1 = slab.partition(nz, world)[rank]
     n = z1 - z0

@@ -53,8 +53,35 @@ def _host_ptr(a):
     return ctypes.c_void_p(a.ctypes.data)
 
 
+class _LibBlock:
+    """`nbytes` of cudaMalloc memory from the library (mlb_block_alloc), seen by
+    torch through `__cuda_array_interface__`.  The z-slab exchange exports
+    population blocks over CUDA IPC, which needs plain cudaMalloc allocations:
+    taking them from the library keeps that independent of how torch's caching
+    allocator is configured (expandable segments, cudaMallocAsync).  The tensor
+    made from this object keeps it alive; the memory goes back to the library
+    when the last reference dies."""
+
+    def __init__(self, lib, device_index, nbytes, shape, typestr):
+        ptr = ctypes.c_void_p()
+        _cabi.check(lib.mlb_block_alloc(int(device_index), int(nbytes), ctypes.byref(ptr)))
+        self._lib, self.ptr, self.nbytes = lib, ptr.value, int(nbytes)
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (self.ptr, False), "strides": None,
+                                         "version": 2}
+
+    def __del__(self):
+        ptr, self.ptr = getattr(self, "ptr", None), None
+        if ptr:
+            try:
+                self._lib.mlb_block_free(ctypes.c_void_p(ptr))
+            except Exception:   # interpreter shutdown
+                pass
+
+
 class DeviceField:
-    """One population block in the padded device layout, owned by torch.
+    """One population block in the padded device layout; torch views memory
+    the library allocated (`KernelPlan.alloc`).
 
     `tensor` has shape (19, nz+2, ny, xp); storage plane 0 and nz+1 are the
     halo planes, slab plane lz is storage plane lz+1, xp is nx rounded up
@@ -189,10 +216,21 @@ class KernelPlan:
         return int(self._layout.bytes)
 
     def alloc(self, zero=False):
-        """A caller-owned device population block (torch owns the memory)."""
-        make = torch.zeros if zero else torch.empty
-        t = make(self.field_shape, dtype=_torch_dtype(self.precision),
-                 device=self.device)
+        """A caller-owned device population block: cudaMalloc memory from the
+        library (exportable over CUDA IPC whatever torch's allocator is set to),
+        wrapped as a torch tensor that keeps it alive."""
+        typestr = {Precision.SINGLE: "<f4", Precision.DOUBLE: "<f8", Precision.MIXED1: "<f2",
+                   Precision.MIXED2: "<f4"}[self.precision]
+        try:
+            block = _LibBlock(self._lib, self.device.index, self.field_bytes, self.field_shape,
+                              typestr)
+        except MemoryError:
+            torch.cuda.empty_cache()   # let torch's cache go, then once more
+            block = _LibBlock(self._lib, self.device.index, self.field_bytes, self.field_shape,
+                              typestr)
+        t = torch.as_tensor(block, device=self.device)
+        if zero:
+            t.zero_()
         return DeviceField(t, self.nx, self.ny, self.nz)
 
     def device_flags(self):
@@ -241,6 +279,11 @@ class KernelPlan:
         to the strict never-written mode, but every store is a full line."""
         self.passthrough = bool(on)
         _cabi.check(self._lib.mlb_plan_set_passthrough(self._plan, int(self.passthrough)))
+
+    def set_graph(self, mode):
+        """CUDA graphs in `run_steps` / `run_steps_inplace`: -1 auto (small,
+        launch-bound domains), 0 never, 1 always.  Never changes bits."""
+        _cabi.check(self._lib.mlb_plan_set_graph(self._plan, int(mode)))
 
     def set_prefetch(self, cells):
         """L2 prefetch distance of the pack kernels in cells (-1 auto, 0 off);

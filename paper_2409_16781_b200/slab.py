@@ -179,6 +179,25 @@ class PeerRing:
         return ((self.below["blocks"][k], self.below["nz"]),
                 (self.above["blocks"][k], self.above["nz"]))
 
+    def c_ring(self, first, overlap):
+        """This rank's view of the ring as the library's `mlb_ring`, for the
+        one-call loops (mlb_slab_run_steps*): `first` is the local block that
+        plays d_a (index 0 of the struct's block arrays)."""
+        from . import _cabi
+        r = _cabi.Ring()
+        order = [first] + [k for k in range(len(self.blocks)) if k != first]
+        for j, k in enumerate(order):
+            r.below[j] = self.below["blocks"][k]
+            r.above[j] = self.above["blocks"][k]
+        r.nz_below, r.nz_above = self.below["nz"], self.above["nz"]
+        # I am the slab ABOVE my below-neighbour, and BELOW my above-neighbour
+        r.post_below = self.below["sig"] + self.SLOT_FROM_ABOVE
+        r.post_above = self.above["sig"] + self.SLOT_FROM_BELOW
+        r.wait_below = self.sig + self.SLOT_FROM_BELOW
+        r.wait_above = self.sig + self.SLOT_FROM_ABOVE
+        r.t, r.wait_mode, r.overlap = self.t, self.wait_mode, int(bool(overlap))
+        return r
+
     def _stream(self):
         return self._ct.c_void_p(torch.cuda.current_stream(self.plan.device).cuda_stream)
 
@@ -238,8 +257,13 @@ class DistSlab:
     """
 
     def __init__(self, stepper, nz_local, rank=0, world=1, group=None,
-                 overlap=True, ring=None, force_dist=False):
+                 overlap=True, ring=None, force_dist=False, c_loop=True):
         self.stepper = stepper
+        # with a peer ring, `run` / `run_inplace` hand the whole loop to the
+        # library (mlb_slab_run_steps*: the same schedule as `step`, no Python
+        # between steps); c_loop=False keeps the step-by-step Python schedule
+        self.c_loop = bool(c_loop)
+        self.host_us_per_step = None   # of the last one-call loop
         self.nz = int(nz_local)
         self.rank, self.world, self.group = rank, world, group
         self.below, self.above = ring_neighbours(rank, world)
@@ -375,9 +399,26 @@ class DistSlab:
             main.wait_event(done)
         f.repr ^= 1
 
+    def _loop_args(self):
+        import ctypes
+        st = self.stepper
+        main = ctypes.c_void_p(torch.cuda.current_stream(st.device).cuda_stream)
+        hi = ctypes.c_void_p(st.hi.cuda_stream)
+        return ctypes, main, hi, ctypes.c_double(0.0)
+
     def run_inplace(self, f, nsteps):
-        for _ in range(nsteps):
-            self.step_inplace(f)
+        if self.ring is None or not self.c_loop:
+            for _ in range(nsteps):
+                self.step_inplace(f)
+            return f
+        from . import _cabi
+        ct, main, hi, us = self._loop_args()
+        ring = self.ring.c_ring(self.ring.index(f), self.overlap)
+        r = ct.c_int(f.repr)
+        _cabi.check(_cabi.lib().mlb_slab_run_steps_inplace(
+            self.stepper.plan._plan, f.ptr, int(nsteps), ct.byref(r), ct.byref(ring), main, hi,
+            ct.byref(us)))
+        f.repr, self.ring.t, self.host_us_per_step = r.value, int(ring.t), us.value
         return f
 
     def normalize(self, f):
@@ -411,6 +452,15 @@ class DistSlab:
 
     def run(self, a, b, nsteps):
         """`nsteps` steps alternating a -> b -> a; returns (newest, other)."""
+        if self.ring is not None and self.c_loop and self.cuda:
+            from . import _cabi
+            ct, main, hi, us = self._loop_args()
+            ring = self.ring.c_ring(self.ring.index(a), self.overlap)
+            _cabi.check(_cabi.lib().mlb_slab_run_steps(
+                self.stepper.plan._plan, a.ptr, b.ptr, int(nsteps), ct.byref(ring), main, hi,
+                ct.byref(us)))
+            self.ring.t, self.host_us_per_step = int(ring.t), us.value
+            return (a, b) if nsteps % 2 == 0 else (b, a)
         pre, post = a, b
         for _ in range(nsteps):
             self.step(pre, post)

@@ -107,3 +107,25 @@ def to_xyzq(block, nx, ny, nz):
 def from_xyzq(a):
     nx, ny, nz, _ = a.shape
     return np.ascontiguousarray(a.transpose(3, 2, 1, 0).reshape(19, nz * ny * nx))
+
+
+def init_ranks(rank, world, port):
+    """Process-group + device setup of a multi-process GPU test.  On a box with
+    at least `world` GPUs every rank takes its own device and the control plane
+    is NCCL - the exchange then really crosses NVLink; on a smaller box all
+    ranks share device 0 over a gloo control plane (separate CUDA contexts,
+    real IPC mappings, same protocol).  Returns (device index, the device
+    argument for slab.exchange_flag_halos: None = host tensors)."""
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if torch.cuda.device_count() >= world and os.environ.get("MLB_TEST_SHARE_GPU") != "1":
+        dev = rank
+        torch.cuda.set_device(dev)
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", dev))
+        return dev, torch.device("cuda", dev)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    return 0, None

@@ -193,3 +193,60 @@ def test_bench_sweep_protocol_and_survival():
     assert recs[2].error == "" and recs[2].inplace and recs[2].mlups > 5.0
     with pytest.raises(ValueError, match="reps"):
         perfport.bench_sweep([good], reps=0)
+
+
+def test_run_on_a_resident_state_keeps_the_device_steps():
+    """A state made resident and advanced on the device holds its newest
+    populations THERE: a following engine.run must continue from them, not
+    from the stale host arrays (k + n steps == the oracle's k + n), and must
+    refuse a configuration the resident session was not built for."""
+    from oracle.cpu import CpuOracle
+    spec = CaseSpec("ldc", 20, 18, 14, re=80.0, u0=0.08)
+    for inplace in (False, True):
+        state = cases.init(spec, Precision.DOUBLE)
+        f0 = state.f_pre.data.copy()
+        sess = engine.open_session(state, RunConfig(steps=1, precision=Precision.DOUBLE,
+                                                    inplace=inplace))
+        sess.advance(5)
+        assert state.t == 5 and sess.host_stale
+        engine.run(state, RunConfig(steps=4, precision=Precision.DOUBLE, inplace=inplace))
+        assert state.t == 9
+        want = CpuOracle(20, 18, 14, state.mask, state.params.omega, state.wall_u).run(
+            f0.copy(), f0.copy(), 9)
+        np.testing.assert_array_equal(state.f_pre.data, want)
+        # host arrays current again: an edit made now IS the truth of the next run
+        state.f_pre.data[:] = f0
+        state.t = 0
+        engine.run(state, RunConfig(steps=9, precision=Precision.DOUBLE, inplace=inplace))
+        np.testing.assert_array_equal(state.f_pre.data, want)
+        with pytest.raises(ValueError, match="close the session first"):
+            engine.run(state, RunConfig(steps=1, precision=Precision.DOUBLE, inplace=not inplace))
+        with pytest.raises(ValueError, match="close the session first"):
+            engine.run(state, RunConfig(steps=1, precision=Precision.DOUBLE, inplace=inplace,
+                                        schedule=Schedule("tiled", 32, 2, 2)))
+        sess.close()
+
+
+def test_divergence_leaves_the_diverged_populations_in_the_host_arrays():
+    """engine.py:258-259 of the reference raises with the diverged populations
+    in state.f_pre at the reported step; here the host arrays are synchronised
+    on the way out, so `t` and the data agree."""
+    spec = CaseSpec("ldc", 16, 16, 12, re=50.0, u0=0.05)
+    state = cases.init(spec, Precision.SINGLE)
+    state.f_pre.data[3, 1234] = np.nan
+    with pytest.raises(engine.DivergenceError, match="divergence at step 2"):
+        engine.run(state, RunConfig(steps=4, output_every=2))
+    assert state.t == 2
+    assert np.isnan(state.f_pre.data).sum() > 1     # the NaN has spread: these are step-2 data
+
+
+def test_entry_points_leave_the_current_device_alone():
+    """The library selects the plan's device per call and restores the caller's."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two visible GPUs")
+    torch.cuda.set_device(0)
+    spec = CaseSpec("ldc", 16, 16, 12, re=50.0, u0=0.05)
+    state = cases.init(spec, Precision.SINGLE)
+    engine.run(state, RunConfig(steps=3, device=1))
+    assert torch.cuda.current_device() == 0

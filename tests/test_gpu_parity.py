@@ -342,3 +342,48 @@ def test_engine_run_on_chained_outlets_falls_back_to_strict_stores(tag, rng):
     engine.run(state, engine.RunConfig(steps=9, precision=prec))
     want = make_oracle(grid, 1.2, wall_u, inlet_u).run(f0.copy(), f0.copy(), 9)
     np.testing.assert_array_equal(state.f_pre.data, want)
+
+
+@pytest.mark.parametrize("tag", ["f32", "f64", "f16"])
+def test_graph_replay_never_changes_bits(tag):
+    """mlb_run_steps / mlb_run_steps_inplace replay runs of steps from a CUDA
+    graph on small domains (mlb_plan_set_graph): the very launches of the plain
+    loop, so the same bits - for run lengths around the 32-step graph unit, odd
+    and even, two blocks and in place, with walls and open boundaries."""
+    from paper_2409_16781_b200.kernels import KernelPlan
+    prec = {"f64": Precision.DOUBLE, "f32": Precision.SINGLE, "f16": Precision.MIXED1}[tag]
+    for geom in ("cavity16", "channel40"):
+        grid, wall_u, inlet_u = geometries3d()[geom]
+        nx, ny, nz = grid.shape
+        flags = B.flatten_mask(grid)
+        f = random_block(np.random.default_rng(20240917), grid.size, prec.storage)
+        want = {}
+        for steps in (9, 32, 71):
+            for graph in (0, 1):
+                plan = KernelPlan(nx, ny, nz, Layout.ROW, prec, flags, 1.3, wall_u, inlet_u=inlet_u)
+                plan.set_graph(graph)
+                a, b = plan.alloc(), plan.alloc()
+                plan.upload(f, a)
+                plan.upload(f, b)
+                newest, _, _ = plan.run_steps(a, b, steps)
+                got = np.empty_like(f)
+                plan.download(newest, got)
+                if graph == 0:
+                    want[steps] = got
+                else:
+                    np.testing.assert_array_equal(got, want[steps])
+                    # a second call reuses the cached graph (same blocks, same plan state)
+                    newest2, _, _ = plan.run_steps(newest, b if newest is a else a, steps)
+                    # and in place, from both representations
+                    c = plan.alloc()
+                    plan.upload(f, c)
+                    plan.set_variant(1008 if tag != "f16" else 2008)
+                    plan.run_steps_inplace(c, 1)            # now shifted: the replay starts from repr 1
+                    plan.run_steps_inplace(c, steps - 1)
+                    plan.normalize(c)
+                    got = np.empty_like(f)
+                    plan.download(c, got)
+                    np.testing.assert_array_equal(got, want[steps])
+                plan.close()
+    orc = CpuOracle(nx, ny, nz, flags, 1.3, wall_u, inlet_u)
+    np.testing.assert_array_equal(orc.run(f.copy(), f.copy(), 71), want[71])

@@ -1,11 +1,13 @@
-"""The fused peer-store halo exchange across PROCESSES: two ranks, each with
-its own CUDA context, map each other's population blocks and step counters
-through CUDA IPC and run the real DistSlab + PeerRing driver.  The box has one
-GPU, so both ranks share device 0 - the memory mapping, the in-kernel stores
-into the neighbour's halo planes and the stream-ordered signal protocol are
-exactly what runs with one rank per GPU; only the wire (same-device instead
-of NVLink) differs.  The control plane (handle exchange, barriers) is gloo.
-The gathered result must be BITWISE the single-domain run."""
+"""The fused peer-store halo exchange across PROCESSES: two or three ranks,
+each with its own CUDA context, map each other's population blocks and step
+counters through CUDA IPC and run the real DistSlab + PeerRing driver.  On a
+box with enough GPUs every rank takes its own device (rank % device_count,
+NCCL control plane) and the stores cross NVLink; on a one-GPU box all ranks
+share device 0 - the memory mapping, the in-kernel stores into the
+neighbour's halo planes and the stream-ordered signal protocol are exactly
+what runs with one rank per GPU; only the wire differs - with a gloo control
+plane (helpers.init_ranks).  The gathered result must be BITWISE the
+single-domain run."""
 
 import os
 import signal
@@ -18,7 +20,7 @@ from oracle.cpu import CpuOracle
 from paper_2409_16781_b200 import boundaries as B
 from paper_2409_16781_b200.fields import Layout, Precision
 
-from .helpers import geometries3d, random_block
+from .helpers import geometries3d, init_ranks, random_block
 
 pytestmark = pytest.mark.gpu
 
@@ -29,16 +31,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, geom, tag, steps, omega, wait_mode, overlap, passthrough, out_dir):
+def _worker(rank, world, port, geom, tag, steps, omega, wait_mode, overlap, passthrough, out_dir,
+            c_loop=True):
     signal.alarm(240)  # a protocol bug must not hang the box
-    import torch
     import torch.distributed as dist
     from paper_2409_16781_b200 import slab
     from paper_2409_16781_b200.kernels import KernelPlan
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    _, fdev = init_ranks(rank, world, port)
     try:
-        torch.cuda.set_device(0)
         grid, wall_u, inlet_u = geometries3d()[geom]
         prec = {"f64": Precision.DOUBLE, "f32": Precision.SINGLE, "f16": Precision.MIXED1}[tag]
         nx, ny, nz = grid.shape
@@ -46,7 +46,7 @@ def _worker(rank, world, port, geom, tag, steps, omega, wait_mode, overlap, pass
         f = random_block(np.random.default_rng(20240917), grid.size, prec.storage)
         z0, z1 = slab.partition(nz, world)[rank]
         n = z1 - z0
-        lo, hi = slab.exchange_flag_halos(flags[z0:z1], rank, world)
+        lo, hi = slab.exchange_flag_halos(flags[z0:z1], rank, world, device=fdev)
         plan = KernelPlan(nx, ny, n, Layout.ROW, prec, flags[z0:z1], omega, wall_u,
                           inlet_u=inlet_u, halo_lo=lo, halo_hi=hi, slab=True)
         part = np.ascontiguousarray(f.reshape(19, nz, ny, nx)[:, z0:z1]).reshape(19, -1)
@@ -60,7 +60,8 @@ def _worker(rank, world, port, geom, tag, steps, omega, wait_mode, overlap, pass
             except ValueError:
                 pass
         ring = slab.PeerRing(plan, blocks, rank, world, wait_mode=wait_mode)
-        runner = slab.DistSlab(slab.CudaStepper(plan), n, rank, world, overlap=overlap, ring=ring)
+        runner = slab.DistSlab(slab.CudaStepper(plan), n, rank, world, overlap=overlap, ring=ring,
+                               c_loop=c_loop)
         runner.exchange(blocks[0])
         newest, _ = runner.run(blocks[0], blocks[1], steps)
         runner.finish()
@@ -72,7 +73,7 @@ def _worker(rank, world, port, geom, tag, steps, omega, wait_mode, overlap, pass
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("wait_mode", [0, 2])
+@pytest.mark.parametrize("wait_mode,c_loop", [(0, True), (2, True), (0, False)])
 @pytest.mark.parametrize("geom,tag,world,overlap,passthrough", [
     ("cavity_oblique_lid", "f64", 2, False, False),
     ("cavity16", "f32", 2, True, True),
@@ -82,7 +83,10 @@ def _worker(rank, world, port, geom, tag, steps, omega, wait_mode, overlap, pass
     ("periodic8", "f16", 2, False, True),
     ("cavity16", "f32", 3, False, True),
 ])
-def test_peer_ring_across_processes(geom, tag, world, overlap, passthrough, wait_mode, tmp_path):
+def test_peer_ring_across_processes(geom, tag, world, overlap, passthrough, wait_mode, c_loop,
+                                    tmp_path):
+    """c_loop: the whole loop in one library call (mlb_slab_run_steps, the
+    default) or the same schedule driven step by step from Python."""
     import torch.multiprocessing as mp
     steps, omega = 7, 1.3
     grid, wall_u, inlet_u = geometries3d()[geom]
@@ -92,7 +96,7 @@ def test_peer_ring_across_processes(geom, tag, world, overlap, passthrough, wait
     want = CpuOracle(nx, ny, nz, B.flatten_mask(grid), omega, wall_u, inlet_u).run(
         f.copy(), f.copy(), steps)
     mp.spawn(_worker, args=(world, _free_port(), geom, tag, steps, omega, wait_mode, overlap,
-                            passthrough, str(tmp_path)), nprocs=world, join=True)
+                            passthrough, str(tmp_path), c_loop), nprocs=world, join=True)
     got = np.concatenate([np.load(tmp_path / f"slab{r}.npy") for r in range(world)], axis=1)
     np.testing.assert_array_equal(got.reshape(19, -1), want)
 
@@ -148,13 +152,10 @@ def test_send_recv_transport_over_nccl(geom, tmp_path):
 
 def _engine_worker(rank, world, port, case, tag, out_dir, inplace=False):
     signal.alarm(240)
-    import torch
     import torch.distributed as dist
     from paper_2409_16781_b200 import cases, engine
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    init_ranks(rank, world, port)
     try:
-        torch.cuda.set_device(0)
         prec = {"f64": Precision.DOUBLE, "f32": Precision.SINGLE}[tag]
         spec = (cases.CaseSpec("ldc", 24, 20, 17, re=100.0, u0=0.1) if case == "ldc"
                 else cases.CaseSpec("ldc", 128, 12, 9, re=100.0, u0=0.1) if case == "ldc128"
@@ -201,16 +202,14 @@ def test_engine_run_is_the_same_call_under_torch_distributed(case, tag, world, i
     assert all((tmp_path / f"ok{r}").exists() for r in range(world))
 
 
-def _inplace_worker(rank, world, port, geom, tag, variant, steps, overlap, wait_mode, out_dir):
+def _inplace_worker(rank, world, port, geom, tag, variant, steps, overlap, wait_mode, out_dir,
+                    c_loop=True):
     signal.alarm(240)
-    import torch
     import torch.distributed as dist
     from paper_2409_16781_b200 import slab
     from paper_2409_16781_b200.kernels import KernelPlan
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    _, fdev = init_ranks(rank, world, port)
     try:
-        torch.cuda.set_device(0)
         grid, wall_u, inlet_u = geometries3d()[geom]
         prec = {"f64": Precision.DOUBLE, "f32": Precision.SINGLE, "f16": Precision.MIXED1}[tag]
         nx, ny, nz = grid.shape
@@ -218,7 +217,7 @@ def _inplace_worker(rank, world, port, geom, tag, variant, steps, overlap, wait_
         f = random_block(np.random.default_rng(20240917), grid.size, prec.storage)
         z0, z1 = slab.partition(nz, world)[rank]
         n = z1 - z0
-        lo, hi = slab.exchange_flag_halos(flags[z0:z1], rank, world)
+        lo, hi = slab.exchange_flag_halos(flags[z0:z1], rank, world, device=fdev)
         plan = KernelPlan(nx, ny, n, Layout.ROW, prec, flags[z0:z1], 1.3, wall_u,
                           inlet_u=inlet_u, halo_lo=lo, halo_hi=hi, slab=True)
         plan.set_variant(variant)
@@ -227,7 +226,8 @@ def _inplace_worker(rank, world, port, geom, tag, variant, steps, overlap, wait_
         blk.tensor.fill_(float("nan"))
         plan.upload(part, blk)
         ring = slab.PeerRing(plan, [blk], rank, world, wait_mode=wait_mode)
-        runner = slab.DistSlab(slab.CudaStepper(plan), n, rank, world, overlap=overlap, ring=ring)
+        runner = slab.DistSlab(slab.CudaStepper(plan), n, rank, world, overlap=overlap, ring=ring,
+                               c_loop=c_loop)
         runner.exchange(blk)
         runner.run_inplace(blk, steps)
         runner.normalize(blk)
@@ -239,16 +239,16 @@ def _inplace_worker(rank, world, port, geom, tag, variant, steps, overlap, wait_
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("geom,tag,variant,world,steps,overlap,wait_mode", [
-    ("cavity16", "f32", 1008, 2, 7, False, 0),
-    ("cavity16", "f32", 1016, 2, 6, True, 2),
-    ("porous", "f64", 1008, 3, 5, False, 0),
-    ("channel40", "f32", 1008, 2, 7, False, 0),
-    ("periodic8", "f16", 2008, 2, 4, False, 0),
-    ("porous", "f32", 1008, 2, 9, True, 0),
+@pytest.mark.parametrize("geom,tag,variant,world,steps,overlap,wait_mode,c_loop", [
+    ("cavity16", "f32", 1008, 2, 7, False, 0, True),
+    ("cavity16", "f32", 1016, 2, 6, True, 2, True),
+    ("porous", "f64", 1008, 3, 5, False, 0, True),
+    ("channel40", "f32", 1008, 2, 7, False, 0, False),
+    ("periodic8", "f16", 2008, 2, 4, False, 0, True),
+    ("porous", "f32", 1008, 2, 9, True, 0, False),
 ])
 def test_inplace_slabs_across_processes(geom, tag, variant, world, steps, overlap, wait_mode,
-                                        tmp_path):
+                                        c_loop, tmp_path):
     """One block per rank: the in-place update over z-slabs, ranks in separate
     processes writing into each other's boundary planes (pull half) and halo
     planes (local half) through CUDA IPC mappings."""
@@ -260,6 +260,19 @@ def test_inplace_slabs_across_processes(geom, tag, variant, world, steps, overla
     want = CpuOracle(nx, ny, nz, B.flatten_mask(grid), 1.3, wall_u, inlet_u).run(
         f.copy(), f.copy(), steps)
     mp.spawn(_inplace_worker, args=(world, _free_port(), geom, tag, variant, steps, overlap,
-                                    wait_mode, str(tmp_path)), nprocs=world, join=True)
+                                    wait_mode, str(tmp_path), c_loop), nprocs=world, join=True)
     got = np.concatenate([np.load(tmp_path / f"slab{r}.npy") for r in range(world)], axis=1)
     np.testing.assert_array_equal(got.reshape(19, -1), want)
+
+
+def test_peer_ring_does_not_depend_on_the_torch_allocator(tmp_path, monkeypatch):
+    """The population blocks are cudaMalloc memory from the library
+    (KernelPlan.alloc -> mlb_block_alloc), so they can be exported over CUDA IPC
+    even when torch's caching allocator runs with expandable segments (whose
+    blocks cannot): engine.run over 2 ranks still takes the peer-memory ring
+    (the worker asserts transport == "peer")."""
+    import torch.multiprocessing as mp
+    monkeypatch.setenv("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+    mp.spawn(_engine_worker, args=(2, _free_port(), "ldc", "f32", str(tmp_path), False),
+             nprocs=2, join=True)
+    assert all((tmp_path / f"ok{r}").exists() for r in range(2))

@@ -267,3 +267,99 @@ def test_ldc1024_maximum_sizes_in_place_and_two_buffer():
     plan.close()
     del f
     torch.cuda.empty_cache()
+
+
+def _oracle_window(spec_args, prec, steps, inplace=False, threads=16):
+    """engine.run at a BASELINE size against the CPU oracle, bitwise."""
+    import torch
+    from paper_2409_16781_b200 import cases, engine
+    spec = cases.CaseSpec(*spec_args[0], **spec_args[1])
+    state = cases.init(spec, prec)
+    f0 = state.f_pre.data.copy()
+    engine.run(state, engine.RunConfig(steps=steps, precision=prec, inplace=inplace))
+    orc = CpuOracle(spec.nx, spec.ny, spec.nz, state.mask, state.params.omega, state.wall_u,
+                    state.inlet_u, threads=threads)
+    want = orc.run(f0, f0.copy(), steps)
+    same = np.array_equal(state.f_pre.data, want)
+    if not same:
+        bad = np.argwhere(state.f_pre.data != want)
+        raise AssertionError(f"{len(bad)} populations differ from the oracle, first at {bad[0]}")
+    del want, f0, state
+    torch.cuda.empty_cache()
+
+
+def test_ldc512_fp32_oracle_window():
+    """configs[2] exactly as bench.py times it - LDC 512^3 fp32, Re 1000, the
+    default variant (16-byte packs), automatic prefetch distance, pass-through
+    stores, cavity walls on 512-wide rows - 3 steps through engine.run against
+    the CPU oracle, BITWISE (the reference's one-step / five-step kernel-vs-
+    oracle tests, pkg/tests/test_kernels.py:45-79, at the headline size)."""
+    _oracle_window((("ldc", 512, 512, 512), dict(re=1000.0, u0=0.1)), Precision.SINGLE, 3)
+
+
+def test_ldc512_fp32_in_place_oracle_window():
+    """The same configuration on ONE block (pull half, local half, pull half,
+    then the swap back to the normal representation)."""
+    _oracle_window((("ldc", 512, 512, 512), dict(re=1000.0, u0=0.1)), Precision.SINGLE, 3,
+                   inplace=True)
+
+
+def test_ldc512_fp64_oracle_window():
+    _oracle_window((("ldc", 512, 512, 512), dict(re=1000.0, u0=0.1)), Precision.DOUBLE, 2)
+
+
+def test_ldc1024_slab_oracle_window():
+    """configs[3]'s plane shape: a 1024 x 1024 x 16 z-slab of the 1024^3 cavity
+    WITH its halo planes (the slab that holds the cavity floor: solid plane
+    below, fluid above), 3 steps with the halos refilled from a neighbouring
+    oracle-stepped domain - i.e. the oracle runs the 1024 x 1024 x 20 piece and
+    the CUDA slab must reproduce its 16 inner planes bit for bit, fed only
+    through its halo planes."""
+    import torch
+    from paper_2409_16781_b200 import slab
+    from paper_2409_16781_b200.kernels import KernelPlan
+    from paper_2409_16781_b200.lattice import omega_from_reynolds
+    n, nzt, steps = 1024, 24, 3
+    omega = omega_from_reynolds(1000.0, 0.1, n).omega
+    grid = B.cavity_mask(n, n, nzt)          # solid shell, lid on y = n-1; walls at z = 0, nzt-1
+    flags = B.flatten_mask(grid).reshape(nzt, n, n)
+    f = np.empty((19, nzt * n * n), dtype=np.float32)
+    prng = np.random.default_rng(20240917)
+    for q in range(19):   # a smooth non-trivial state: weights with a 1 % random ripple
+        f[q] = (L.W[q] * (1.0 + 0.01 * prng.standard_normal(nzt * n * n))).astype(np.float32)
+    orc = CpuOracle(n, n, nzt, flags, omega, (0.1, 0.0, 0.0), threads=16)
+    # slab [z0, z1) of the piece; the oracle supplies the halo planes every step
+    z0, z1 = 0, 16
+    lo, hi = slab.slab_halo_flags(flags, n, n, z0, z1)
+    plan = KernelPlan(n, n, z1 - z0, Layout.ROW, Precision.SINGLE, flags[z0:z1], omega,
+                      (0.1, 0.0, 0.0), halo_lo=lo, halo_hi=hi, slab=True)
+    a, b = plan.alloc(), plan.alloc()
+    f4 = f.reshape(19, nzt, n, n)
+    part = np.ascontiguousarray(f4[:, z0:z1]).reshape(19, -1)
+    plan.upload(part, a)
+    plan.upload(part, b)
+    plan.set_passthrough(True)
+
+    def fill_halos(blk, full):
+        v = full.reshape(19, nzt, n, n)
+        t = blk.tensor
+        for q in L.UP:
+            t[q, 0, :, :n] = torch.from_numpy(v[q, (z0 - 1) % nzt]).to(t.device)
+        for q in L.DOWN:
+            t[q, z1 - z0 + 1, :, :n] = torch.from_numpy(v[q, z1 % nzt]).to(t.device)
+
+    cur, nxt = f, f.copy()
+    pre, post = a, b
+    fill_halos(pre, cur)
+    for _ in range(steps):
+        plan.step_open_range(pre, post, 0, z1 - z0)
+        orc.step(cur, nxt)
+        orc.open_pass(nxt)
+        cur, nxt = nxt, cur
+        pre, post = post, pre
+        fill_halos(pre, cur)
+    got = np.empty_like(part)
+    plan.download(pre, got)
+    want = np.ascontiguousarray(cur.reshape(19, nzt, n, n)[:, z0:z1]).reshape(19, -1)
+    np.testing.assert_array_equal(got, want)
+    plan.close()

@@ -28,10 +28,15 @@ def test_only_tests_smoke_and_the_bench_cpu_arm_use_the_oracle():
     for name in os.listdir(tools):
         if name.endswith(".py"):
             assert not pat.search(open(os.path.join(tools, name)).read()), f"tools/{name}"
-    # bench.py: inside cpu_arm only; __graft_entry__.py: inside smoke only
+    # bench.py: only as the timed CPU arm (cpu_arm) and as the CHECKER of the GPU result
+    # (parity_and_cpu_baseline at N = 1, preflight at N > 1) - never inside the functions
+    # that produce the GPU numbers; __graft_entry__.py: inside smoke only
     bench = open(os.path.join(ROOT, "bench.py")).read()
+    allowed = {bench.find("\ndef " + fn) for fn in ("cpu_arm", "parity_and_cpu_baseline",
+                                                      "preflight")}
+    assert -1 not in allowed
     assert [m.start() for m in pat.finditer(bench)] and all(
-        bench.rfind("\ndef ", 0, m.start()) == bench.find("\ndef cpu_arm") for m in pat.finditer(bench))
+        bench.rfind("\ndef ", 0, m.start()) in allowed for m in pat.finditer(bench))
     entry = open(os.path.join(ROOT, "__graft_entry__.py")).read()
     assert all(entry.rfind("\ndef ", 0, m.start()) == entry.find("\ndef smoke")
                for m in pat.finditer(entry))
