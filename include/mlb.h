@@ -360,6 +360,28 @@ int mlb_probe(const mlb_plan *plan, const void *d_f, int x, int y, int lz,
 int mlb_step_host(mlb_plan *plan, const void *h_fpre, void *h_fpost,
                   void *d_a, void *d_b, void *stream);
 
+/* engine.run on a host-resident state in ONE call (engine.py:218-275: the
+ * reference's run is upload-free because it lives on the host; here the host
+ * block is what the caller holds before and after).  Equivalent to mlb_upload
+ * (h_in -> d_a), d_b := d_a, nsteps x (fused update, open-boundary pass, swap),
+ * mlb_download(newest -> h_out), synchronised - same bits - but when planes 0
+ * and nz-1 of the domain are walls (no update depends on the periodic wrap in
+ * z) the three phases OVERLAP: the domain is cut into chunks of `chunk_planes`
+ * z planes (0 = automatic) which are uploaded on one copy stream, stepped
+ * time-skewed behind the upload front (step s of chunk c right after step s-1
+ * of chunk c+1), and downloaded on a second copy stream as soon as their last
+ * step is done, while later chunks still arrive.  h_in / h_out are dense
+ * (19, N) blocks, pinned for the copies to be asynchronous; they may be the same
+ * block.  h_flags (dense [nz][ny][nx], may be NULL if the plan has flags) is
+ * handed to mlb_plan_set_flags while the first chunks are in flight.  Turns
+ * pass-through stores on when the geometry allows them (the two blocks are
+ * identical by construction).  *ms (may be NULL): device time of the whole call;
+ * *overlapped (may be NULL): 1 if the skewed schedule ran, 0 if the plain
+ * sequence did (periodic z, fewer than 4 chunks). */
+int mlb_run_steps_host(mlb_plan *plan, const void *h_in, void *h_out, void *d_a, void *d_b,
+                       int nsteps, int chunk_planes, const uint8_t *h_flags, void *stream,
+                       float *ms, int *overlapped);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <type_traits>
 #include <vector>
 
 namespace {
@@ -217,6 +218,11 @@ struct mlb_plan {
     // z-slab schedule (mlb_slab_run_steps): fork / join between the main and the
     // boundary stream
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // host-resident runs (mlb_run_steps_host): planes 0 and nz-1 hold no fluid /
+    // open-boundary cell, so no update depends on the periodic wrap in z and the
+    // domain can be stepped chunk by chunk behind the upload
+    bool z_closed = false;
+    cudaStream_t up_stream = nullptr, down_stream = nullptr;
 };
 
 namespace {
@@ -321,8 +327,12 @@ void inlet_values(double u_in, T *e)
 // thread with that block width; W * 1000 + LX = packs of (16 >> (W - 1)) bytes
 // (W = 1: 16 B = 4 floats / 2 doubles; W = 2: 8 B = 4 halves; W = 3: 4 B =
 // 2 halves) with LX = 8 / 16 / 32 packs per warp row.
+constexpr int VARIANT_STAGED = 4000;   // step_stage_kernel: rows staged through shared memory
+
 int pack_cells(int dtype, int variant)
 {
+    if (variant == VARIANT_STAGED)   // 16-byte packs, 8 bytes with fp16 / fp32-for-fp64 storage
+        return dtype == MLB_F32 ? 4 : dtype == MLB_F16 ? 4 : 2;
     const int bytes = 16 >> (variant / 1000 - 1);
     const int sz = dtype == MLB_F64 ? 8 : dtype == MLB_F16 ? 2 : 4;
     return bytes / sz;
@@ -331,7 +341,7 @@ int pack_cells(int dtype, int variant)
 bool variant_exists(int dtype, int variant)
 {
     if (variant == 0 || variant == 32 || variant == 64 || variant == 128 || variant == 256
-        || variant == 512)
+        || variant == 512 || variant == VARIANT_STAGED)
         return true;
     const int w = variant / 1000, lx = variant % 1000;
     if (lx != 8 && lx != 16 && lx != 32)
@@ -345,12 +355,32 @@ bool variant_exists(int dtype, int variant)
     return w == 1;
 }
 
+// The staged kernel works on tiles of TY whole (padded) rows with STAGE_NT threads:
+// it needs xp / V threads per row to divide STAGE_NT, whole tiles per plane, and
+// the tile (19 populations + kind bytes) to fit shared memory twice per SM.
+constexpr int STAGE_NT = 256;
+bool stage_shape(const mlb_plan *p, int &ty, size_t &smem)
+{
+    const int V = pack_cells(p->dtype, VARIANT_STAGED);
+    const long long tpr = p->lay.xp / V;
+    if (p->lay.xp % V || tpr < 32 || tpr > STAGE_NT || STAGE_NT % tpr)
+        return false;
+    ty = (int)(STAGE_NT / tpr);
+    if (p->ny % ty)
+        return false;
+    smem = (size_t)ty * ((size_t)MLB_Q * p->lay.xp * p->lay.itemsize + p->lay.xp);
+    return smem <= (100u << 10);
+}
+
 // the kernel `variant` resolves to for this plan (0 = auto); measured on B200
 // with tools/sweep.py: packs win in fp32 and fp16 storage, not in fp64
-int resolve_variant(const mlb_plan *p)
+int resolve_variant(const mlb_plan *p, bool allow_staged = true)
 {
-    if (p->variant != 0)
-        return p->variant;
+    if (p->variant != 0 && !(p->variant == VARIANT_STAGED && !allow_staged)) {
+        int ty; size_t smem;
+        if (p->variant != VARIANT_STAGED || stage_shape(p, ty, smem))
+            return p->variant;
+    }
     if (p->dtype == MLB_F32 && p->nx % 4 == 0 && p->nx >= 128)
         return 1016;
     if (p->dtype == MLB_F32 && p->nx % 2 == 0 && p->nx >= 128)
@@ -459,12 +489,12 @@ template <typename TS, int V, bool PUSH>
 int launch_vec(mlb_plan *p, const mlb::StepArgs<TS> &a, const mlb::PushArgs<TS> &ph, int lx,
                int nplanes, cudaStream_t st)
 {
-    if (p->nx % V != 0)
-        return fail(MLB_EINVAL, "this vectorised kernel needs nx %% %d == 0", V);
     const int rows = 128 / lx;  // rows per 128-thread block
-    // pass-through launches cover the padded row (see step_vec_kernel)
+    // pass-through launches cover the padded row (see step_vec_kernel); a row the
+    // pack does not divide ends in a pack of real cells + padding
     const long long cols = a.passthrough ? p->lay.xp : p->nx;
-    const dim3 grid((unsigned)((cols / V + lx - 1) / lx), (p->ny + rows - 1) / rows, nplanes);
+    const dim3 grid((unsigned)(((cols + V - 1) / V + lx - 1) / lx), (p->ny + rows - 1) / rows,
+                    nplanes);
     if (lx == 8) mlb::step_vec_kernel<TS, V, 8, PUSH><<<grid, 128, 0, st>>>(a, ph);
     else if (lx == 16) mlb::step_vec_kernel<TS, V, 16, PUSH><<<grid, 128, 0, st>>>(a, ph);
     else mlb::step_vec_kernel<TS, V, 32, PUSH><<<grid, 128, 0, st>>>(a, ph);
@@ -491,12 +521,36 @@ int launch_scalar(mlb_plan *p, const mlb::StepArgs<TS> &a, const mlb::PushArgs<T
     return MLB_OK;
 }
 
+template <typename TS, int V>
+int launch_stage(mlb_plan *p, const mlb::StepArgs<TS> &a, int nplanes, cudaStream_t st)
+{
+    int ty = 0;
+    size_t smem = 0;
+    if (!stage_shape(p, ty, smem))
+        return fail(MLB_EUNSUPPORTED, "the staged kernel does not fit this grid");
+    static const int tpb_env = std::getenv("MLB_STAGE_TPB") ? std::atoi(std::getenv("MLB_STAGE_TPB")) : 0;
+    const int tiles = nplanes * (p->ny / ty);
+    const int tpb = tpb_env > 0 ? tpb_env : 16;
+    auto kernel = mlb::step_stage_kernel<TS, V, STAGE_NT>;
+    MLB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kernel<<<(tiles + tpb - 1) / tpb, STAGE_NT, smem, st>>>(a, ty, tpb, tiles);
+    MLB_LAUNCHED();
+    return MLB_OK;
+}
+
 template <typename TS, int V1, int V2, bool PUSH>
 int launch_typed(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cudaStream_t st,
                  bool fuse_open, int variant, const PushTarget *push)
 {
     mlb::StepArgs<TS> a;
     fill_args<TS>(p, fpre, fpost, z0, fuse_open, a);
+    if (variant == VARIANT_STAGED) {
+        if constexpr (!PUSH) {
+            a.pf_dz = a.pf_dy = 0;
+            constexpr int V = sizeof(TS) == 8 || std::is_same<TS, mlb::f32w>::value ? 2 : 4;
+            return launch_stage<TS, V>(p, a, z1 - z0, st);
+        }
+    }
     mlb::PushArgs<TS> ph{};
     if (PUSH)
         fill_push<TS>(p, *push, ph);
@@ -520,7 +574,8 @@ int launch_typed(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cud
 int launch_step(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cudaStream_t st,
                 bool fuse_open = false, const PushTarget *push = nullptr)
 {
-    const int variant = resolve_variant(p);
+    // (a launch that also pushes into the neighbours' halos keeps the direct kernel)
+    const int variant = resolve_variant(p, push == nullptr);
     if (!variant_exists(p->dtype, variant))
         return fail(MLB_EINVAL, "kernel variant %d does not exist for dtype code %d", variant,
                     p->dtype);
@@ -640,7 +695,7 @@ int launch_aa_vec_lx(mlb_plan *p, void *f, int kind, int lx, const AaRange &r, c
 // length allows)
 int resolve_aa_variant(const mlb_plan *p)
 {
-    if (p->variant != 0)
+    if (p->variant != 0 && p->variant != VARIANT_STAGED)
         return p->variant;
     if (p->dtype == MLB_F32 && p->nx % 4 == 0 && p->nx >= 128) return 1016;
     if (p->dtype == MLB_F32 && p->nx % 2 == 0 && p->nx >= 128) return 2016;
@@ -854,6 +909,8 @@ int mlb_plan_destroy(mlb_plan *p)
     if (p->ev_join) cudaEventDestroy(p->ev_join);
     if (p->gc.exec) cudaGraphExecDestroy(p->gc.exec);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+    if (p->up_stream) cudaStreamDestroy(p->up_stream);
+    if (p->down_stream) cudaStreamDestroy(p->down_stream);
     delete p;
     return MLB_OK;
 }
@@ -899,7 +956,10 @@ const char *mlb_plan_kernel_name(const mlb_plan *p)
     const int v = resolve_variant(p);
     const char *t = p->dtype == MLB_F32 ? "float" : p->dtype == MLB_F64 ? "double"
                   : p->dtype == MLB_F32C64 ? "f32w" : "__half";
-    if (v >= 1000)
+    if (v == VARIANT_STAGED)
+        snprintf(name, sizeof(name), "mlb::step_stage_kernel<%s, %d, %d>", t,
+                 pack_cells(p->dtype, v), STAGE_NT);
+    else if (v >= 1000)
         snprintf(name, sizeof(name), "mlb::step_vec_kernel<%s, %d, %d, false>", t,
                  pack_cells(p->dtype, v), v % 1000);
     else
@@ -987,6 +1047,15 @@ int mlb_plan_set_flags(mlb_plan *p, const uint8_t *h_flags, const uint8_t *h_lo,
     MLB_CUDA(cudaMemcpy(census, d_census, sizeof(census), cudaMemcpyDeviceToHost));
     pool_free(d_census);
 
+    {
+        auto wall_plane = [&](const uint8_t *pl) {
+            for (size_t i = 0; i < dense_plane; ++i)
+                if (pl[i] != 1 && pl[i] != 2) return false;
+            return true;
+        };
+        p->z_closed = p->z_mode == MLB_Z_PERIODIC && nz >= 2 && wall_plane(h_flags)
+                      && wall_plane(h_flags + (size_t)(nz - 1) * dense_plane);
+    }
     std::vector<long long> in_idx, out_idx;
     p->in_zoff.assign(nz + 1, 0);
     p->out_zoff.assign(nz + 1, 0);
@@ -1506,7 +1575,7 @@ int mlb_step_push_range(mlb_plan *p, const void *d_fpre, void *d_fpost, int z0, 
     const bool any = t.below || t.above;
     MLB_ON_DEVICE(p->device);
     const bool open_cells = p->in_zoff[z1] > p->in_zoff[z0] || p->out_zoff[z1] > p->out_zoff[z0];
-    const bool fuse = can_fuse_open(p, resolve_variant(p));
+    const bool fuse = can_fuse_open(p, resolve_variant(p, !any));   // the kernel launch_step picks
     if (!open_cells || fuse)
         return launch_step(p, d_fpre, d_fpost, z0, z1, S(stream), fuse, any ? &t : nullptr);
     // list-driven open-boundary pass: it rewrites cells of the boundary plane
@@ -1751,6 +1820,192 @@ int mlb_step_host(mlb_plan *p, const void *h_fpre, void *h_fpost, void *d_a, voi
     if (int rc = mlb_download(p, d_b, h_fpost, stream)) return rc;
     MLB_CUDA(cudaStreamSynchronize(S(stream)));
     return MLB_OK;
+}
+
+// ---- a whole run on HOST blocks, transfers overlapped with the steps ------------
+// engine.run on a host-resident state (engine.py:218-275) is upload, K steps,
+// download; at PCIe speed the two transfers of a 512^3 fp32 block take 0.19 s
+// each, the 20 steps between them 0.06 s.  When the domain is closed in z (planes
+// 0 and nz-1 are walls: no update depends on the periodic wrap) the three phases
+// can overlap.  The domain is cut into chunks of z planes and the steps are
+// time-skewed: step s of chunk c runs at tick c + s, right after step s-1 of
+// chunk c+1 (same stream, so the planes it still reads in the block it will
+// overwrite have been consumed).  Chunk u is uploaded at tick u on a copy
+// stream; chunk c's final populations are downloaded on a second copy stream
+// as soon as its last step is done - while later chunks are still arriving
+// (PCIe is full duplex).  Every cell sees exactly the launches of the plain
+// loop restricted to its plane range, so the result is the plain loop's, bit
+// for bit.  At most SKEW_MAX steps ride on each transfer (the kernels must keep
+// up with the link); the steps in between run as plain whole-domain launches.
+namespace {
+
+constexpr int SKEW_MAX = 40;
+
+struct ChunkCopy {
+    const mlb_plan *p;
+    int z0, z1;
+    // one strided copy for all 19 populations when rows are not padded
+    cudaError_t run(void *dst, const void *src, cudaMemcpyKind kind, cudaStream_t st) const
+    {
+        const int sz = p->lay.itemsize;
+        const size_t row = (size_t)p->nx * sz, rows = (size_t)(z1 - z0) * p->ny;
+        const size_t dense_pop = (size_t)p->nz * p->ny * row;
+        const size_t dev_pop = (size_t)p->lay.pop * sz, dev_row = (size_t)p->lay.xp * sz;
+        const size_t hoff = (size_t)z0 * p->ny * row, doff = ((size_t)z0 + 1) * p->lay.plane * sz;
+        const bool h2d = kind == cudaMemcpyHostToDevice, d2d = kind == cudaMemcpyDeviceToDevice;
+        if (d2d)
+            return cudaMemcpy2DAsync((char *)dst + doff, dev_pop, (const char *)src + doff, dev_pop,
+                                     rows * dev_row, MLB_Q, kind, st);
+        if (p->lay.xp == p->nx)
+            return h2d ? cudaMemcpy2DAsync((char *)dst + doff, dev_pop, (const char *)src + hoff,
+                                           dense_pop, rows * row, MLB_Q, kind, st)
+                       : cudaMemcpy2DAsync((char *)dst + hoff, dense_pop, (const char *)src + doff,
+                                           dev_pop, rows * row, MLB_Q, kind, st);
+        for (int q = 0; q < MLB_Q; ++q) {
+            const cudaError_t e =
+                h2d ? cudaMemcpy2DAsync((char *)dst + q * dev_pop + doff, dev_row,
+                                        (const char *)src + q * dense_pop + hoff, row, row, rows,
+                                        kind, st)
+                    : cudaMemcpy2DAsync((char *)dst + q * dense_pop + hoff, row,
+                                        (const char *)src + q * dev_pop + doff, dev_row, row, rows,
+                                        kind, st);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
+};
+
+}  // namespace
+
+int mlb_run_steps_host(mlb_plan *p, const void *h_in, void *h_out, void *d_a, void *d_b,
+                       int nsteps, int chunk_planes, const uint8_t *h_flags, void *stream,
+                       float *ms, int *overlapped)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (!h_in || !h_out || !d_a || !d_b || d_a == d_b)
+        return fail(MLB_EINVAL, "need host source / destination and two distinct device blocks");
+    if (nsteps < 0) return fail(MLB_EINVAL, "nsteps < 0");
+    if (p->z_mode != MLB_Z_PERIODIC)
+        return fail(MLB_EUNSUPPORTED, "mlb_run_steps_host needs an MLB_Z_PERIODIC plan");
+    if (!p->have_flags && !h_flags)
+        return fail(MLB_EINVAL, "plan has no flags and none were passed");
+    MLB_ON_DEVICE(p->device);
+    cudaStream_t cs = S(stream);
+    if (!p->up_stream) MLB_CUDA(cudaStreamCreateWithFlags(&p->up_stream, cudaStreamNonBlocking));
+    if (!p->down_stream) MLB_CUDA(cudaStreamCreateWithFlags(&p->down_stream, cudaStreamNonBlocking));
+    const int nz = p->nz;
+    int cz = chunk_planes > 0 ? chunk_planes : (nz + 127) / 128;
+    // a chunk of a population should stay at least 1 MB (copy efficiency)
+    while (cz < nz && (size_t)cz * p->lay.plane * p->lay.itemsize < (1u << 20)) ++cz;
+    const int C = (nz + cz - 1) / cz;
+    auto zlo = [&](int c) { return c * cz; };
+    auto zhi = [&](int c) { return (c + 1) * cz < nz ? (c + 1) * cz : nz; };
+
+    if (ms) MLB_CUDA(cudaEventRecord(p->ev0, cs));
+    // The flag tables first.  (Enqueuing the uploads first and building the tables
+    // "meanwhile" does not work: the flag copy queues behind every chunk already
+    // handed to the copy engine, and the first kernel would wait for the whole
+    // upload - measured 0.40 s instead of 0.27 s for 20 steps at 512^3.)
+    if (!p->have_flags)
+        if (int rc = mlb_plan_set_flags(p, h_flags, nullptr, nullptr)) return rc;
+    std::vector<cudaEvent_t> up(C, nullptr), done(C, nullptr);
+    auto cleanup = [&]() {
+        for (cudaEvent_t e : up) if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : done) if (e) cudaEventDestroy(e);
+    };
+#define MLB_CUDA_C(expr)                                                        \
+    do {                                                                        \
+        cudaError_t e_ = (expr);                                                \
+        if (e_ != cudaSuccess) {                                                \
+            cleanup();                                                          \
+            return fail(MLB_ECUDA, "%s: %s (%s:%d)", #expr,                     \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);            \
+        }                                                                       \
+    } while (0)
+    // (the copy stream starts after whatever the caller enqueued before)
+    MLB_CUDA_C(cudaEventRecord(p->ev_fork, cs));
+    MLB_CUDA_C(cudaStreamWaitEvent(p->up_stream, p->ev_fork, 0));
+    MLB_CUDA_C(cudaStreamWaitEvent(p->down_stream, p->ev_fork, 0));
+    for (int c = 0; c < C; ++c) {
+        MLB_CUDA_C(cudaEventCreateWithFlags(&up[c], cudaEventDisableTiming));
+        MLB_CUDA_C(cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming));
+        const ChunkCopy cc{p, zlo(c), zhi(c)};
+        MLB_CUDA_C(cc.run(d_a, h_in, cudaMemcpyHostToDevice, p->up_stream));
+        MLB_CUDA_C(cudaEventRecord(up[c], p->up_stream));
+    }
+    // both blocks identical from here on (engine.py:148): pass-through stores are valid
+    // unless the geometry chains outlet cells
+    p->passthrough = p->out_chained ? 0 : 1;
+    ++p->epoch;
+
+    const bool skew = p->z_closed && C >= 4 && nsteps >= 1;
+    if (overlapped) *overlapped = skew ? 1 : 0;
+    void *blk[2] = {d_a, d_b};
+    int rc = MLB_OK;
+    auto download = [&](int c, void *src) -> cudaError_t {
+        cudaError_t e = cudaEventRecord(done[c], cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(p->down_stream, done[c], 0);
+        if (e == cudaSuccess)
+            e = ChunkCopy{p, zlo(c), zhi(c)}.run(h_out, src, cudaMemcpyDeviceToHost, p->down_stream);
+        return e;
+    };
+    // one time-skewed sweep of `S` steps starting from block `from`; uploads ride on
+    // it when `with_up`, downloads when `with_down`
+    auto sweep = [&](int S, int from, bool with_up, bool with_down) -> int {
+        for (int u = 0; u < C + S; ++u) {
+            if (with_up && u < C) {
+                MLB_CUDA(cudaStreamWaitEvent(cs, up[u], 0));
+                MLB_CUDA((ChunkCopy{p, zlo(u), zhi(u)}.run(d_b, d_a, cudaMemcpyDeviceToDevice, cs)));
+            }
+            for (int s = 1; s <= S; ++s) {
+                const int c = u - s;
+                if (c < 0 || c >= C) continue;
+                void *pre = blk[(from + s - 1) & 1], *post = blk[(from + s) & 1];
+                if (int r = mlb_step_open_range(p, pre, post, zlo(c), zhi(c), stream)) return r;
+                if (s == S && with_down) MLB_CUDA(download(c, post));
+            }
+        }
+        return MLB_OK;
+    };
+    if (skew) {
+        const int s1 = nsteps < SKEW_MAX ? nsteps : SKEW_MAX;
+        const int rest = nsteps - s1;
+        const int s3 = rest < SKEW_MAX ? rest : SKEW_MAX, s2 = rest - s3;
+        rc = sweep(s1, 0, true, rest == 0);
+        int at = s1 & 1;
+        for (int t = 0; t < s2 && rc == MLB_OK; ++t, at ^= 1)
+            rc = one_step(p, blk[at], blk[at ^ 1], stream);
+        if (rc == MLB_OK && s3 > 0) rc = sweep(s3, at, false, true);
+    } else {
+        // no overlap possible (periodic in z, or a tiny domain): the plain sequence
+        for (int c = 0; c < C && rc == MLB_OK; ++c) {
+            cudaError_t e = cudaStreamWaitEvent(cs, up[c], 0);
+            if (e == cudaSuccess)
+                e = ChunkCopy{p, zlo(c), zhi(c)}.run(d_b, d_a, cudaMemcpyDeviceToDevice, cs);
+            if (e != cudaSuccess) rc = fail(MLB_ECUDA, "chunk copy: %s", cudaGetErrorString(e));
+        }
+        int at = 0;
+        for (int t = 0; t < nsteps && rc == MLB_OK; ++t, at ^= 1)
+            rc = one_step(p, blk[at], blk[at ^ 1], stream);
+        for (int c = 0; c < C && rc == MLB_OK; ++c) {
+            const cudaError_t e = download(c, blk[at]);
+            if (e != cudaSuccess) rc = fail(MLB_ECUDA, "download: %s", cudaGetErrorString(e));
+        }
+    }
+    if (rc == MLB_OK) {
+        // join: the caller's stream ends after the last download
+        cudaError_t e = cudaEventRecord(p->ev_join, p->down_stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, p->ev_join, 0);
+        if (e == cudaSuccess && ms) e = cudaEventRecord(p->ev1, cs);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+        if (e == cudaSuccess && ms) e = cudaEventElapsedTime(ms, p->ev0, p->ev1);
+        if (e != cudaSuccess) rc = fail(MLB_ECUDA, "mlb_run_steps_host: %s", cudaGetErrorString(e));
+    } else {
+        cudaDeviceSynchronize();
+    }
+    cleanup();
+#undef MLB_CUDA_C
+    return rc;
 }
 
 // ---- peer memory: CUDA IPC mapping and stream-ordered signals --------------

@@ -859,50 +859,18 @@ __device__ __forceinline__ void pull_pack(const TS *__restrict__ row, int x0, in
     }
 }
 
-template <typename TS, int V, int LX, bool PUSH>
-__global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
-                                                          const PushArgs<TS> ph)
+// What follows the loads of a pack, shared by the direct kernel (step_vec_kernel)
+// and the staged one (step_stage_kernel): class words, link-bit patching, collide,
+// pass-through / open-boundary substitution, stores, fused halo push.  `g` holds
+// the pulled populations of the pack's V cells, `kpack` their kind bytes, `d` the
+// pack's offset inside a population, `o_plane` its offset inside the plane.
+template <typename TS, int V, bool PUSH>
+__device__ __forceinline__ void vec_finish(const StepArgs<TS> &a, const PushArgs<TS> &ph,
+                                           typename Store<TS>::C (&g)[Q][V], const uint32_t kpack,
+                                           const int d, const int o_plane, const int lz)
 {
     using T = typename Store<TS>::C;
-    constexpr int RPW = 32 / LX;        // rows per warp
     const Geom &gm = a.g;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int x0 = (blockIdx.x * LX + (lane % LX)) * V;
-    const int y = blockIdx.y * (4 * RPW) + warp * RPW + lane / LX;
-    const int lz = a.z0 + blockIdx.z;
-    const int xp = (int)gm.xp, plane = (int)gm.plane;
-    // Pass-through mode also rewrites the row padding (kind 1: "solid", holds
-    // whatever the block was allocated with, read by nobody): the last line of a
-    // row whose length is not a multiple of 128 bytes is then stored whole instead
-    // of leaving a partial sector for L2 to complete with a DRAM read.
-    if (x0 >= (a.passthrough ? xp : gm.nx) || y >= gm.ny)
-        return;
-
-    const int zc = (lz + 1) * plane;
-    const int zm = ((lz == 0) ? gm.zlo_src : lz) * plane;
-    const int zq = ((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) * plane;
-    const int ym = (y == 0) ? gm.ny - 1 : y - 1;
-    const int yq = (y == gm.ny - 1) ? 0 : y + 1;
-    const int rc = y * xp, rm = ym * xp, rq = yq * xp;
-    const int xl = (x0 == 0) ? gm.nx - 1 : x0 - 1;
-    const int xr = (x0 + V >= gm.nx) ? 0 : x0 + V;
-    const int d = zc + rc + x0;
-
-    // kind bytes of the pack and all pulls, issued together
-    const uint32_t kpack = KindIO<V>::load(a.ct.kind + d);
-    T g[Q][V];
-    PackIO<TS, V>::load(a.pre[0] + d, g[0]);
-#define MLB_X(i, CX, Z, R) pull_pack<TS, V, CX>(a.pre[i] + ((Z) + (R)), x0, xl, xr, g[i]);
-    MLB_DIRS(MLB_X)
-#undef MLB_X
-
-    if (a.pf_bulk) {
-        if (blockIdx.x == 0 && threadIdx.x < Q && (a.pf_dz | a.pf_dy) != 0)
-            prefetch_rows<TS, true>(a.pre, gm, a.pf_dz, a.pf_dy, blockIdx.y * (4 * RPW), 4 * RPW, lz,
-                                    threadIdx.x);
-    } else
-        prefetch_ahead<TS, V, LX, true>(a.pre, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
-
     // class words: all zero for a pack of bulk cells (the usual case), else from
     // the dictionary.  (A separate code path for bulk packs was measured and is
     // slower: warps that mix bulk and wall packs then run the collide twice.)
@@ -1008,7 +976,7 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
         const bool lo = lz == 0 && ph.lo[0] != nullptr;
         const bool hi = lz == gm.nz - 1 && ph.hi[0] != nullptr;
         if (lo || hi) {
-            const int o = rc + x0;
+            const int o = o_plane;
 #pragma unroll
             for (int j = 0; j < 5; ++j) {
                 if (allfluid || a.passthrough) {
@@ -1023,6 +991,229 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
                         }
                 }
             }
+        }
+    }
+}
+
+template <typename TS, int V, int LX, bool PUSH>
+__global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
+                                                          const PushArgs<TS> ph)
+{
+    using T = typename Store<TS>::C;
+    constexpr int RPW = 32 / LX;        // rows per warp
+    const Geom &gm = a.g;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int x0 = (blockIdx.x * LX + (lane % LX)) * V;
+    const int y = blockIdx.y * (4 * RPW) + warp * RPW + lane / LX;
+    const int lz = a.z0 + blockIdx.z;
+    const int xp = (int)gm.xp, plane = (int)gm.plane;
+    // Pass-through mode also rewrites the row padding (kind 1: "solid", holds
+    // whatever the block was allocated with, read by nobody): the last line of a
+    // row whose length is not a multiple of 128 bytes is then stored whole instead
+    // of leaving a partial sector for L2 to complete with a DRAM read.
+    if (x0 >= (a.passthrough ? xp : gm.nx) || y >= gm.ny)
+        return;
+
+    const int zc = (lz + 1) * plane;
+    const int zm = ((lz == 0) ? gm.zlo_src : lz) * plane;
+    const int zq = ((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) * plane;
+    const int ym = (y == 0) ? gm.ny - 1 : y - 1;
+    const int yq = (y == gm.ny - 1) ? 0 : y + 1;
+    const int rc = y * xp, rm = ym * xp, rq = yq * xp;
+    const int xl = (x0 == 0) ? gm.nx - 1 : x0 - 1;
+    const int xr = (x0 + V >= gm.nx) ? 0 : x0 + V;
+    const int d = zc + rc + x0;
+
+    // kind bytes of the pack and all pulls, issued together
+    const uint32_t kpack = KindIO<V>::load(a.ct.kind + d);
+    T g[Q][V];
+    PackIO<TS, V>::load(a.pre[0] + d, g[0]);
+#define MLB_X(i, CX, Z, R) pull_pack<TS, V, CX>(a.pre[i] + ((Z) + (R)), x0, xl, xr, g[i]);
+    MLB_DIRS(MLB_X)
+#undef MLB_X
+    // rows whose length the pack does not divide: the cell at x = nx-1 sits inside
+    // the last pack, and its x+1 neighbour is cell 0 of the row, not the padding
+    if (x0 + V > gm.nx) {
+        const int js = gm.nx - 1 - x0;
+#define MLB_X(i, CX, Z, R)                                                           \
+        if (CX < 0) {                                                                \
+            const T w0 = Store<TS>::up((a.pre[i] + ((Z) + (R)))[0]);                 \
+            _Pragma("unroll") for (int j = 0; j < V - 1; ++j)                        \
+                if (j == js) g[i][j] = w0;                                           \
+        }
+        MLB_DIRS(MLB_X)
+#undef MLB_X
+    }
+
+    if (a.pf_bulk) {
+        if (blockIdx.x == 0 && threadIdx.x < Q && (a.pf_dz | a.pf_dy) != 0)
+            prefetch_rows<TS, true>(a.pre, gm, a.pf_dz, a.pf_dy, blockIdx.y * (4 * RPW), 4 * RPW, lz,
+                                    threadIdx.x);
+    } else
+        prefetch_ahead<TS, V, LX, true>(a.pre, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
+
+    vec_finish<TS, V, PUSH>(a, ph, g, kpack, d, rc + x0, lz);
+}
+
+// ---------------------------------------------------------------------------
+// Staged variant (the north star's "shared-memory or TMA staging of the
+// neighbour planes"): the rows a tile pulls from travel global -> shared memory
+// as 1-D bulk copies (cp.async.bulk, the TMA engine; SASS UBLKCP) that complete
+// on an mbarrier, one tile ahead of the arithmetic.  A tile is TY whole rows of
+// one plane (NT threads = TY rows x xp / V packs); a block walks `tiles_per_block`
+// consecutive tiles.  For each population the TY source rows (shifted by the
+// direction's y / z component, periodic wrap or halo plane exactly as in the
+// direct kernels) are copied WHOLE, so the x shift is an index into the staged
+// row - wrap included, which also serves rows whose length no pack divides.  The
+// kind bytes of the tile ride along.  Per tile:
+//   wait(full)  ->  staged rows -> registers  ->  __syncthreads  ->  warp 0 issues
+//   the NEXT tile's copies into the same buffer  ->  patch / collide / store.
+// The next tile's bytes are therefore in flight during the whole arithmetic
+// phase without holding a register (the direct kernels hold 19 packs per thread
+// across the DRAM round trip, or rely on the L2 prefetch to shorten it).  Meant
+// for the storage modes that are latency- and issue-bound rather than HBM-bound:
+// fp16 storage and fp32 storage with fp64 arithmetic.  Stores, patch loads and
+// everything after the loads are vec_finish: bits cannot differ.
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "MLB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra MLB_DONE;\n"
+        "bra MLB_WAIT;\n"
+        "MLB_DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(__cvta_generic_to_global(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// y / z component of direction i (0 for the rest population)
+__device__ __forceinline__ void dir_yz(int i, int &cy, int &cz)
+{
+    cy = cz = 0;
+#define MLB_X(ii, CX, Z, R)                                                          \
+    if (i == ii) {                                                                   \
+        cy = SEL_##R == SEL_rm ? 1 : SEL_##R == SEL_rq ? -1 : 0;                     \
+        cz = SEL_##Z == SEL_zm ? 1 : SEL_##Z == SEL_zq ? -1 : 0;                     \
+    }
+    MLB_DIRS(MLB_X)
+#undef MLB_X
+}
+
+template <typename TS, int V, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT)
+step_stage_kernel(const StepArgs<TS> a, const int ty, const int tiles_per_block, const int ntiles)
+{
+    using T = typename Store<TS>::C;
+    extern __shared__ __align__(128) unsigned char stage[];
+    __shared__ uint64_t full;
+    const Geom &gm = a.g;
+    const int xp = (int)gm.xp, plane = (int)gm.plane;
+    const int tpr = NT / ty;                       // threads per row = xp / V
+    const int r = threadIdx.x / tpr, x0 = (threadIdx.x - r * tpr) * V;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned rowbytes = (unsigned)xp * (unsigned)sizeof(TS);
+    const int tpp = gm.ny / ty;                    // tiles per plane (the host checks ny % ty == 0)
+    // staged layout: [population][tile row][xp] elements, then [tile row][xp] kind bytes
+    const TS *srow = reinterpret_cast<const TS *>(stage);
+    const uint8_t *skind = stage + (size_t)Q * ty * rowbytes;
+
+    // warp 0 fetches a tile: lane i < 19 the rows of population i, lane 19 the kind bytes
+    auto fetch = [&](int tile) {
+        const int lz = a.z0 + tile / tpp, y0 = (tile - (tile / tpp) * tpp) * ty;
+        if (lane == 0)
+            mbar_expect_tx(&full, (unsigned)ty * ((unsigned)Q * rowbytes + (unsigned)xp));
+        __syncwarp();
+        if (lane < Q) {
+            int cy, cz;
+            dir_yz(lane, cy, cz);
+            const int zs = cz == 0 ? lz + 1
+                         : cz > 0 ? ((lz == 0) ? gm.zlo_src : lz)
+                                  : ((lz == gm.nz - 1) ? gm.zhi_src : lz + 2);
+            const TS *src = a.pre[lane] + (long long)zs * plane;
+            TS *dst = const_cast<TS *>(srow) + (size_t)lane * ty * xp;
+            const int ys0 = y0 - cy;
+            if (ys0 >= 0 && ys0 + ty <= gm.ny) {
+                bulk_g2s(dst, src + (long long)ys0 * xp, (unsigned)ty * rowbytes, &full);
+            } else {
+                for (int k = 0; k < ty; ++k) {
+                    int ys = ys0 + k;
+                    ys = ys < 0 ? ys + gm.ny : ys >= gm.ny ? ys - gm.ny : ys;
+                    bulk_g2s(dst + (size_t)k * xp, src + (long long)ys * xp, rowbytes, &full);
+                }
+            }
+        } else if (lane == Q) {
+            bulk_g2s(const_cast<uint8_t *>(skind),
+                     a.ct.kind + ((long long)(lz + 1) * plane + (long long)y0 * xp),
+                     (unsigned)ty * (unsigned)xp, &full);
+        }
+    };
+
+    if (threadIdx.x == 0) {
+        mbar_init(&full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int first = blockIdx.x * tiles_per_block;
+    const int last = min(first + tiles_per_block, ntiles);
+    if (first >= last)
+        return;
+    if (warp == 0)
+        fetch(first);
+
+    const bool active = x0 < (a.passthrough ? xp : gm.nx);
+    const int xl = (x0 == 0) ? gm.nx - 1 : x0 - 1;
+    const int xr = (x0 + V >= gm.nx) ? 0 : x0 + V;
+    const PushArgs<TS> noph{};
+    for (int tile = first; tile < last; ++tile) {
+        const int lz = a.z0 + tile / tpp, y = (tile - (tile / tpp) * tpp) * ty + r;
+        mbar_wait(&full, (unsigned)(tile - first) & 1u);
+        uint32_t kpack = 0u;
+        T g[Q][V];
+        if (active) {
+            kpack = KindIO<V>::load(skind + (size_t)r * xp + x0);
+            PackIO<TS, V>::load(srow + (size_t)r * xp + x0, g[0]);
+#define MLB_X(i, CX, Z, R) pull_pack<TS, V, CX>(srow + ((size_t)i * ty + r) * xp, x0, xl, xr, g[i]);
+            MLB_DIRS(MLB_X)
+#undef MLB_X
+            if (x0 + V > gm.nx) {   // the pack that holds x = nx-1 of a ragged row (see step_vec_kernel)
+                const int js = gm.nx - 1 - x0;
+#define MLB_X(i, CX, Z, R)                                                           \
+                if (CX < 0) {                                                        \
+                    const T w0 = Store<TS>::up((srow + ((size_t)i * ty + r) * xp)[0]); \
+                    _Pragma("unroll") for (int j = 0; j < V - 1; ++j)                \
+                        if (j == js) g[i][j] = w0;                                   \
+                }
+                MLB_DIRS(MLB_X)
+#undef MLB_X
+            }
+        }
+        __syncthreads();            // every thread holds its pack: the buffer is free again
+        if (warp == 0 && tile + 1 < last)
+            fetch(tile + 1);
+        if (active) {
+            const int o_plane = y * xp + x0;
+            vec_finish<TS, V, false>(a, noph, g, kpack, (lz + 1) * plane + o_plane, o_plane, lz);
         }
     }
 }

@@ -95,6 +95,12 @@ class RunConfig:
     distributed: bool | None = None
     gather: bool = True          # distributed runs: every rank ends with the whole host state
     transport: str = "peer"      # distributed runs: "peer" (fused peer stores) or "nccl"
+    # A run on a host-resident state is upload, steps, download.  None / True: when
+    # nothing has to look at the state in between (no hooks, no probe, two blocks, not
+    # resident) the three phases are overlapped chunk by chunk (mlb_run_steps_host);
+    # RunStats.seconds is then the device time of the WHOLE pipelined call, transfers
+    # included, and RunStats.overlapped says so.  False: always upload, loop, download.
+    overlap_io: bool | None = None
 
     def __post_init__(self):
         if self.steps < 1:
@@ -359,6 +365,7 @@ class RunStats:
     probe_series: np.ndarray | None = None
     probe_samples: np.ndarray | None = None
     transport: str | None = None  # distributed runs: how the halos travelled
+    overlapped: bool = False      # seconds covers upload + steps + download, pipelined
 
 
 def run(state, config, on_output=None, on_checkpoint=None, probe=None):
@@ -374,6 +381,10 @@ def run(state, config, on_output=None, on_checkpoint=None, probe=None):
     if _wants_slabs(config):
         return _run_slabs(state, config, on_output, on_checkpoint, probe)
     own = state.session is None
+    if (own and config.overlap_io is not False and not config.inplace and probe is None
+            and not config.output_every and not config.checkpoint_every
+            and state.f_post_ is None and _closed_in_z(state)):
+        return _run_host_pipelined(state, config)
     if not own and state.session.inplace != bool(config.inplace):
         raise ValueError(
             f"state is resident with inplace={state.session.inplace} but the run asks for "
@@ -447,6 +458,45 @@ def run(state, config, on_output=None, on_checkpoint=None, probe=None):
                     nz=state.nz, mlups=mlups,
                     probe_series=(rec[:, 2].copy() if rec is not None else None),
                     probe_samples=rec)
+
+
+def _closed_in_z(state):
+    """Planes 0 and nz-1 are walls and the domain is deep enough to be cut into
+    at least four chunks of 1 MB or more per population: what the overlapped host
+    run needs (mlb_run_steps_host; the library applies the same rule)."""
+    nz, plane = state.nz, state.nx * state.ny
+    if nz < 4:
+        return False
+    m = state.mask.reshape(nz, plane)
+    walls = (boundaries.SOLID, boundaries.MOVING_WALL)
+    if not (np.isin(m[0], walls).all() and np.isin(m[-1], walls).all()):
+        return False
+    item = state.precision.storage.itemsize
+    line = 128 // item
+    xp = -(-state.nx // line) * line
+    cz = max(-(-nz // 128), -(-(1 << 20) // (state.ny * xp * item)))
+    return -(-nz // min(cz, nz)) >= 4
+
+
+def _run_host_pipelined(state, config):
+    """`run` for a host-resident state that nothing looks at before the end: one
+    library call uploads, steps and downloads, overlapped chunk by chunk when
+    the domain is closed in z (include/mlb.h, mlb_run_steps_host); otherwise
+    the same call performs the plain sequence.  Same bits either way."""
+    plan = build_plan(state, config, defer_flags=True)
+    try:
+        a, b = plan.alloc(), plan.alloc()
+        data = state.f_pre.data
+        _, _, ms, overlapped = plan.run_host(data, data, a, b, config.steps)
+        del a, b
+    finally:
+        plan.close()
+    state.t += config.steps
+    seconds = ms * 1e-3
+    updates = state.nx * state.ny * state.nz * config.steps
+    mlups = updates / (seconds * 1e6) if seconds > 0.0 else float("inf")
+    return RunStats(steps=config.steps, seconds=seconds, nx=state.nx, ny=state.ny,
+                    nz=state.nz, mlups=mlups, overlapped=overlapped)
 
 
 def _wants_slabs(config):

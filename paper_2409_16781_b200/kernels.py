@@ -361,6 +361,26 @@ class KernelPlan:
         newest, other = (a, b) if nsteps % 2 == 0 else (b, a)
         return newest, other, (ms.value if timed else None)
 
+    def run_host(self, host_in, host_out, a, b, nsteps, chunk_planes=0):
+        """A whole run on HOST blocks in one call (mlb_run_steps_host): upload
+        `host_in` into `a`, `nsteps` steps over (a, b), download the newest
+        populations into `host_out` (may be `host_in`) - with the three phases
+        overlapped chunk by chunk when the domain is closed in z.  Hands the
+        flags over on the way if `ensure_flags` has not run yet.  Synchronous.
+        Returns (newest, other, ms of the whole call, overlapped?)."""
+        self._check_host(host_in)
+        self._check_host(host_out)
+        ms, ov = ctypes.c_float(0.0), ctypes.c_int(0)
+        flags = None if self._flags_set else _host_ptr(self.mask)
+        if not self._flags_set and any(h is not None for h in self._halo):
+            raise ValueError("run_host is for whole-domain plans (no halo flag planes)")
+        _cabi.check(self._lib.mlb_run_steps_host(
+            self._plan, _host_ptr(host_in), _host_ptr(host_out), a.ptr, b.ptr, int(nsteps),
+            int(chunk_planes), flags, _stream_ptr(self.device), ctypes.byref(ms), ctypes.byref(ov)))
+        self._flags_set = True
+        newest, other = (a, b) if nsteps % 2 == 0 else (b, a)
+        return newest, other, ms.value, bool(ov.value)
+
     def run_steps_inplace(self, f, nsteps, timed=False):
         """`nsteps` steps on ONE block (the AA pattern): same arithmetic and
         traffic as `run_steps`, half the memory.  Walls only.  `f.repr`

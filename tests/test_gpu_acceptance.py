@@ -223,7 +223,7 @@ def test_run_on_a_resident_state_keeps_the_device_steps():
             engine.run(state, RunConfig(steps=1, precision=Precision.DOUBLE, inplace=not inplace))
         with pytest.raises(ValueError, match="close the session first"):
             engine.run(state, RunConfig(steps=1, precision=Precision.DOUBLE, inplace=inplace,
-                                        schedule=Schedule("tiled", 32, 2, 2)))
+                                        schedule=Schedule("tiled", 16, 2, 2)))
         sess.close()
 
 
@@ -250,3 +250,40 @@ def test_entry_points_leave_the_current_device_alone():
     state = cases.init(spec, Precision.SINGLE)
     engine.run(state, RunConfig(steps=3, device=1))
     assert torch.cuda.current_device() == 0
+
+
+@pytest.mark.parametrize("case,prec,steps", [
+    ("ldc", Precision.SINGLE, 7), ("ldc", Precision.DOUBLE, 3), ("ldc", Precision.MIXED1, 45),
+    ("vks", Precision.SINGLE, 12), ("ldc", Precision.SINGLE, 93), ("vks", Precision.MIXED2, 5)])
+def test_overlapped_host_run_is_the_plain_run(case, prec, steps):
+    """engine.run on a host-resident state overlaps upload, steps and download
+    chunk by chunk (time-skewed, mlb_run_steps_host) when the domain is closed
+    in z.  Same launches per cell, so the same bits as upload / loop / download
+    - compared with that path (RunConfig(overlap_io=False)) and with the CPU
+    oracle, for step counts below and above one skewed sweep (40), with inlet /
+    outlet faces, and with rows that are not whole 128-byte lines."""
+    from oracle.cpu import CpuOracle
+    spec = (CaseSpec("ldc", 256, 96, 160, re=400.0, u0=0.1) if case == "ldc"
+            else CaseSpec("vks", 250, 96, 132, re=100.0, u0=0.06))
+    a = cases.init(spec, prec)
+    f0 = a.f_pre.data.copy()
+    ra = engine.run(a, RunConfig(steps=steps, precision=prec))
+    assert ra.overlapped and a.t == steps
+    b = cases.init(spec, prec)
+    rb = engine.run(b, RunConfig(steps=steps, precision=prec, overlap_io=False))
+    assert not rb.overlapped
+    np.testing.assert_array_equal(a.f_pre.data, b.f_pre.data)
+    if steps <= 12:
+        orc = CpuOracle(spec.nx, spec.ny, spec.nz, a.mask, a.params.omega, a.wall_u, a.inlet_u,
+                        threads=8, compute=np.float64 if prec is Precision.MIXED2 else None)
+        np.testing.assert_array_equal(a.f_pre.data, orc.run(f0, f0.copy(), steps))
+
+
+def test_host_run_that_cannot_overlap_keeps_the_loop_timing():
+    """Periodic in z (or too shallow to cut): the upload / loop / download path,
+    RunStats.seconds = the update loop only, as in the reference."""
+    spec = CaseSpec("tgv", 64, 64, 48, u0=0.05, omega=OMEGA)
+    st = cases.init(spec, Precision.SINGLE)
+    assert not engine.run(st, RunConfig(steps=5)).overlapped
+    st = cases.init(CaseSpec("ldc", 32, 32, 32, re=50.0, u0=0.05), Precision.SINGLE)
+    assert not engine.run(st, RunConfig(steps=5)).overlapped

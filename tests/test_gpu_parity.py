@@ -387,3 +387,101 @@ def test_graph_replay_never_changes_bits(tag):
                 plan.close()
     orc = CpuOracle(nx, ny, nz, flags, 1.3, wall_u, inlet_u)
     np.testing.assert_array_equal(orc.run(f.copy(), f.copy(), 71), want[71])
+
+
+def _stage_geometries():
+    """Grids the staged kernel serves (padded row = 32..256 packs) - walls inside
+    and between packs, a ragged row (100, 250), inlet / outlet faces, and a
+    fully periodic box where the x wrap is live."""
+    prng = np.random.default_rng(11)
+    cav = B.cavity_mask(100, 16, 6)
+    cav[40:47, 5:9, 2:4] = B.SOLID
+    cav[77, 11, 3] = B.MOVING_WALL
+    chan = B.channel_mask(128, 16, 6, B.sphere_cells(128, 16, 6, 6, 30.0, 8.0, 2.5))
+    per = B.open_mask(250, 8, 5)
+    u = prng.random(per.shape)
+    per[u < 0.04] = B.SOLID
+    per[u > 0.98] = B.MOVING_WALL
+    return {"cavity100": (cav, (0.05, 0.0, -0.03), 0.0),
+            "channel128": (chan, (0.0, 0.0, 0.0), 0.06),
+            "periodic250": (per, (0.02, 0.03, -0.04), 0.0)}
+
+
+@pytest.mark.parametrize("mode", ["strict", "passthrough", "slab"])
+@pytest.mark.parametrize("tag", ["f16", "m2", "f32", "f64"])
+@pytest.mark.parametrize("geom", ["cavity100", "channel128", "periodic250"])
+def test_staged_kernel_never_changes_bits(geom, tag, mode, rng):
+    """step_stage_kernel (variant 4000): the rows a tile pulls from are staged
+    in shared memory by bulk copies one tile ahead of the arithmetic.  What
+    follows the loads is the direct kernel's code, so - like tiling in the
+    reference (test_kernels.py:107-126) - it never changes a bit: strict and
+    pass-through stores, fused open-boundary pass, ragged rows, periodic wrap
+    in x / y / z, and z-slabs with halo planes (plane ranges, boundary first)."""
+    from paper_2409_16781_b200 import slab
+    grid, wall_u, inlet_u = _stage_geometries()[geom]
+    prec = PREC[tag]
+    nx, ny, nz = grid.shape
+    f = random_block(rng, grid.size, prec.storage)
+    sentinel = random_block(rng, grid.size, prec.storage)
+    if mode != "strict":
+        sentinel = f.copy()
+    omega, steps = 1.55, 4
+    want = make_oracle(grid, omega, wall_u, inlet_u, prec).run(f.copy(), sentinel.copy(), steps)
+    if mode == "slab":
+        flags = B.flatten_mask(grid).reshape(nz, ny, nx)
+        lo, hi = slab.slab_halo_flags(flags, nx, ny, 0, nz)
+        plan = make_plan(grid, prec, omega, wall_u, inlet_u, halo_lo=lo, halo_hi=hi, slab=True)
+    else:
+        plan = make_plan(grid, prec, omega, wall_u, inlet_u)
+    plan.set_variant(4000)
+    if tag == "f64" and geom == "cavity100":
+        assert "stage" not in plan.kernel_name      # 112-element rows: 56 packs do not tile 256 threads
+    else:
+        assert "step_stage_kernel" in plan.kernel_name
+    plan.set_passthrough(mode != "strict")
+    a, b = plan.alloc(), plan.alloc()
+    a.tensor.fill_(float("nan"))
+    b.tensor.fill_(float("nan"))
+    plan.upload(f, a)
+    plan.upload(sentinel, b)
+    if mode == "slab":
+        runner = slab.DistSlab(slab.CudaStepper(plan), nz)
+        runner.exchange(a)
+        newest, _ = runner.run(a, b, steps)
+    else:
+        newest, _, _ = plan.run_steps(a, b, steps)
+    got = np.empty_like(f)
+    plan.download(newest, got)
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("passthrough", [False, True])
+@pytest.mark.parametrize("tag,variant", [("f32", 1008), ("f32", 1016), ("f32", 2032), ("f16", 2008),
+                                         ("f16", 3016), ("m2", 2016), ("f64", 1008)])
+@pytest.mark.parametrize("shape", [(13, 6, 5), (15, 5, 4), (101, 4, 3), (131, 9, 3)])
+def test_pack_kernels_on_rows_no_pack_divides(shape, tag, variant, passthrough, rng):
+    """Rows whose length the pack does not divide end in a pack of real cells +
+    row padding; the cell at x = nx-1 then sits inside a pack and its x+1
+    neighbour is cell 0 of the row (periodic wrap), not the padding.  Periodic
+    box with scattered walls (the wrap is live) and a closed cavity."""
+    nx, ny, nz = shape
+    prec = PREC[tag]
+    for kind in ("periodic", "cavity"):
+        grid = B.open_mask(nx, ny, nz) if kind == "periodic" else B.cavity_mask(nx, ny, nz)
+        u = np.random.default_rng(nx).random(grid.shape)
+        grid[(u < 0.05) & (grid == B.FLUID)] = B.SOLID
+        grid[(u > 0.97) & (grid == B.FLUID)] = B.MOVING_WALL
+        f = random_block(rng, grid.size, prec.storage)
+        sentinel = f.copy() if passthrough else random_block(rng, grid.size, prec.storage)
+        wall_u = (0.04, -0.02, 0.03)
+        want = make_oracle(grid, 1.7, wall_u, 0.0, prec).run(f.copy(), sentinel.copy(), 3)
+        plan = make_plan(grid, prec, 1.7, wall_u)
+        plan.set_variant(variant)
+        plan.set_passthrough(passthrough)
+        a, b = plan.alloc(), plan.alloc()
+        plan.upload(f, a)
+        plan.upload(sentinel, b)
+        newest, _, _ = plan.run_steps(a, b, 3)
+        got = np.empty_like(f)
+        plan.download(newest, got)
+        np.testing.assert_array_equal(got, want)
