@@ -12,7 +12,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmlb_d3q19.so")
+# (MLB_LIB_PATH: A/B experiments with a second build, tools/ only)
+LIB_PATH = os.environ.get("MLB_LIB_PATH") or os.path.join(_HERE, "libmlb_d3q19.so")
 ABI_VERSION = 2
 
 MLB_F32, MLB_F64, MLB_F16, MLB_F32C64 = 0, 1, 2, 3

@@ -355,21 +355,15 @@ bool variant_exists(int dtype, int variant)
     return w == 1;
 }
 
-// The staged kernel works on tiles of TY whole (padded) rows with STAGE_NT threads:
-// it needs xp / V threads per row to divide STAGE_NT, whole tiles per plane, and
-// the tile (19 populations + kind bytes) to fit shared memory twice per SM.
-constexpr int STAGE_NT = 256;
-bool stage_shape(const mlb_plan *p, int &ty, size_t &smem)
+// The staged kernel (step_stage_kernel): a warp per column of 32 packs; it serves
+// any row length (ragged rows and the periodic wrap are index arithmetic inside
+// the staged segment) as long as a block's staging buffers fit shared memory.
+template <typename TS, int V>
+constexpr size_t stage_smem() { return 4 * (size_t)mlb::StageShape<TS, V>::WARP_BYTES; }
+bool stage_shape(const mlb_plan *p)
 {
-    const int V = pack_cells(p->dtype, VARIANT_STAGED);
-    const long long tpr = p->lay.xp / V;
-    if (p->lay.xp % V || tpr < 32 || tpr > STAGE_NT || STAGE_NT % tpr)
-        return false;
-    ty = (int)(STAGE_NT / tpr);
-    if (p->ny % ty)
-        return false;
-    smem = (size_t)ty * ((size_t)MLB_Q * p->lay.xp * p->lay.itemsize + p->lay.xp);
-    return smem <= (100u << 10);
+    // fp16 storage and fp32 storage / fp64 arithmetic (see StageShape::OK)
+    return (p->dtype == MLB_F16 || p->dtype == MLB_F32C64) && p->nx >= 2;
 }
 
 // the kernel `variant` resolves to for this plan (0 = auto); measured on B200
@@ -377,15 +371,16 @@ bool stage_shape(const mlb_plan *p, int &ty, size_t &smem)
 int resolve_variant(const mlb_plan *p, bool allow_staged = true)
 {
     if (p->variant != 0 && !(p->variant == VARIANT_STAGED && !allow_staged)) {
-        int ty; size_t smem;
-        if (p->variant != VARIANT_STAGED || stage_shape(p, ty, smem))
+        if (p->variant != VARIANT_STAGED || stage_shape(p))
             return p->variant;
     }
-    if (p->dtype == MLB_F32 && p->nx % 4 == 0 && p->nx >= 128)
+    // fp32 and fp16 storage: packs of four cells for any row length - a row the pack
+    // does not divide ends in a pack of real cells + padding (511^3, fraction of the HBM
+    // peak: fp32 0.984 one cell per thread -> 1.002 packs; fp16 storage 0.62 -> see DESIGN)
+    static const int ragged = std::getenv("MLB_RAGGED_PACKS") ? std::atoi(std::getenv("MLB_RAGGED_PACKS")) : 1;
+    if (p->dtype == MLB_F32 && (p->nx % 4 == 0 || ragged) && p->nx >= 128)
         return 1016;
-    if (p->dtype == MLB_F32 && p->nx % 2 == 0 && p->nx >= 128)
-        return 2016;
-    if (p->dtype == MLB_F16 && p->nx % 4 == 0 && p->nx >= 128)
+    if (p->dtype == MLB_F16 && (p->nx % 4 == 0 || ragged) && p->nx >= 128)
         return 2008;
     // fp64: the scalar kernel is ~2 % faster, unless there are open-boundary
     // cells, which only a pack kernel can handle inside the fused pass (~7 %)
@@ -524,16 +519,18 @@ int launch_scalar(mlb_plan *p, const mlb::StepArgs<TS> &a, const mlb::PushArgs<T
 template <typename TS, int V>
 int launch_stage(mlb_plan *p, const mlb::StepArgs<TS> &a, int nplanes, cudaStream_t st)
 {
-    int ty = 0;
-    size_t smem = 0;
-    if (!stage_shape(p, ty, smem))
-        return fail(MLB_EUNSUPPORTED, "the staged kernel does not fit this grid");
-    static const int tpb_env = std::getenv("MLB_STAGE_TPB") ? std::atoi(std::getenv("MLB_STAGE_TPB")) : 0;
-    const int tiles = nplanes * (p->ny / ty);
-    const int tpb = tpb_env > 0 ? tpb_env : 16;
-    auto kernel = mlb::step_stage_kernel<TS, V, STAGE_NT>;
-    MLB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kernel<<<(tiles + tpb - 1) / tpb, STAGE_NT, smem, st>>>(a, ty, tpb, tiles);
+    using SS = mlb::StageShape<TS, V>;
+    static const int rows_env = std::getenv("MLB_STAGE_ROWS") ? std::atoi(std::getenv("MLB_STAGE_ROWS")) : 0;
+    const int rows = rows_env > 0 ? rows_env : 16;           // rows a warp walks: pipeline fill 1 / rows
+    const long long cols = a.passthrough ? p->lay.xp : p->nx;
+    const int ncol = (int)((cols + SS::W - 1) / SS::W);
+    const int nrg = (p->ny + rows - 1) / rows;
+    const long long ntasks = (long long)ncol * nrg * nplanes;
+    const size_t smem = stage_smem<TS, V>();
+    auto kernel = mlb::step_stage_kernel<TS, V>;
+    if (smem > (48u << 10))
+        MLB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kernel<<<(unsigned)((ntasks + 3) / 4), 128, smem, st>>>(a, rows, ncol, nrg, (int)ntasks);
     MLB_LAUNCHED();
     return MLB_OK;
 }
@@ -545,9 +542,10 @@ int launch_typed(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cud
     mlb::StepArgs<TS> a;
     fill_args<TS>(p, fpre, fpost, z0, fuse_open, a);
     if (variant == VARIANT_STAGED) {
-        if constexpr (!PUSH) {
-            a.pf_dz = a.pf_dy = 0;
-            constexpr int V = sizeof(TS) == 8 || std::is_same<TS, mlb::f32w>::value ? 2 : 4;
+        constexpr int V = sizeof(TS) == 8 || std::is_same<TS, mlb::f32w>::value ? 2 : 4;
+        if constexpr (!PUSH && mlb::StageShape<TS, V>::OK) {
+            static const int pf = std::getenv("MLB_STAGE_PF") ? std::atoi(std::getenv("MLB_STAGE_PF")) : 0;
+            if (!pf) a.pf_dz = a.pf_dy = 0;
             return launch_stage<TS, V>(p, a, z1 - z0, st);
         }
     }
@@ -957,8 +955,7 @@ const char *mlb_plan_kernel_name(const mlb_plan *p)
     const char *t = p->dtype == MLB_F32 ? "float" : p->dtype == MLB_F64 ? "double"
                   : p->dtype == MLB_F32C64 ? "f32w" : "__half";
     if (v == VARIANT_STAGED)
-        snprintf(name, sizeof(name), "mlb::step_stage_kernel<%s, %d, %d>", t,
-                 pack_cells(p->dtype, v), STAGE_NT);
+        snprintf(name, sizeof(name), "mlb::step_stage_kernel<%s, %d>", t, pack_cells(p->dtype, v));
     else if (v >= 1000)
         snprintf(name, sizeof(name), "mlb::step_vec_kernel<%s, %d, %d, false>", t,
                  pack_cells(p->dtype, v), v % 1000);

@@ -1056,151 +1056,144 @@ __global__ void __launch_bounds__(128, 4) step_vec_kernel(const StepArgs<TS> a,
 }
 
 // ---------------------------------------------------------------------------
-// Staged variant (the north star's "shared-memory or TMA staging of the
-// neighbour planes"): the rows a tile pulls from travel global -> shared memory
-// as 1-D bulk copies (cp.async.bulk, the TMA engine; SASS UBLKCP) that complete
-// on an mbarrier, one tile ahead of the arithmetic.  A tile is TY whole rows of
-// one plane (NT threads = TY rows x xp / V packs); a block walks `tiles_per_block`
-// consecutive tiles.  For each population the TY source rows (shifted by the
-// direction's y / z component, periodic wrap or halo plane exactly as in the
-// direct kernels) are copied WHOLE, so the x shift is an index into the staged
-// row - wrap included, which also serves rows whose length no pack divides.  The
-// kind bytes of the tile ride along.  Per tile:
-//   wait(full)  ->  staged rows -> registers  ->  __syncthreads  ->  warp 0 issues
-//   the NEXT tile's copies into the same buffer  ->  patch / collide / store.
-// The next tile's bytes are therefore in flight during the whole arithmetic
-// phase without holding a register (the direct kernels hold 19 packs per thread
-// across the DRAM round trip, or rely on the L2 prefetch to shorten it).  Meant
-// for the storage modes that are latency- and issue-bound rather than HBM-bound:
-// fp16 storage and fp32 storage with fp64 arithmetic.  Stores, patch loads and
-// everything after the loads are vec_finish: bits cannot differ.
-__device__ __forceinline__ uint32_t smem_u32(const void *p)
+// Staged variant (the north star's "shared-memory ... staging of the neighbour
+// planes"): every WARP is its own software pipeline.  A warp owns a column of
+// 32 packs (32 V cells) and walks `rows` consecutive rows of one plane; the 19
+// row segments the next row's cells pull from (shifted by the direction's y / z
+// component - periodic wrap or halo plane exactly as in the direct kernel - plus
+// one 16-byte chunk either side for the x shift, the periodic wrap in x
+// included) and the kind bytes travel global -> shared memory with cp.async
+// (LDGSTS: no register is held while the bytes are in flight), two rows ahead
+// of the arithmetic:
+//     issue row t+1   ->   wait for row t   ->   shared -> registers   ->
+//     patch / collide / store (vec_finish: the direct kernel's code, same bits)
+// No block-level barrier, only __syncwarp: warps drift freely, as in the direct
+// kernel.  What it buys over the direct kernel: the loads of the next row are in
+// flight during the whole arithmetic phase instead of an L2 prefetch that only
+// shortens the round trip; what it costs: 29 shared-memory loads per pack.
+// (A first version staged whole-row tiles per BLOCK with cp.async.bulk + mbarrier:
+// bit-exact too, but the block-wide phases left the SM idle two thirds of the
+// time - 41 instead of 72 GLUPS with fp16 storage at 512^3.)
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc, bool pred)
 {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
-{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
-        "MLB_WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@p bra MLB_DONE;\n"
-        "bra MLB_WAIT;\n"
-        "MLB_DONE:\n"
-        "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+        "setp.ne.b32 p, %2, 0;\n"
+#ifdef MLB_STAGE_CA
+        "@p cp.async.ca.shared.global [%0], [%1], 16;\n"
+#else
+        "@p cp.async.cg.shared.global [%0], [%1], 16;\n"
+#endif
+        "}\n" ::"r"(d), "l"(gsrc), "r"((int)pred) : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
-{
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-        ::"r"(smem_u32(dst)), "l"(__cvta_generic_to_global(src)), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// y / z component of direction i (0 for the rest population)
-__device__ __forceinline__ void dir_yz(int i, int &cy, int &cz)
-{
-    cy = cz = 0;
-#define MLB_X(ii, CX, Z, R)                                                          \
-    if (i == ii) {                                                                   \
-        cy = SEL_##R == SEL_rm ? 1 : SEL_##R == SEL_rq ? -1 : 0;                     \
-        cz = SEL_##Z == SEL_zm ? 1 : SEL_##Z == SEL_zq ? -1 : 0;                     \
-    }
-    MLB_DIRS(MLB_X)
-#undef MLB_X
-}
+template <typename TS, int V>
+struct StageShape {
+    static constexpr int E = 16 / (int)sizeof(TS);          // elements per 16-byte chunk
+    static constexpr int W = 32 * V;                         // cells per warp row
+    static constexpr int SLICE = W + 2 * E;                  // elements per staged segment
+    static constexpr int CHUNKS = SLICE / E;                 // 16-byte chunks per segment (<= 32)
+    static constexpr int KCHUNKS = W / 16;                   // chunks of kind bytes
+    static constexpr int STAGE_BYTES = Q * SLICE * (int)sizeof(TS) + W;
+    static constexpr int WARP_BYTES = 2 * STAGE_BYTES;       // two rows in flight / in use
+    // one lane per chunk: the modes this kernel is meant for (fp16 storage, fp32
+    // storage with fp64 arithmetic: 256-byte warp rows); fp32 / fp64 run at the HBM
+    // roofline with the direct kernel
+    static constexpr bool OK = CHUNKS <= 32;
+    static_assert(STAGE_BYTES % 16 == 0, "stages stay 16-byte aligned");
+};
 
-template <typename TS, int V, int NT>
-__global__ void __launch_bounds__(NT, 512 / NT)
-step_stage_kernel(const StepArgs<TS> a, const int ty, const int tiles_per_block, const int ntiles)
+template <typename TS, int V>
+__global__ void __launch_bounds__(128, 4)
+step_stage_kernel(const StepArgs<TS> a, const int rows, const int ncol, const int nrg,
+                  const int ntasks)
 {
     using T = typename Store<TS>::C;
-    extern __shared__ __align__(128) unsigned char stage[];
-    __shared__ uint64_t full;
+    using SS = StageShape<TS, V>;
+    static_assert(SS::OK, "a staged segment must fit one cp.async per lane");
+    extern __shared__ __align__(128) unsigned char stage_mem[];
     const Geom &gm = a.g;
-    const int xp = (int)gm.xp, plane = (int)gm.plane;
-    const int tpr = NT / ty;                       // threads per row = xp / V
-    const int r = threadIdx.x / tpr, x0 = (threadIdx.x - r * tpr) * V;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned rowbytes = (unsigned)xp * (unsigned)sizeof(TS);
-    const int tpp = gm.ny / ty;                    // tiles per plane (the host checks ny % ty == 0)
-    // staged layout: [population][tile row][xp] elements, then [tile row][xp] kind bytes
-    const TS *srow = reinterpret_cast<const TS *>(stage);
-    const uint8_t *skind = stage + (size_t)Q * ty * rowbytes;
+    const int task = blockIdx.x * 4 + warp;
+    if (task >= ntasks)
+        return;                                   // (no block-level barrier below)
+    const int col = task % ncol, rg = (task / ncol) % nrg;
+    const int lz = a.z0 + task / (ncol * nrg);
+    const int y_begin = rg * rows, y_end = min(y_begin + rows, gm.ny);
+    const int xp = (int)gm.xp, plane = (int)gm.plane;
+    const int xw = col * SS::W, x0 = xw + lane * V;
+    unsigned char *mine = stage_mem + (size_t)warp * SS::WARP_BYTES;
 
-    // warp 0 fetches a tile: lane i < 19 the rows of population i, lane 19 the kind bytes
-    auto fetch = [&](int tile) {
-        const int lz = a.z0 + tile / tpp, y0 = (tile - (tile / tpp) * tpp) * ty;
-        if (lane == 0)
-            mbar_expect_tx(&full, (unsigned)ty * ((unsigned)Q * rowbytes + (unsigned)xp));
-        __syncwarp();
-        if (lane < Q) {
-            int cy, cz;
-            dir_yz(lane, cy, cz);
-            const int zs = cz == 0 ? lz + 1
-                         : cz > 0 ? ((lz == 0) ? gm.zlo_src : lz)
-                                  : ((lz == gm.nz - 1) ? gm.zhi_src : lz + 2);
-            const TS *src = a.pre[lane] + (long long)zs * plane;
-            TS *dst = const_cast<TS *>(srow) + (size_t)lane * ty * xp;
-            const int ys0 = y0 - cy;
-            if (ys0 >= 0 && ys0 + ty <= gm.ny) {
-                bulk_g2s(dst, src + (long long)ys0 * xp, (unsigned)ty * rowbytes, &full);
-            } else {
-                for (int k = 0; k < ty; ++k) {
-                    int ys = ys0 + k;
-                    ys = ys < 0 ? ys + gm.ny : ys >= gm.ny ? ys - gm.ny : ys;
-                    bulk_g2s(dst + (size_t)k * xp, src + (long long)ys * xp, rowbytes, &full);
-                }
-            }
-        } else if (lane == Q) {
-            bulk_g2s(const_cast<uint8_t *>(skind),
-                     a.ct.kind + ((long long)(lz + 1) * plane + (long long)y0 * xp),
-                     (unsigned)ty * (unsigned)xp, &full);
-        }
+    const int zc = (lz + 1) * plane;
+    const int zm = ((lz == 0) ? gm.zlo_src : lz) * plane;
+    const int zq = ((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) * plane;
+    // chunk `lane` of a segment: elements [xw - E + lane E, + E) of the source row,
+    // the outer two wrapped around the row (periodic in x) where the column touches
+    // its ends; chunks past the padded row are not fetched (nobody reads them)
+    int coff = xw - SS::E + lane * SS::E;
+    if (lane == 0 && xw == 0) coff = ((gm.nx - 1) / SS::E) * SS::E;
+    if (lane == SS::CHUNKS - 1 && xw + SS::W >= gm.nx) coff = 0;
+    const bool cpred = lane < SS::CHUNKS && coff >= 0 && coff < xp;
+    // kind bytes of the warp's own cells: lanes CHUNKS.. take them when there is room
+    // in the warp, else the first lanes do in a second instruction
+    constexpr bool KSAME = SS::CHUNKS + SS::KCHUNKS <= 32;
+    const int klane = KSAME ? lane - SS::CHUNKS : lane;
+    const bool kpred = klane >= 0 && klane < SS::KCHUNKS && xw + klane * 16 < xp;
+
+    auto fetch = [&](int y, int st) {
+        TS *seg = reinterpret_cast<TS *>(mine + (size_t)st * SS::STAGE_BYTES);
+        const int ym = (y == 0) ? gm.ny - 1 : y - 1;
+        const int yq = (y == gm.ny - 1) ? 0 : y + 1;
+        const int rc = y * xp, rm = ym * xp, rq = yq * xp;
+        cp_async16(seg + lane * SS::E, a.pre[0] + (zc + rc + coff), cpred);
+#define MLB_X(i, CX, Z, R)                                                           \
+        cp_async16(seg + i * SS::SLICE + lane * SS::E, a.pre[i] + ((Z) + (R) + coff), cpred);
+        MLB_DIRS(MLB_X)
+#undef MLB_X
+        unsigned char *kd = reinterpret_cast<unsigned char *>(seg + Q * SS::SLICE);
+        cp_async16(kd + klane * 16, a.ct.kind + (zc + rc + xw + klane * 16), kpred);
+        cp_async_commit();
+        // (optional) the L2 prefetch of the direct kernel on top: the staged copies
+        // then find their lines in L2
+        prefetch_ahead<TS, V, 32, true>(a.pre, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
     };
 
-    if (threadIdx.x == 0) {
-        mbar_init(&full, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const int first = blockIdx.x * tiles_per_block;
-    const int last = min(first + tiles_per_block, ntiles);
-    if (first >= last)
-        return;
-    if (warp == 0)
-        fetch(first);
-
     const bool active = x0 < (a.passthrough ? xp : gm.nx);
-    const int xl = (x0 == 0) ? gm.nx - 1 : x0 - 1;
-    const int xr = (x0 + V >= gm.nx) ? 0 : x0 + V;
+    // positions inside a staged segment: own pack, the cell left of it, the cell right of it
+    const int p = SS::E + lane * V;
+    const int pl = (x0 == 0) ? (gm.nx - 1) % SS::E : p - 1;
+    const int pr = (x0 + V >= gm.nx) ? SS::E + SS::W : p + V;
     const PushArgs<TS> noph{};
-    for (int tile = first; tile < last; ++tile) {
-        const int lz = a.z0 + tile / tpp, y = (tile - (tile / tpp) * tpp) * ty + r;
-        mbar_wait(&full, (unsigned)(tile - first) & 1u);
+
+    fetch(y_begin, 0);
+    for (int y = y_begin; y < y_end; ++y) {
+        const int st = (y - y_begin) & 1;
+        if (y + 1 < y_end) {
+            fetch(y + 1, st ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        const TS *seg = reinterpret_cast<const TS *>(mine + (size_t)st * SS::STAGE_BYTES);
         uint32_t kpack = 0u;
         T g[Q][V];
         if (active) {
-            kpack = KindIO<V>::load(skind + (size_t)r * xp + x0);
-            PackIO<TS, V>::load(srow + (size_t)r * xp + x0, g[0]);
-#define MLB_X(i, CX, Z, R) pull_pack<TS, V, CX>(srow + ((size_t)i * ty + r) * xp, x0, xl, xr, g[i]);
+            kpack = KindIO<V>::load(reinterpret_cast<const uint8_t *>(seg + Q * SS::SLICE) + lane * V);
+            PackIO<TS, V>::load(seg + p, g[0]);
+#define MLB_X(i, CX, Z, R) pull_pack<TS, V, CX>(seg + i * SS::SLICE, p, pl, pr, g[i]);
             MLB_DIRS(MLB_X)
 #undef MLB_X
             if (x0 + V > gm.nx) {   // the pack that holds x = nx-1 of a ragged row (see step_vec_kernel)
                 const int js = gm.nx - 1 - x0;
 #define MLB_X(i, CX, Z, R)                                                           \
                 if (CX < 0) {                                                        \
-                    const T w0 = Store<TS>::up((srow + ((size_t)i * ty + r) * xp)[0]); \
+                    const T w0 = Store<TS>::up((seg + i * SS::SLICE)[SS::E + SS::W]); \
                     _Pragma("unroll") for (int j = 0; j < V - 1; ++j)                \
                         if (j == js) g[i][j] = w0;                                   \
                 }
@@ -1208,12 +1201,10 @@ step_stage_kernel(const StepArgs<TS> a, const int ty, const int tiles_per_block,
 #undef MLB_X
             }
         }
-        __syncthreads();            // every thread holds its pack: the buffer is free again
-        if (warp == 0 && tile + 1 < last)
-            fetch(tile + 1);
+        __syncwarp();               // every lane holds its pack: the stage may be refilled
         if (active) {
             const int o_plane = y * xp + x0;
-            vec_finish<TS, V, false>(a, noph, g, kpack, (lz + 1) * plane + o_plane, o_plane, lz);
+            vec_finish<TS, V, false>(a, noph, g, kpack, zc + o_plane, o_plane, lz);
         }
     }
 }
