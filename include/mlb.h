@@ -206,6 +206,13 @@ int mlb_run_steps(mlb_plan *plan, void *d_a, void *d_b, int nsteps,
 int mlb_run_steps_inplace(mlb_plan *plan, void *d_f, int nsteps, int *repr,
                           void *stream, float *ms);
 int mlb_inplace_normalize(mlb_plan *plan, void *d_f, int *repr, void *stream);
+/* Thread layout of the in-place pull half's pack kernel (tuning knob, never
+ * changes bits): 0 = classic (a warp is LX packs x 32 / LX rows; the lanes at
+ * the ends of a warp row fall back to per-cell stores), 1 = row blocks (a warp
+ * is 32 packs of one row, the block's warps sit side by side in x and pass the
+ * value that crosses a warp boundary through shared memory: a block that spans
+ * the row has no row ends), -1 = automatic. */
+int mlb_plan_set_inplace_layout(mlb_plan *plan, int mode);
 
 /* The in-place update over z-slabs (MLB_Z_HALO plans, pack kernels, peer
  * memory).  One half-step on slab planes [z0, z1); `repr` says which: 0 = the

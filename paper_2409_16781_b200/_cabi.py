@@ -40,6 +40,7 @@ SYMBOLS = (
     "mlb_step_host",
     "mlb_block_alloc", "mlb_block_free", "mlb_plan_set_graph",
     "mlb_slab_run_steps", "mlb_slab_run_steps_inplace", "mlb_run_steps_host",
+    "mlb_plan_set_inplace_layout",
 )
 
 
@@ -126,6 +127,7 @@ def lib():
         "mlb_block_alloc": (i, [i, ctypes.c_int64, ctypes.POINTER(vp)]),
         "mlb_block_free": (i, [vp]),
         "mlb_plan_set_graph": (i, [vp, i]),
+        "mlb_plan_set_inplace_layout": (i, [vp, i]),
         "mlb_run_steps_host": (i, [vp, vp, vp, vp, vp, i, i, vp, vp,
                                    ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i)]),
         "mlb_slab_run_steps": (i, [vp, vp, vp, i, ctypes.POINTER(Ring), vp, vp,

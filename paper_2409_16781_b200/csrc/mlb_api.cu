@@ -206,6 +206,7 @@ struct mlb_plan {
     // CUDA graph of a run of steps (mlb_run_steps / mlb_run_steps_inplace on small,
     // launch-bound domains): captured once on the library's own stream, replayed on
     // the caller's
+    int aa_layout = -1;             // in-place pull half: 1 = row-block layout, 0 / -1 = classic
     int graph_mode = -1;            // -1 auto (small domains), 0 never, 1 always
     cudaStream_t cap_stream = nullptr;
     struct GraphCache {
@@ -648,6 +649,15 @@ int launch_aa(mlb_plan *p, void *f, int kind, const AaRange &r, cudaStream_t st)
     return MLB_OK;
 }
 
+// layout of the in-place pull half: row blocks (mlb_plan_set_inplace_layout; MLB_AA_ROWB
+// overrides for A/B runs)
+bool aa_row_blocks(const mlb_plan *p)
+{
+    static const int env = std::getenv("MLB_AA_ROWB") ? std::atoi(std::getenv("MLB_AA_ROWB")) : -1;
+    const int mode = env >= 0 ? env : p->aa_layout;
+    return mode == 1;
+}
+
 template <typename TS, int V, int LX>
 int launch_aa_vec(mlb_plan *p, void *f, int kind, const AaRange &r, cudaStream_t st)
 {
@@ -659,7 +669,18 @@ int launch_aa_vec(mlb_plan *p, void *f, int kind, const AaRange &r, cudaStream_t
     const long long cols = kind == 1 ? p->lay.xp : p->nx;
     const dim3 grid((unsigned)((cols / V + LX - 1) / LX), (p->ny + rows - 1) / rows, n);
     const bool remote = r.below || r.above;
-    if (kind == 0) {
+    if (kind == 0 && aa_row_blocks(p)) {
+        // pull half, row-block layout: a block is WPR warps side by side in x (values that
+        // cross a warp boundary go through shared memory) times 4 / WPR rows
+        const int ppr = (p->nx + V - 1) / V;
+        const int wpr = ppr <= 32 ? 1 : ppr <= 64 ? 2 : 4;
+        const dim3 rgrid((ppr + 32 * wpr - 1) / (32 * wpr), (p->ny + 4 / wpr - 1) / (4 / wpr), n);
+#define MLB_ROWB(W)                                                                      \
+        if (remote) mlb::aa_pull_vec_kernel<TS, V, 32, true, W><<<rgrid, 128, 0, st>>>(a); \
+        else mlb::aa_pull_vec_kernel<TS, V, 32, false, W><<<rgrid, 128, 0, st>>>(a);
+        if (wpr == 1) { MLB_ROWB(1) } else if (wpr == 2) { MLB_ROWB(2) } else { MLB_ROWB(4) }
+#undef MLB_ROWB
+    } else if (kind == 0) {
         // pull half: results for crossing directions go into the neighbours' planes
         if (remote) mlb::aa_pull_vec_kernel<TS, V, LX, true><<<grid, 128, 0, st>>>(a);
         else mlb::aa_pull_vec_kernel<TS, V, LX, false><<<grid, 128, 0, st>>>(a);
@@ -1378,6 +1399,16 @@ int run_graphed(mlb_plan *p, void *a, void *b, int nsteps, int repr, cudaStream_
 }
 
 }  // namespace
+
+int mlb_plan_set_inplace_layout(mlb_plan *p, int mode)
+{
+    if (int rc = check_plan(p, false)) return rc;
+    if (mode < -1 || mode > 1)
+        return fail(MLB_EINVAL, "in-place layout %d: must be -1 (auto), 0 (classic) or 1 (row blocks)", mode);
+    p->aa_layout = mode;
+    ++p->epoch;
+    return MLB_OK;
+}
 
 int mlb_plan_set_graph(mlb_plan *p, int mode)
 {

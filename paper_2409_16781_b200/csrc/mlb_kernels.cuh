@@ -1232,18 +1232,29 @@ step_stage_kernel(const StepArgs<TS> a, const int rows, const int ncol, const in
 // better off with 168 registers and no spills, fp32 / fp16 storage with 128)
 template <typename TS> struct AaMinBlocks { static constexpr int value = 4; };
 template <> struct AaMinBlocks<double> { static constexpr int value = 3; };
-template <typename TS, int V, int LX, bool REMOTE>
+// WPR > 0 selects the ROW-BLOCK layout: a warp is one row segment of 32 packs, the
+// block's four warps are WPR segments side by side in x times 4 / WPR rows, and
+// the one value (and the bulk flag) that crosses a WARP boundary travels through
+// shared memory - so a block that spans the whole row (nx = WPR * 32 * V, the
+// periodic wrap included) has no row ends at all, and every store of a bulk pack
+// is an aligned pack; a longer row has ends only at block boundaries.
+template <typename TS, int V, int LX, bool REMOTE, int WPR = 0>
 __global__ void __launch_bounds__(128, AaMinBlocks<TS>::value)
 aa_pull_vec_kernel(const AAArgs<TS> a)
 {
     using T = typename Store<TS>::C;
-    constexpr int RPW = 32 / LX;
+    constexpr bool ROWB = WPR > 0;
+    constexpr int LXE = ROWB ? 32 : LX;          // packs per warp row
+    constexpr int RPW = 32 / LXE;
+    constexpr int BROWS = ROWB ? 4 / (WPR > 0 ? WPR : 1) : 4 * RPW;   // rows per block
     constexpr unsigned FULL = 0xffffffffu;
     const Geom &gm = a.g;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int seg = lane % LX;
-    int x0 = (blockIdx.x * LX + seg) * V;
-    int y = blockIdx.y * (4 * RPW) + warp * RPW + lane / LX;
+    const int seg = lane % LXE;
+    const int wseg = ROWB ? warp % (WPR > 0 ? WPR : 1) : 0;   // the warp's segment of the block row
+    int x0 = ROWB ? ((blockIdx.x * WPR + wseg) * 32 + lane) * V : (blockIdx.x * LX + seg) * V;
+    int y = ROWB ? blockIdx.y * BROWS + warp / (WPR > 0 ? WPR : 1)
+                 : blockIdx.y * (4 * RPW) + warp * RPW + lane / LXE;
     const int lz = a.z0 + blockIdx.z;
     // z-slabs: crossing directions of a boundary plane store into the neighbour slab
     const bool rlo = REMOTE && lz == 0 && a.lo[0] != nullptr;
@@ -1272,15 +1283,15 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
 #undef MLB_X
     if (a.pf_bulk) {
         if (blockIdx.x == 0 && threadIdx.x < Q && (a.pf_dz | a.pf_dy) != 0)
-            prefetch_rows<TS, true>(a.f, gm, a.pf_dz, a.pf_dy, blockIdx.y * (4 * RPW), 4 * RPW, lz,
+            prefetch_rows<TS, true>(a.f, gm, a.pf_dz, a.pf_dy, blockIdx.y * BROWS, BROWS, lz,
                                     threadIdx.x);
     } else
-        prefetch_ahead<TS, V, LX, true>(a.f, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
+        prefetch_ahead<TS, V, LXE, true>(a.f, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
 
     const bool bulk = valid && kpack == 0u;
-    const bool bulk_r = __shfl_down_sync(FULL, (int)bulk, 1) != 0 && seg != LX - 1
-                        && x0 + V < gm.nx;
-    const bool bulk_l = __shfl_up_sync(FULL, (int)bulk, 1) != 0 && seg != 0;
+    bool bulk_r = __shfl_down_sync(FULL, (int)bulk, 1) != 0 && seg != LXE - 1
+                  && x0 + V < gm.nx;
+    bool bulk_l = __shfl_up_sync(FULL, (int)bulk, 1) != 0 && seg != 0;
 
     uint32_t c[V];
 #pragma unroll
@@ -1357,6 +1368,36 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
             }
     }
 
+    // ---- row-block layout: what crosses a warp boundary goes through shared memory
+    int wr = -1, wl = -1;          // the warps holding the packs right / left of this warp's row
+    __shared__ T pub0[ROWB ? 4 : 1][5], pub31[ROWB ? 4 : 1][5];
+    __shared__ int pb0[ROWB ? 4 : 1], pb31[ROWB ? 4 : 1];
+    if constexpr (ROWB) {
+        if (lane == 0) {
+            pb0[warp] = (int)bulk;
+            int n = 0;
+#define MLB_X(i, CX, Z, R) if (CX > 0) pub0[warp][n++] = g[opp(i)][0];
+            MLB_DIRS(MLB_X)
+#undef MLB_X
+        }
+        if (lane == 31) {
+            pb31[warp] = (int)bulk;
+            int n = 0;
+#define MLB_X(i, CX, Z, R) if (CX < 0) pub31[warp][n++] = g[opp(i)][V - 1];
+            MLB_DIRS(MLB_X)
+#undef MLB_X
+        }
+        __syncthreads();
+        // a block that spans the whole row closes it on itself (periodic wrap in x)
+        const bool full = gridDim.x == 1 && gm.nx == WPR * 32 * V;
+        wr = (wseg + 1 < WPR) ? warp + 1 : (full ? warp + 1 - WPR : -1);
+        wl = (wseg > 0) ? warp - 1 : (full ? warp - 1 + WPR : -1);
+        if (lane == 31)
+            bulk_r = valid && wr >= 0 && pb0[wr] != 0 && (x0 + V < gm.nx || full);
+        if (lane == 0)
+            bulk_l = valid && wl >= 0 && pb31[wl] != 0;
+    }
+
     // ---- stores ---------------------------------------------------------------
 #define MLB_T(i, Z, R, X) aa_target<TS, CZ_##Z, REMOTE>(a, i, (Z), (R), (X), rlo, rhi)
     // The stores go to the very addresses the loads came from; left alone the
@@ -1382,6 +1423,12 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
 #define MLB_X(i, CX, Z, R) if (CX > 0) nb[n++] = __shfl_down_sync(FULL, g[opp(i)][0], 1);
         MLB_DIRS(MLB_X)
 #undef MLB_X
+        if constexpr (ROWB) {
+            if (lane == 31 && wr >= 0) {
+#pragma unroll
+                for (int q = 0; q < 5; ++q) nb[q] = pub0[wr][q];
+            }
+        }
         if (bulk) {
             n = 0;
 #define MLB_X(i, CX, Z, R)                                                            \
@@ -1405,6 +1452,12 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
 #define MLB_X(i, CX, Z, R) if (CX < 0) nb[n++] = __shfl_up_sync(FULL, g[opp(i)][V - 1], 1);
         MLB_DIRS(MLB_X)
 #undef MLB_X
+        if constexpr (ROWB) {
+            if (lane == 0 && wl >= 0) {
+#pragma unroll
+                for (int q = 0; q < 5; ++q) nb[q] = pub31[wl][q];
+            }
+        }
         if (bulk) {
             n = 0;
 #define MLB_X(i, CX, Z, R)                                                            \

@@ -280,6 +280,11 @@ class KernelPlan:
         self.passthrough = bool(on)
         _cabi.check(self._lib.mlb_plan_set_passthrough(self._plan, int(self.passthrough)))
 
+    def set_inplace_layout(self, mode):
+        """Thread layout of the in-place pull half (include/mlb.h): 0 classic,
+        1 row blocks, -1 auto.  Never changes bits."""
+        _cabi.check(self._lib.mlb_plan_set_inplace_layout(self._plan, int(mode)))
+
     def set_graph(self, mode):
         """CUDA graphs in `run_steps` / `run_steps_inplace`: -1 auto (small,
         launch-bound domains), 0 never, 1 always.  Never changes bits."""

@@ -225,3 +225,52 @@ def test_engine_run_inplace_channel_equals_two_buffer_run():
     orc = CpuOracle(128, 48, 12, a.mask, a.params.omega, inlet_u=a.inlet_u, threads=8)
     f0 = cases.init(spec, Precision.SINGLE).f_pre.data
     np.testing.assert_array_equal(a.f_pre.data, orc.run(f0.copy(), f0.copy(), 23))
+
+
+def _row_block_grids():
+    """Rows that exactly fill a block of 1, 2 or 4 warps (the periodic wrap then
+    closes inside the block), rows that do not, walls inside and between packs,
+    inlet / outlet faces."""
+    out = {}
+    for nx, ny, nz in ((128, 6, 4), (256, 5, 3), (512, 4, 3), (72, 4, 3), (200, 5, 3)):
+        g = B.open_mask(nx, ny, nz)
+        u = np.random.default_rng(nx).random(g.shape)
+        g[u < 0.03] = B.SOLID
+        g[u > 0.985] = B.MOVING_WALL
+        out[f"periodic{nx}"] = (g, (0.03, -0.02, 0.04), 0.0)
+    cav = B.cavity_mask(256, 8, 5)
+    cav[100:104, 3:5, 2] = B.SOLID
+    out["cavity256"] = (cav, (0.06, 0.0, 0.0), 0.0)
+    out["channel128"] = (B.channel_mask(128, 8, 5, B.sphere_cells(128, 8, 5, 4, 30.0, 4.0, 2.5)),
+                         (0.0, 0.0, 0.0), 0.05)
+    return out
+
+
+@pytest.mark.parametrize("tag,variant", [("f32", 1016), ("f64", 1016), ("f16", 2016), ("m2", 2016),
+                                         ("f32", 2016)])
+@pytest.mark.parametrize("geom", list(_row_block_grids()))
+def test_inplace_row_block_layout_never_changes_bits(geom, tag, variant, rng):
+    """mlb_plan_set_inplace_layout(1): the pull half's warps sit side by side in
+    x and hand the value that crosses a warp boundary through shared memory.  A
+    thread layout, like the reference's tiles (test_kernels.py:107-126): same
+    bits as the oracle, odd and even step counts."""
+    from paper_2409_16781_b200.kernels import KernelPlan
+    grid, wall_u, inlet_u = _row_block_grids()[geom]
+    prec = PREC[tag]
+    nx, ny, nz = grid.shape
+    flags = B.flatten_mask(grid)
+    f = random_block(rng, grid.size, prec.storage)
+    orc = CpuOracle(nx, ny, nz, flags, 1.5, wall_u, inlet_u,
+                    compute=np.float64 if prec is Precision.MIXED2 else None)
+    for steps in (1, 4):
+        want = orc.run(f.copy(), f.copy(), steps)
+        plan = KernelPlan(nx, ny, nz, Layout.ROW, prec, flags, 1.5, wall_u, inlet_u=inlet_u)
+        plan.set_variant(variant)
+        plan.set_inplace_layout(1)
+        d = plan.alloc()
+        plan.upload(f, d)
+        plan.run_steps_inplace(d, steps)
+        plan.normalize(d)
+        got = np.empty_like(f)
+        plan.download(d, got)
+        np.testing.assert_array_equal(got, want)

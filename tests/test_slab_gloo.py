@@ -117,3 +117,40 @@ def test_single_rank_ring_closes_on_itself():
     runner.exchange(blocks[0])
     newest, _ = runner.run(blocks[0], blocks[1], 3)
     np.testing.assert_array_equal(newest[:, 1:-1].reshape(19, -1), want)
+
+
+def _mismatch_worker(rank, world, port, same, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2409_16781_b200 import cases, engine
+        from paper_2409_16781_b200.fields import Precision
+        # a process group that serves a SWEEP: one simulation per rank, different physics
+        spec = cases.CaseSpec("ldc", 8, 8, 8, re=50.0 if same else 50.0 + 25.0 * rank, u0=0.05)
+        state = cases.init(spec, Precision.SINGLE)
+        try:
+            engine.run(state, engine.RunConfig(steps=1))
+            outcome = "ran"
+        except ValueError as exc:
+            outcome = "ValueError: " + str(exc)
+        except RuntimeError as exc:      # no CUDA device here: the decomposition itself was accepted
+            outcome = "RuntimeError: " + str(exc)
+        open(os.path.join(out_dir, f"out{rank}.txt"), "w").write(outcome)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the host-side guard without a GPU")
+@pytest.mark.parametrize("same", [False, True])
+def test_engine_run_decomposes_only_one_common_problem(same, tmp_path):
+    """With a process group initialised engine.run treats the ranks' states as
+    ONE z-decomposed domain - but only after checking that they ARE one (shape,
+    step, physics, mask).  Ranks holding different problems (a sweep) all get a
+    ValueError telling them to pass distributed=False; nobody hangs in a
+    collective."""
+    mp.spawn(_mismatch_worker, args=(2, _free_port(), same, str(tmp_path)), nprocs=2, join=True)
+    outs = [open(tmp_path / f"out{r}.txt").read() for r in range(2)]
+    if same:
+        assert all(o.startswith("RuntimeError") for o in outs), outs   # reached the CUDA path
+    else:
+        assert all(o.startswith("ValueError") and "distributed=False" in o for o in outs), outs

@@ -1,25 +1,32 @@
 #!/bin/bash
 # Round profile capture (run under gpurun, ONE GPU): launch list of the bench
-# command + one `--set full` capture per dominant kernel.  Outputs in gpurun_out/.
+# command + one `--set full` capture per dominant kernel.  Outputs in gpurun_out/;
+# tools/profile_collect.py turns them into the tracked summaries under profiles/.
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
 NCU="ncu --clock-control none"
+python -c "from paper_2409_16781_b200 import _cabi; print(_cabi.build_id())" > $OUT/build_id.txt
 # launch list of the same command bench.py is judged on (shares, not absolutes)
-$NCU --metrics gpu__time_duration.sum -c 80 --csv --log-file $OUT/launches_bench.csv \
-    python bench.py --steps 10 --warmup 3 --no-cpu-baseline > $OUT/launches_bench.log 2>&1
-# launch list of the slab driver with the fused peer-store exchange (world 1)
-$NCU --metrics gpu__time_duration.sum -c 120 --csv --log-file $OUT/launches_slab.csv \
-    python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --force-slab > $OUT/launches_slab.log 2>&1
-# full captures: fused kernel in the three storage modes, in-place pair
-$NCU --set full --import-source on -k regex:step_ -s 2 -c 1 -f -o $OUT/step_f32_512 python tools/one.py 512x512x512 single 0 4 > /dev/null 2>&1
-$NCU --set full --import-source on -k regex:step_ -s 2 -c 1 -f -o $OUT/step_f64_512 python tools/one.py 512x512x512 double 0 4 > /dev/null 2>&1
-$NCU --set full --import-source on -k regex:step_ -s 2 -c 1 -f -o $OUT/step_f16_512 python tools/one.py 512x512x512 mixed1 0 4 > /dev/null 2>&1
-$NCU --set full --import-source on -k regex:aa_pull -s 2 -c 1 -f -o $OUT/aa_pull_f32_512 python tools/aa_one.py > /dev/null 2>&1
-$NCU --set full --import-source on -k regex:aa_local -s 2 -c 1 -f -o $OUT/aa_local_f32_512 python tools/aa_one.py > /dev/null 2>&1
-# summarise on the box (gpurun_out/ travels back only under 64 MiB); keep one report
-for r in step_f32_512 step_f64_512 step_f16_512 aa_pull_f32_512 aa_local_f32_512; do
-    python tools/ncu_summary.py $OUT/$r.ncu-rep > $OUT/ncu_$r.txt 2>&1
-    [ "$r" != step_f32_512 ] && rm -f $OUT/$r.ncu-rep
+$NCU --metrics gpu__time_duration.sum -c 200 --csv --log-file $OUT/launches_bench.csv \
+    python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extra > $OUT/launches_bench.log 2>&1
+# launch list of the slab driver with the fused peer-store exchange (world 1, one-call loop)
+$NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file $OUT/launches_slab.csv \
+    python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --force-slab --no-preflight > $OUT/launches_slab.log 2>&1
+cap() {  # name, kernel regex, command...
+  local name=$1 regex=$2; shift 2
+  $NCU --set full --import-source on -k regex:$regex -s 2 -c 1 -f -o $OUT/$name "$@" > /dev/null 2>&1
+  python tools/ncu_summary.py $OUT/$name.ncu-rep > $OUT/ncu_$name.txt 2>&1
+  [ "$name" != step_f32_512 ] && rm -f $OUT/$name.ncu-rep
+  head -3 $OUT/ncu_$name.txt
+}
+# full captures: fused kernel in the four storage modes, the in-place pair in each, the staged kernel
+for pt in single:f32 double:f64 mixed1:f16 mixed2:m2; do
+  p=${pt%%:*}; t=${pt##*:}
+  cap step_${t}_512 step_ python tools/one.py 512x512x512 $p 0 4
+  cap aa_pull_${t}_512 aa_pull python tools/aa_one.py $p
+  cap aa_local_${t}_512 aa_local python tools/aa_one.py $p
 done
+cap stage_f16_512 step_stage python tools/one.py 512x512x512 mixed1 4000 4
+cap aa_pull_rowb_f32_512 aa_pull python tools/aa_one.py single 1
 ls -la $OUT
