@@ -705,7 +705,7 @@ def main():
 
     # ---- device-timed run: W warm-up, then exactly K steps -------------------
     main_run = run_device(wl, args, prec_tok, rank, world, device, fdev, args.steps, args.warmup,
-                          clocks=True)
+                          clocks=rank == 0)
     ms, value = main_run["ms"], main_run["value"]
     cells_rank = main_run["cells_rank"]
 
