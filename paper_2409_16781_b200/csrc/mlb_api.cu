@@ -667,7 +667,7 @@ int launch_aa_vec(mlb_plan *p, void *f, int kind, const AaRange &r, cudaStream_t
     const int n = (r.z1 < 0 ? p->nz : r.z1) - r.z0;
     // the local half covers the padded row (it rewrites the padding: whole last lines)
     const long long cols = kind == 1 ? p->lay.xp : p->nx;
-    const dim3 grid((unsigned)((cols / V + LX - 1) / LX), (p->ny + rows - 1) / rows, n);
+    const dim3 grid((unsigned)(((cols + V - 1) / V + LX - 1) / LX), (p->ny + rows - 1) / rows, n);
     const bool remote = r.below || r.above;
     if (kind == 0 && aa_row_blocks(p)) {
         // pull half, row-block layout: a block is WPR warps side by side in x (values that
@@ -716,18 +716,15 @@ int resolve_aa_variant(const mlb_plan *p)
 {
     if (p->variant != 0 && p->variant != VARIANT_STAGED)
         return p->variant;
-    if (p->dtype == MLB_F32 && p->nx % 4 == 0 && p->nx >= 128) return 1016;
-    if (p->dtype == MLB_F32 && p->nx % 2 == 0 && p->nx >= 128) return 2016;
-    if (p->dtype == MLB_F64 && p->nx % 2 == 0 && p->nx >= 128) return 1016;
-    if (p->dtype == MLB_F16 && p->nx % 4 == 0 && p->nx >= 128) return 2016;
-    if (p->dtype == MLB_F32C64 && p->nx % 2 == 0 && p->nx >= 128) return 2016;
+    // packs for any row length (a ragged row ends in a pack of real cells + padding)
+    if (p->nx >= 128) return p->dtype == MLB_F32 || p->dtype == MLB_F64 ? 1016 : 2016;
     return 128;
 }
 
 bool aa_uses_packs(const mlb_plan *p, int variant)
 {
     return variant >= 1000 && variant_exists(p->dtype, variant)
-        && p->nx % pack_cells(p->dtype, variant) == 0;
+        && p->nx >= pack_cells(p->dtype, variant);
 }
 
 // Open boundaries in place: the pack kernels apply the pass inside the step

@@ -1281,6 +1281,17 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
 #define MLB_X(i, CX, Z, R) pull_pack<TS, V, CX>(a.f[i] + ((Z) + (R)), x0, xl, xr, g[i]);
     MLB_DIRS(MLB_X)
 #undef MLB_X
+    if (x0 + V > gm.nx) {   // the pack that holds x = nx-1 of a ragged row (see step_vec_kernel)
+        const int js = gm.nx - 1 - x0;
+#define MLB_X(i, CX, Z, R)                                                           \
+        if (CX < 0) {                                                                \
+            const T w0 = Store<TS>::up((a.f[i] + ((Z) + (R)))[0]);                   \
+            _Pragma("unroll") for (int j = 0; j < V - 1; ++j)                        \
+                if (j == js) g[i][j] = w0;                                           \
+        }
+        MLB_DIRS(MLB_X)
+#undef MLB_X
+    }
     if (a.pf_bulk) {
         if (blockIdx.x == 0 && threadIdx.x < Q && (a.pf_dz | a.pf_dy) != 0)
             prefetch_rows<TS, true>(a.f, gm, a.pf_dz, a.pf_dy, blockIdx.y * BROWS, BROWS, lz,
@@ -1497,7 +1508,7 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
         if (aa_participant(c[j])) {                                                   \
             const int xs = (CX) == 0 ? x0 + j                                         \
                          : (CX) > 0 ? (j == 0 ? xl : x0 + j - 1)                      \
-                                    : (j == V - 1 ? xr : x0 + j + 1);                 \
+                                    : (x0 + j + 1 >= gm.nx ? 0 : x0 + j + 1);         \
             if (c[j] & cls_link(i)) a.f[opp(i)][d + j] = Store<TS>::down(g[opp(i)][j]); \
             else *MLB_T(i, Z, R, xs) = Store<TS>::down(g[opp(i)][j]);                 \
         }

@@ -214,11 +214,10 @@ def test_two_cell_packs_on_rows_that_four_does_not_divide(tag, variant, rng):
     np.testing.assert_array_equal(got, want)
 
 
-def test_in_place_pack_kernels_still_need_whole_packs():
-    """Two-buffer pack kernels serve any row length (see
-    test_pack_kernels_on_rows_no_pack_divides); the in-place pack kernels still
-    need rows made of whole packs and fall back to one cell per thread - same
-    bits - when the row is ragged."""
+def test_pack_variant_on_a_nine_cell_row_in_place():
+    """A pack variant on a row of 9 cells (two packs + one cell): served by the
+    pack kernels, two blocks and in place (see
+    test_pack_kernels_on_rows_no_pack_divides, test_inplace_pack_kernels_on_ragged_rows)."""
     grid, wall_u, inlet_u = geometries3d()["cavity"]  # nx = 9
     f = random_block(np.random.default_rng(3), grid.size, np.float32)
     want = make_oracle(grid, 1.0, wall_u).run(f.copy(), f.copy(), 4)
