@@ -723,9 +723,11 @@ def main():
                 data[q].fill(vals[q])
             from paper_2409_16781_b200.fields import PopulationField
             from paper_2409_16781_b200.lattice import RelaxationParams
+            mask = pinned_empty((cells_rank,), np.uint8)   # page-locked, as cases.init makes it
+            np.copyto(mask.reshape(wl.nz, wl.ny, wl.nx), wl.planes(0, wl.nz))
             state = engine.SimState(
                 f_pre=PopulationField(data, wl.nx, wl.ny, wl.nz, Layout.ROW), f_post_=None,
-                mask=wl.planes(0, wl.nz).reshape(-1), nx=wl.nx, ny=wl.ny, nz=wl.nz,
+                mask=mask, nx=wl.nx, ny=wl.ny, nz=wl.nz,
                 layout=Layout.ROW, precision=prec, params=RelaxationParams.from_omega(wl.omega),
                 wall_u=wl.wall_u, inlet_u=wl.inlet_u, case=wl.case)
             cfg = engine.RunConfig(steps=args.steps, precision=prec, device=local,

@@ -222,8 +222,11 @@ def state_from_macroscopic(rho, ux, uy, uz, mask_grid, layout, precision,
             stored = convert_precision(feq, precision.storage, policy="strict")
             view[:, z] = stored.transpose(0, 2, 1)
     f_pre = PopulationField(data, nx, ny, nz, layout)
+    # (the flags in page-locked memory too: they are uploaded at the start of every run)
+    mask = pinned_empty((nx * ny * nz,), np.uint8)
+    np.copyto(mask.reshape(nz, ny, nx), mask_grid.transpose(2, 1, 0))
     return SimState(
-        f_pre=f_pre, f_post_=None, mask=boundaries.flatten_mask(mask_grid),
+        f_pre=f_pre, f_post_=None, mask=mask,
         nx=nx, ny=ny, nz=nz, layout=layout, precision=precision,
         params=params, wall_u=tuple(wall_u), inlet_u=float(inlet_u), case=case)
 
