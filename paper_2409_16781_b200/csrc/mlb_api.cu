@@ -428,10 +428,20 @@ void prefetch_distance(const mlb_plan *p, int &dz, int &dy)
 
 // pack kernels: one lane per line (0, default) or the bulk form (1; MLB_PF_BULK=1 for
 // A/B runs: measured slower at 512^3 for fp32 / fp16 / mixed2 packs)
-int prefetch_bulk()
+// Measured on B200 (profiles/pf_bulk_sizes_r2.txt): on SHORT rows the bulk form wins - 128^3 fp32
+// two blocks 0.64 -> 0.81 of the HBM peak, 256^3 fp16 storage 0.77 -> 0.81, fp32 storage / fp64
+// arithmetic 0.84 -> 0.85 (in place 0.83 -> 0.86) - from 384-cell rows on one lane per line does
+// (fp32 256^3 two blocks already prefers it: 0.99 vs 0.975).
+int prefetch_bulk(const mlb_plan *p, bool inplace)
 {
-    static const int v = std::getenv("MLB_PF_BULK") ? std::atoi(std::getenv("MLB_PF_BULK")) : 0;
-    return v;
+    static const int v = std::getenv("MLB_PF_BULK") ? std::atoi(std::getenv("MLB_PF_BULK")) : -1;
+    if (v >= 0)
+        return v;
+    if (inplace)
+        return p->dtype == MLB_F32C64 && p->nx <= 256;
+    if (p->dtype == MLB_F32)
+        return p->nx <= 128;
+    return p->nx <= 256;
 }
 
 template <typename TS>
@@ -449,7 +459,7 @@ void fill_args(mlb_plan *p, const void *fpre, void *fpost, int z0, bool fuse_ope
     a.passthrough = p->passthrough;
     a.fuse_open = fuse_open ? 1 : 0;
     prefetch_distance(p, a.pf_dz, a.pf_dy);
-    a.pf_bulk = prefetch_bulk();
+    a.pf_bulk = prefetch_bulk(p, false);
     T cv[MLB_Q];
     inlet_values<T>(p->inlet_u, cv);  // compute dtype, then storage dtype (engine.py:167-171)
     for (int q = 0; q < MLB_Q; ++q)
@@ -618,7 +628,7 @@ void fill_aa(mlb_plan *p, void *f, const AaRange &r, mlb::AAArgs<TS> &a)
         a.inlet[q] = mlb::Store<TS>::down(cv[q]);
     a.z0 = r.z0;
     prefetch_distance(p, a.pf_dz, a.pf_dy);
-    a.pf_bulk = prefetch_bulk();
+    a.pf_bulk = prefetch_bulk(p, true);
     const long long plane = p->lay.plane;
     for (int j = 0; j < 5; ++j) {
         // slab below: its top plane lz = nz_below-1 (storage nz_below), c_z = +1 populations

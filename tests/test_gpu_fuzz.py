@@ -26,7 +26,7 @@ PREC = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE, "f16": Precision.MIXED
         "m2": Precision.MIXED2}
 SCALAR = [32, 64, 128, 256]
 PACKS = {"f32": [1008, 1016, 1032, 2008, 2016, 2032], "f64": [1008, 1016, 1032],
-         "f16": [2008, 2016, 2032, 3008, 3016, 3032], "m2": [2008, 2016, 2032]}
+         "f16": [2008, 2016, 2032, 3008, 3016, 3032, 4000], "m2": [2008, 2016, 2032, 4000]}
 
 
 def draw_case(seed):
@@ -54,10 +54,9 @@ def draw_case(seed):
             grid[x, :, r.integers(0, nz)] = B.OUTLET
     omega = float(r.choice([0.0, r.uniform(0.2, 1.99)], p=[0.05, 0.95]))
     wall_u = tuple(float(v) for v in r.uniform(-0.06, 0.06, 3))
-    variant = int(r.choice(PACKS[tag] if aligned and r.random() < 0.75 else SCALAR))
-    if tag == "f16" and variant // 1000 == 2 and nx % 4:
-        variant = 128
-    steps = int(r.integers(1, 5))
+    # (pack kernels on ragged rows too: the last pack of a row is real cells + padding)
+    variant = int(r.choice(PACKS[tag] if r.random() < 0.75 else SCALAR))
+    steps = int(r.integers(1, 5)) if r.random() < 0.85 else int(r.integers(8, 13))
     return tag, grid, omega, wall_u, inlet_u, variant, steps
 
 
@@ -78,6 +77,8 @@ def test_random_case_every_kernel_family_bitwise(seed):
     def plan_for(**kw):
         p = KernelPlan(nx, ny, nz, Layout.ROW, prec, mask, omega, wall_u, inlet_u=inlet_u, **kw)
         p.set_variant(variant)
+        p.set_inplace_layout(seed % 3 == 0)      # thread layout of the in-place pull half
+        p.set_graph(seed % 2)                    # CUDA-graph replay of the loop (runs of >= 8 steps)
         return p
 
     # two buffers, strict: arbitrary never-written cells in the second buffer
@@ -138,7 +139,7 @@ def test_random_case_every_kernel_family_bitwise(seed):
     plan.download(newest, got)
     np.testing.assert_array_equal(got, want, err_msg=f"slab ring, case {seed}")
     ring.close()
-    if inplace and variant >= 1000:
+    if inplace and 1000 <= variant < 4000:
         c = plan.alloc()
         c.tensor.fill_(float("nan"))
         plan.upload(f, c)
