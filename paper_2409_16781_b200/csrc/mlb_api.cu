@@ -224,6 +224,8 @@ struct mlb_plan {
     // domain can be stepped chunk by chunk behind the upload
     bool z_closed = false;
     cudaStream_t up_stream = nullptr, down_stream = nullptr;
+    unsigned int *d_work = nullptr;   // staged kernel: ring of work counters, one per launch
+    unsigned int work_next = 0;
 };
 
 namespace {
@@ -371,8 +373,9 @@ bool stage_shape(const mlb_plan *p)
 // with tools/sweep.py: packs win in fp32 and fp16 storage, not in fp64
 int resolve_variant(const mlb_plan *p, bool allow_staged = true)
 {
-    if (p->variant != 0 && !(p->variant == VARIANT_STAGED && !allow_staged)) {
-        if (p->variant != VARIANT_STAGED || stage_shape(p))
+    const bool special = p->variant == VARIANT_STAGED;
+    if (p->variant != 0 && !(special && !allow_staged)) {
+        if (!special || stage_shape(p))
             return p->variant;
     }
     // fp32 and fp16 storage: packs of four cells for any row length - a row the pack
@@ -466,6 +469,7 @@ void fill_args(mlb_plan *p, const void *fpre, void *fpost, int z0, bool fuse_ope
         a.inlet[q] = mlb::Store<TS>::down(cv[q]);
     a.omega = T(p->omega);
     wall_terms<T>(p->wall_u, a.k);
+    a.work = nullptr;
 }
 
 // the neighbours' halo planes a launch also stores into (mlb_step_push_range)
@@ -528,20 +532,32 @@ int launch_scalar(mlb_plan *p, const mlb::StepArgs<TS> &a, const mlb::PushArgs<T
 }
 
 template <typename TS, int V>
-int launch_stage(mlb_plan *p, const mlb::StepArgs<TS> &a, int nplanes, cudaStream_t st)
+int launch_stage(mlb_plan *p, mlb::StepArgs<TS> &a, int nplanes, cudaStream_t st)
 {
     using SS = mlb::StageShape<TS, V>;
-    static const int rows_env = std::getenv("MLB_STAGE_ROWS") ? std::atoi(std::getenv("MLB_STAGE_ROWS")) : 0;
-    const int rows = rows_env > 0 ? rows_env : 16;           // rows a warp walks: pipeline fill 1 / rows
+    static const int group_env = std::getenv("MLB_STAGE_GROUP") ? std::atoi(std::getenv("MLB_STAGE_GROUP")) : 0;
+    const int group = group_env > 0 ? group_env : 2;         // warp rows handed out per counter fetch (measured: 2 is best)
     const long long cols = a.passthrough ? p->lay.xp : p->nx;
     const int ncol = (int)((cols + SS::W - 1) / SS::W);
-    const int nrg = (p->ny + rows - 1) / rows;
-    const long long ntasks = (long long)ncol * nrg * nplanes;
+    const long long ntasks = (long long)ncol * p->ny * nplanes;
+    if (ntasks >= (1ll << 30))
+        return fail(MLB_EUNSUPPORTED, "the staged kernel counts at most 2^30 warp rows per launch");
     const size_t smem = stage_smem<TS, V>();
     auto kernel = mlb::step_stage_kernel<TS, V>;
     if (smem > (48u << 10))
         MLB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kernel<<<(unsigned)((ntasks + 3) / 4), 128, smem, st>>>(a, rows, ncol, nrg, (int)ntasks);
+    // the launch's work counter: one slot of a small ring, so that launches in flight on
+    // different streams (boundary planes / interior of a slab) do not share one
+    if (!p->d_work) {
+        MLB_CUDA(pool_alloc(&p->d_work, 64 * sizeof(unsigned int)));
+    }
+    unsigned int *slot = p->d_work + (p->work_next++ & 63);
+    MLB_CUDA(cudaMemsetAsync(slot, 0, sizeof(unsigned int), st));
+    a.work = slot;
+    // as many blocks as can be resident (4 per SM), or fewer for a small launch
+    const long long want = (ntasks + 4 * group - 1) / (4 * group);
+    const long long blocks = want < 4ll * p->sms ? want : 4ll * p->sms;
+    kernel<<<(unsigned)blocks, 128, smem, st>>>(a, group, ncol, (int)ntasks);
     MLB_LAUNCHED();
     return MLB_OK;
 }
@@ -552,6 +568,7 @@ int launch_typed(mlb_plan *p, const void *fpre, void *fpost, int z0, int z1, cud
 {
     mlb::StepArgs<TS> a;
     fill_args<TS>(p, fpre, fpost, z0, fuse_open, a);
+
     if (variant == VARIANT_STAGED) {
         constexpr int V = sizeof(TS) == 8 || std::is_same<TS, mlb::f32w>::value ? 2 : 4;
         if constexpr (!PUSH && mlb::StageShape<TS, V>::OK) {
@@ -929,6 +946,7 @@ int mlb_plan_destroy(mlb_plan *p)
     pool_free(p->d_flags); pool_free(p->d_cls); pool_free(p->d_mlinks); pool_free(p->d_in);
     pool_free(p->d_kind); pool_free(p->d_tab);
     pool_free(p->d_out); pool_free(p->d_out_tmp); pool_free(p->d_partials); pool_free(p->d_diag);
+    pool_free(p->d_work);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);

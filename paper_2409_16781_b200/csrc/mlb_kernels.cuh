@@ -114,6 +114,7 @@ struct StepArgs {
     TS inlet[Q];      // equilibrium(1, u_in, 0, 0), storage dtype
     T omega;
     T k[Q];        // moving-wall terms 6 w_i (c_i . u_w), compute dtype
+    unsigned int *work;   // staged kernel: the launch's work counter (zeroed by the host)
 };
 
 // Fused halo exchange (z-slabs over peer memory).  The launch
@@ -1110,8 +1111,7 @@ struct StageShape {
 
 template <typename TS, int V>
 __global__ void __launch_bounds__(128, 4)
-step_stage_kernel(const StepArgs<TS> a, const int rows, const int ncol, const int nrg,
-                  const int ntasks)
+step_stage_kernel(const StepArgs<TS> a, const int group, const int ncol, const int ntasks)
 {
     using T = typename Store<TS>::C;
     using SS = StageShape<TS, V>;
@@ -1119,37 +1119,54 @@ step_stage_kernel(const StepArgs<TS> a, const int rows, const int ncol, const in
     extern __shared__ __align__(128) unsigned char stage_mem[];
     const Geom &gm = a.g;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int task = blockIdx.x * 4 + warp;
-    if (task >= ntasks)
-        return;                                   // (no block-level barrier below)
-    const int col = task % ncol, rg = (task / ncol) % nrg;
-    const int lz = a.z0 + task / (ncol * nrg);
-    const int y_begin = rg * rows, y_end = min(y_begin + rows, gm.ny);
     const int xp = (int)gm.xp, plane = (int)gm.plane;
-    const int xw = col * SS::W, x0 = xw + lane * V;
     unsigned char *mine = stage_mem + (size_t)warp * SS::WARP_BYTES;
-
-    const int zc = (lz + 1) * plane;
-    const int zm = ((lz == 0) ? gm.zlo_src : lz) * plane;
-    const int zq = ((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) * plane;
-    // chunk `lane` of a segment: elements [xw - E + lane E, + E) of the source row,
-    // the outer two wrapped around the row (periodic in x) where the column touches
-    // its ends; chunks past the padded row are not fetched (nobody reads them)
-    int coff = xw - SS::E + lane * SS::E;
-    if (lane == 0 && xw == 0) coff = ((gm.nx - 1) / SS::E) * SS::E;
-    if (lane == SS::CHUNKS - 1 && xw + SS::W >= gm.nx) coff = 0;
-    const bool cpred = lane < SS::CHUNKS && coff >= 0 && coff < xp;
-    // kind bytes of the warp's own cells: lanes CHUNKS.. take them when there is room
-    // in the warp, else the first lanes do in a second instruction
     constexpr bool KSAME = SS::CHUNKS + SS::KCHUNKS <= 32;
     const int klane = KSAME ? lane - SS::CHUNKS : lane;
-    const bool kpred = klane >= 0 && klane < SS::KCHUNKS && xw + klane * 16 < xp;
+    const PushArgs<TS> noph{};
 
-    auto fetch = [&](int y, int st) {
+    // Work units are warp rows - (column of 32 packs, row, plane), column fastest - handed
+    // out IN ORDER, `group` at a time, from one counter: whichever warp is free takes the
+    // next ones, so the warps in flight always work on one compact window of the domain
+    // that sweeps through memory in address order, exactly like the blocks of the direct
+    // kernel under the hardware scheduler.  (A static assignment - every warp walking its
+    // own 16 rows - was measured at HALF the speed: the windows drift apart and DRAM page
+    // locality goes; the same happened to every looped kernel tried in round 1 and 2.)
+    int ubase = 0, uk = group;
+    auto next_unit = [&]() -> int {
+        if (uk == group) {
+            unsigned int gidx = 0;
+            if (lane == 0) gidx = atomicAdd(a.work, 1u);
+            gidx = __shfl_sync(0xffffffffu, gidx, 0);
+            ubase = gidx > 0x3fffffffu / (unsigned)group ? ntasks : (int)gidx * group;
+            uk = 0;
+        }
+        const int u = ubase + uk++;
+        return u < ntasks ? u : ntasks;
+    };
+    struct Unit { int xw, y, lz; };
+    auto locate = [&](int u) -> Unit {
+        const int col = u % ncol, rest = u / ncol;
+        return Unit{col * SS::W, rest % gm.ny, a.z0 + rest / gm.ny};
+    };
+
+    auto fetch = [&](const Unit &w, int st) {
         TS *seg = reinterpret_cast<TS *>(mine + (size_t)st * SS::STAGE_BYTES);
+        const int lz = w.lz, y = w.y, xw = w.xw;
+        const int zc = (lz + 1) * plane;
+        const int zm = ((lz == 0) ? gm.zlo_src : lz) * plane;
+        const int zq = ((lz == gm.nz - 1) ? gm.zhi_src : lz + 2) * plane;
         const int ym = (y == 0) ? gm.ny - 1 : y - 1;
         const int yq = (y == gm.ny - 1) ? 0 : y + 1;
         const int rc = y * xp, rm = ym * xp, rq = yq * xp;
+        // chunk `lane` of a segment: elements [xw - E + lane E, + E) of the source row,
+        // the outer two wrapped around the row (periodic in x) where the column touches
+        // its ends; chunks past the padded row are not fetched (nobody reads them)
+        int coff = xw - SS::E + lane * SS::E;
+        if (lane == 0 && xw == 0) coff = ((gm.nx - 1) / SS::E) * SS::E;
+        if (lane == SS::CHUNKS - 1 && xw + SS::W >= gm.nx) coff = 0;
+        const bool cpred = lane < SS::CHUNKS && coff >= 0 && coff < xp;
+        const bool kpred = klane >= 0 && klane < SS::KCHUNKS && xw + klane * 16 < xp;
         cp_async16(seg + lane * SS::E, a.pre[0] + (zc + rc + coff), cpred);
 #define MLB_X(i, CX, Z, R)                                                           \
         cp_async16(seg + i * SS::SLICE + lane * SS::E, a.pre[i] + ((Z) + (R) + coff), cpred);
@@ -1160,26 +1177,31 @@ step_stage_kernel(const StepArgs<TS> a, const int rows, const int ncol, const in
         cp_async_commit();
         // (optional) the L2 prefetch of the direct kernel on top: the staged copies
         // then find their lines in L2
-        prefetch_ahead<TS, V, 32, true>(a.pre, gm, a.pf_dz, a.pf_dy, x0, y, lz, lane);
+        prefetch_ahead<TS, V, 32, true>(a.pre, gm, a.pf_dz, a.pf_dy, xw + lane * V, y, lz, lane);
     };
 
-    const bool active = x0 < (a.passthrough ? xp : gm.nx);
-    // positions inside a staged segment: own pack, the cell left of it, the cell right of it
-    const int p = SS::E + lane * V;
-    const int pl = (x0 == 0) ? (gm.nx - 1) % SS::E : p - 1;
-    const int pr = (x0 + V >= gm.nx) ? SS::E + SS::W : p + V;
-    const PushArgs<TS> noph{};
-
-    fetch(y_begin, 0);
-    for (int y = y_begin; y < y_end; ++y) {
-        const int st = (y - y_begin) & 1;
-        if (y + 1 < y_end) {
-            fetch(y + 1, st ^ 1);
+    int u_cur = next_unit();
+    if (u_cur >= ntasks)
+        return;
+    Unit cur = locate(u_cur);
+    fetch(cur, 0);
+    for (int st = 0;; st ^= 1) {
+        const int u_nxt = next_unit();
+        Unit nxt{0, 0, 0};
+        if (u_nxt < ntasks) {
+            nxt = locate(u_nxt);
+            fetch(nxt, st ^ 1);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncwarp();
+        const int x0 = cur.xw + lane * V;
+        const bool active = x0 < (a.passthrough ? xp : gm.nx);
+        // positions inside a staged segment: own pack, the cell left of it, the cell right of it
+        const int p = SS::E + lane * V;
+        const int pl = (x0 == 0) ? (gm.nx - 1) % SS::E : p - 1;
+        const int pr = (x0 + V >= gm.nx) ? SS::E + SS::W : p + V;
         const TS *seg = reinterpret_cast<const TS *>(mine + (size_t)st * SS::STAGE_BYTES);
         uint32_t kpack = 0u;
         T g[Q][V];
@@ -1203,9 +1225,13 @@ step_stage_kernel(const StepArgs<TS> a, const int rows, const int ncol, const in
         }
         __syncwarp();               // every lane holds its pack: the stage may be refilled
         if (active) {
-            const int o_plane = y * xp + x0;
-            vec_finish<TS, V, false>(a, noph, g, kpack, zc + o_plane, o_plane, lz);
+            const int o_plane = cur.y * xp + x0;
+            vec_finish<TS, V, false>(a, noph, g, kpack, (cur.lz + 1) * plane + o_plane, o_plane,
+                                     cur.lz);
         }
+        if (u_nxt >= ntasks)
+            break;
+        cur = nxt;
     }
 }
 
