@@ -548,9 +548,6 @@ int launch_stage(mlb_plan *p, mlb::StepArgs<TS> &a, int nplanes, cudaStream_t st
         MLB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // the launch's work counter: one slot of a small ring, so that launches in flight on
     // different streams (boundary planes / interior of a slab) do not share one
-    if (!p->d_work) {
-        MLB_CUDA(pool_alloc(&p->d_work, 64 * sizeof(unsigned int)));
-    }
     unsigned int *slot = p->d_work + (p->work_next++ & 63);
     MLB_CUDA(cudaMemsetAsync(slot, 0, sizeof(unsigned int), st));
     a.work = slot;
@@ -923,6 +920,7 @@ int mlb_plan_create(mlb_plan **out, int nx, int ny, int nz, int dtype, double om
     p->diag_blocks = p->sms * 8;
     cudaError_t e = pool_alloc(&p->d_partials, sizeof(double) * mlb::DIAG_N * p->diag_blocks);
     if (e == cudaSuccess) e = pool_alloc(&p->d_diag, sizeof(double) * mlb::DIAG_N);
+    if (e == cudaSuccess) e = pool_alloc(&p->d_work, 64 * sizeof(unsigned int));
     if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&p->ev1);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
