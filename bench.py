@@ -97,6 +97,7 @@ def parse():
     ap.add_argument("--extra", action="store_true",
                     help="N > 1: also time c3-weak / c3-strong / c4 (20 steps each) into `extra`")
     ap.add_argument("--no-preflight", action="store_true", help="N > 1: skip the bitwise preflight")
+    ap.add_argument("--preflight-child", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--force-slab", action="store_true",
                     help="run the z-slab driver (halo planes, boundary-first overlap) even on 1 GPU")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
@@ -418,7 +419,8 @@ def preflight(args, rank, world, device, fdev):
     """Small cavity + channel through the very runners that get timed - same
     transport, same one-call loop, two blocks and in place, fp32 and fp64 -
     gathered to rank 0 and compared BITWISE with the CPU oracle (the reference's
-    partition-independence bar, pkg/tests/test_kernels.py:107-126)."""
+    partition-independence bar, pkg/tests/test_kernels.py:107-126).  Returns a
+    record whose "result" is "bitwise" or names the first case that differs."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -432,7 +434,7 @@ def preflight(args, rank, world, device, fdev):
     cav[20:24, 10:14, 3:nz - 2] = B.SOLID
     chan = B.channel_mask(nx, ny, nz, B.cylinder_cells(nx, ny, nz, 8, 40.0, 20.5))
     cases_ = [("cavity", cav, (0.07, 0.0, 0.0), 0.0), ("channel", chan, (0.0, 0.0, 0.0), 0.05)]
-    transports = set()
+    transports, skipped = set(), set()
     n = 0
     for name, grid, wall_u, inlet_u in cases_:
         flags = B.flatten_mask(grid).reshape(nz, ny, nx)
@@ -442,14 +444,21 @@ def preflight(args, rank, world, device, fdev):
             z0, z1 = slab.partition(nz, world)[rank]
             lo, hi = slab.slab_halo_flags(flags, nx, ny, z0, z1)
             part = np.ascontiguousarray(f.reshape(19, nz, ny, nx)[:, z0:z1]).reshape(19, -1)
-            for inplace in (False, True):
+            for inplace in ((False, True) if args.transport == "peer" else (False,)):
                 plan = KernelPlan(nx, ny, z1 - z0, Layout.ROW, prec, flags[z0:z1], 1.3, wall_u,
                                   inlet_u=inlet_u, device=device.index, halo_lo=lo, halo_hi=hi,
                                   slab=True)
                 a = plan.alloc()
                 plan.upload(part, a)
                 if inplace:
-                    runner = slab.open_inplace_runner(plan, a, rank, world)
+                    try:
+                        runner = slab.open_inplace_runner(plan, a, rank, world)
+                    except RuntimeError as exc:
+                        # no peer memory between the ranks (every rank raises alike): the
+                        # in-place slabs cannot run here at all; the two-block run still can
+                        skipped.add(f"in place: {exc}"[:160])
+                        plan.close()
+                        continue
                     runner.c_loop = not args.python_loop
                     runner.run_inplace(a, steps)
                     runner.normalize(a)
@@ -487,13 +496,75 @@ def preflight(args, rank, world, device, fdev):
                 if world > 1:
                     dist.broadcast(flag, src=0)
                 if not bool(flag.item()):
-                    raise SystemExit(f"bench preflight: {name} {prec.token} "
-                                     f"{'in place' if inplace else 'two blocks'} over {world} slabs "
-                                     f"differs from the CPU oracle")
+                    return {"result": f"MISMATCH: {name} {prec.token} "
+                                      f"{'in place' if inplace else 'two blocks'} over {world} slabs "
+                                      f"(halo transport {tr}) differs from the CPU oracle",
+                            "cases": n, "transports": sorted(transports)}
                 n += 1
     return {"result": "bitwise", "cases": n, "transports": sorted(transports),
+            "skipped": sorted(skipped),
             "what": f"cavity + channel {nx}x{ny}x{nz}, fp32 + fp64, {steps} steps, two blocks + in place, "
                     f"{world} z-slab(s), vs the CPU oracle"}
+
+
+def preflight_child(args):
+    """`bench.py --preflight-child`: one rank of the preflight in its OWN process
+    and process group (rendezvous on MASTER_PORT of its environment), so that a
+    protocol problem on hardware this code has never met - a peer mapping that
+    cannot be made, a counter that never arrives - costs a child process and not
+    the benchmark.  Prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    local = 0 if args.share_gpu else int(os.environ.get("LOCAL_RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    fdev = None if args.share_gpu else device
+    if world > 1:
+        init = f"tcp://{os.environ.get('MASTER_ADDR', '127.0.0.1')}:{os.environ['MASTER_PORT']}"
+        if args.share_gpu:
+            dist.init_process_group("gloo", init_method=init, rank=rank, world_size=world)
+        else:
+            dist.init_process_group("nccl", init_method=init, rank=rank, world_size=world,
+                                    device_id=device)
+    try:
+        rec = preflight(args, rank, world, device, fdev)
+        if os.environ.get("MLB_PREFLIGHT_FAIL") == args.transport:   # (test hook for the fallback)
+            rec = {"result": f"MISMATCH: forced by MLB_PREFLIGHT_FAIL={args.transport}"}
+    except BaseException as exc:     # incl. SystemExit from the library layers
+        rec = {"result": f"ERROR: {type(exc).__name__}: {exc}"[:300]}
+    print(json.dumps(rec), flush=True)
+    if world > 1:
+        try:
+            dist.destroy_process_group()
+        except Exception:
+            pass
+    return 0
+
+
+def preflight_guarded(args, world, timeout_s=240):
+    """Run this rank's part of the preflight in a child process with a hard
+    time limit; returns its record (result "bitwise", "MISMATCH ...", "ERROR ..."
+    or "TIMEOUT")."""
+    env = dict(os.environ)
+    env["MASTER_PORT"] = str(20000 + (int(env.get("MASTER_PORT", "29500")) + 17) % 40000)
+    env["TORCHELASTIC_USE_AGENT_STORE"] = "False"
+    cmd = [sys.executable, os.path.abspath(__file__), "--preflight-child", "--gpus", str(world),
+           "--transport", args.transport]
+    if args.share_gpu:
+        cmd.append("--share-gpu")
+    if args.python_loop:
+        cmd.append("--python-loop")
+    try:
+        res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout_s)
+    except subprocess.TimeoutExpired:
+        return {"result": f"TIMEOUT: the preflight did not finish within {timeout_s} s"}
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    if res.returncode != 0 or not lines:
+        tail = (res.stderr.strip().splitlines() or ["no output"])[-1]
+        return {"result": f"ERROR: preflight child exited with {res.returncode}: {tail}"[:300]}
+    return json.loads(lines[-1])
 
 
 def run_device(wl, args, prec_tok, rank, world, device, fdev, steps, warmup, clocks=False):
@@ -640,6 +711,8 @@ def run_device(wl, args, prec_tok, rank, world, device, fdev, steps, warmup, clo
 
 def main():
     args = parse()
+    if args.preflight_child:
+        return preflight_child(args)
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -697,11 +770,27 @@ def main():
         torch.cuda.synchronize()
 
     # ---- N > 1: bitwise preflight through the runners that get timed ---------
+    # In a child process per rank with a time limit.  If the fused peer-store exchange
+    # fails it (mismatch, error or no answer) the run falls back to the send/recv
+    # transport - preflighted the same way - and says so; if that fails too the bench
+    # aborts: a number from a path that does not reproduce the oracle is worthless.
     pre = None
     if slab_mode and not args.no_preflight:
-        signal.alarm(600)           # a protocol bug must not hang the box
-        pre = preflight(args, rank, world, device, fdev)
-        signal.alarm(0)
+        def agreed(rec):
+            ok = torch.tensor([1 if rec.get("result") == "bitwise" else 0], dtype=torch.int32,
+                              device=device if (world > 1 and fdev is not None) else "cpu")
+            if world > 1:
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            return bool(ok.item())
+        pre = preflight_guarded(args, world)
+        if not agreed(pre) and args.transport == "peer":
+            first = pre.get("result", "?")
+            args.transport = "nccl"
+            pre = preflight_guarded(args, world)
+            pre["fallback"] = f"the peer-memory ring failed the preflight on some rank ({first}); " \
+                              f"halo exchange by send/recv instead"
+        if not agreed(pre):
+            raise SystemExit(f"bench preflight failed: {pre.get('result')}")
 
     # ---- device-timed run: W warm-up, then exactly K steps -------------------
     main_run = run_device(wl, args, prec_tok, rank, world, device, fdev, args.steps, args.warmup,
