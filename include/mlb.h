@@ -103,7 +103,12 @@ int mlb_plan_set_physics(mlb_plan *plan, double omega, const double wall_u[3],
  * = packs of consecutive cells, LX = 8 / 16 / 32 packs per warp row, W = 1:
  * 16-byte packs (fp32 / fp64), W = 2: 8-byte packs (fp32: two cells, for even
  * rows that 4 does not divide; fp16 storage: four cells; mixed2: two cells),
- * W = 3: 4-byte packs (fp16 storage) */
+ * W = 3: 4-byte packs (fp16 storage); 4000 = the staged kernel (fp16 storage and
+ * fp32 storage / fp64 arithmetic: the row segments a warp pulls from travel through
+ * shared memory with cp.async one row ahead of the arithmetic, warp rows handed out
+ * in order from a work counter; other dtypes fall back to the automatic choice).
+ * Pack kernels serve any row length: a row the pack does not divide ends in a
+ * pack of real cells + row padding. */
 int mlb_plan_set_variant(mlb_plan *plan, int variant);
 /* name of the fused kernel mlb_step will launch for this plan (for reports) */
 const char *mlb_plan_kernel_name(const mlb_plan *plan);
@@ -199,7 +204,7 @@ int mlb_run_steps(mlb_plan *plan, void *d_a, void *d_b, int nsteps,
  * mlb_inplace_normalize brings it back to 0 without stepping.  *repr is
  * updated by both calls.  Wall cells are never modified.  INLET / OUTLET
  * cells are served by the pack kernels only (variant W*1000 + LX, or auto
- * with nx >= 128), which apply the open-boundary pass inside the step when
+ * with nx >= 128; any row length), which apply the open-boundary pass inside the step when
  * every outlet cell's x-1 neighbour lies in the same pack and no outlet cell
  * copies from another; otherwise, and for MLB_Z_HALO plans, the call is
  * rejected (MLB_EUNSUPPORTED). */

@@ -1479,7 +1479,7 @@ static int check_inplace(const mlb_plan *p, const void *d_f, const int *repr)
                     "(whole domain on one GPU)");
     if (!aa_open_ok(p, resolve_aa_variant(p)))
         return fail(MLB_EUNSUPPORTED, "the in-place update handles walls only unless a pack "
-                    "kernel runs (nx a multiple of the pack, variant W*1000 + LX or auto with "
+                    "kernel runs (variant W*1000 + LX, or auto with "
                     "nx >= 128) and every outlet cell has its x-1 neighbour in the same pack; this "
                     "geometry has %lld inlet and %lld outlet cells - use the two-buffer path",
                     p->n_in, p->n_out);
@@ -1533,8 +1533,8 @@ int mlb_step_inplace_range(mlb_plan *p, void *d_f, int repr, int z0, int z1, voi
                     "(with one slab: the block itself)");
     const int variant = resolve_aa_variant(p);
     if (!aa_uses_packs(p, variant))
-        return fail(MLB_EUNSUPPORTED, "the in-place slab step needs a pack kernel (nx a multiple "
-                    "of the pack; variant W*1000 + LX, or auto with nx >= 128)");
+        return fail(MLB_EUNSUPPORTED, "the in-place slab step needs a pack kernel (variant "
+                    "W*1000 + LX, or auto with nx >= 128)");
     if (!aa_open_ok(p, variant))
         return fail(MLB_EUNSUPPORTED, "the in-place update handles walls only unless every outlet "
                     "cell has its x-1 neighbour in the same pack; this geometry has %lld inlet "
