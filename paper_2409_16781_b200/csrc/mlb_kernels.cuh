@@ -785,30 +785,72 @@ template <> struct PackIO<float, 4> {
     { const float4 v = *reinterpret_cast<const float4 *>(p); o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
     static __device__ __forceinline__ void store(float *p, const float (&o)[4])
     { *reinterpret_cast<float4 *>(p) = make_float4(o[0], o[1], o[2], o[3]); }
+    // all but the last / all but the first cell of the pack, in the widest aligned pieces
+    // (the in-place pull half at the ends of a warp row; `full` picks the whole pack instead)
+    static __device__ __forceinline__ void store_head(float *p, const float (&o)[4], bool full)
+    {
+        if (full) { store(p, o); return; }
+        *reinterpret_cast<float2 *>(p) = make_float2(o[0], o[1]);
+        p[2] = o[2];
+    }
+    static __device__ __forceinline__ void store_tail(float *p, const float (&o)[4], bool full)
+    {
+        if (full) { store(p, o); return; }
+        p[1] = o[1];
+        *reinterpret_cast<float2 *>(p + 2) = make_float2(o[2], o[3]);
+    }
 };
 template <> struct PackIO<float, 2> {   // 8-byte packs: rows whose length is even but not a multiple of 4
     static __device__ __forceinline__ void load(const float *p, float (&o)[2])
     { const float2 v = *reinterpret_cast<const float2 *>(p); o[0] = v.x; o[1] = v.y; }
     static __device__ __forceinline__ void store(float *p, const float (&o)[2])
     { *reinterpret_cast<float2 *>(p) = make_float2(o[0], o[1]); }
+    static __device__ __forceinline__ void store_head(float *p, const float (&o)[2], bool full)
+    { if (full) store(p, o); else p[0] = o[0]; }
+    static __device__ __forceinline__ void store_tail(float *p, const float (&o)[2], bool full)
+    { if (full) store(p, o); else p[1] = o[1]; }
 };
 template <> struct PackIO<double, 2> {
     static __device__ __forceinline__ void load(const double *p, double (&o)[2])
     { const double2 v = *reinterpret_cast<const double2 *>(p); o[0] = v.x; o[1] = v.y; }
     static __device__ __forceinline__ void store(double *p, const double (&o)[2])
     { *reinterpret_cast<double2 *>(p) = make_double2(o[0], o[1]); }
+    static __device__ __forceinline__ void store_head(double *p, const double (&o)[2], bool full)
+    { if (full) store(p, o); else p[0] = o[0]; }
+    static __device__ __forceinline__ void store_tail(double *p, const double (&o)[2], bool full)
+    { if (full) store(p, o); else p[1] = o[1]; }
 };
 template <> struct PackIO<f32w, 2> {
     static __device__ __forceinline__ void load(const f32w *p, double (&o)[2])
     { const float2 v = *reinterpret_cast<const float2 *>(p); o[0] = (double)v.x; o[1] = (double)v.y; }
     static __device__ __forceinline__ void store(f32w *p, const double (&o)[2])
     { *reinterpret_cast<float2 *>(p) = make_float2((float)o[0], (float)o[1]); }
+    static __device__ __forceinline__ void store_head(f32w *p, const double (&o)[2], bool full)
+    {
+        const float2 r = make_float2((float)o[0], (float)o[1]);   // one rounding per value either way
+        if (full) *reinterpret_cast<float2 *>(p) = r; else p[0].v = r.x;
+    }
+    static __device__ __forceinline__ void store_tail(f32w *p, const double (&o)[2], bool full)
+    {
+        const float2 r = make_float2((float)o[0], (float)o[1]);
+        if (full) *reinterpret_cast<float2 *>(p) = r; else p[1].v = r.y;
+    }
 };
 template <> struct PackIO<__half, 2> {
     static __device__ __forceinline__ void load(const __half *p, float (&o)[2])
     { const __half2 v = *reinterpret_cast<const __half2 *>(p); o[0] = __low2float(v); o[1] = __high2float(v); }
     static __device__ __forceinline__ void store(__half *p, const float (&o)[2])
     { *reinterpret_cast<__half2 *>(p) = __floats2half2_rn(o[0], o[1]); }
+    static __device__ __forceinline__ void store_head(__half *p, const float (&o)[2], bool full)
+    {
+        const __half2 r = __floats2half2_rn(o[0], o[1]);
+        if (full) *reinterpret_cast<__half2 *>(p) = r; else p[0] = __low2half(r);
+    }
+    static __device__ __forceinline__ void store_tail(__half *p, const float (&o)[2], bool full)
+    {
+        const __half2 r = __floats2half2_rn(o[0], o[1]);
+        if (full) *reinterpret_cast<__half2 *>(p) = r; else p[1] = __high2half(r);
+    }
 };
 template <> struct PackIO<__half, 4> {
     static __device__ __forceinline__ void load(const __half *p, float (&o)[4])
@@ -825,6 +867,33 @@ template <> struct PackIO<__half, 4> {
         u.x = *reinterpret_cast<const unsigned *>(&a);
         u.y = *reinterpret_cast<const unsigned *>(&b);
         *reinterpret_cast<uint2 *>(p) = u;
+    }
+    // the two packed words are converted ONCE (F2FP) whichever pieces get stored
+    static __device__ __forceinline__ void store_head(__half *p, const float (&o)[4], bool full)
+    {
+        const __half2 a = __floats2half2_rn(o[0], o[1]), b = __floats2half2_rn(o[2], o[3]);
+        if (full) {
+            uint2 u;
+            u.x = *reinterpret_cast<const unsigned *>(&a);
+            u.y = *reinterpret_cast<const unsigned *>(&b);
+            *reinterpret_cast<uint2 *>(p) = u;
+        } else {
+            *reinterpret_cast<__half2 *>(p) = a;
+            p[2] = __low2half(b);
+        }
+    }
+    static __device__ __forceinline__ void store_tail(__half *p, const float (&o)[4], bool full)
+    {
+        const __half2 a = __floats2half2_rn(o[0], o[1]), b = __floats2half2_rn(o[2], o[3]);
+        if (full) {
+            uint2 u;
+            u.x = *reinterpret_cast<const unsigned *>(&a);
+            u.y = *reinterpret_cast<const unsigned *>(&b);
+            *reinterpret_cast<uint2 *>(p) = u;
+        } else {
+            p[1] = __high2half(a);
+            *reinterpret_cast<__half2 *>(p + 2) = b;
+        }
     }
 };
 // the kind bytes of a pack, as one word (byte j = cell j)
@@ -1476,10 +1545,9 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
                 T o[V];                                                               \
                 _Pragma("unroll") for (int j = 0; j < V - 1; ++j) o[j] = g[opp(i)][j + 1]; \
                 o[V - 1] = nb[n];                                                     \
-                if (bulk_r) PackIO<TS, V>::store(base, o);                            \
-                _Pragma("unroll") for (int j = 0; j < V - 1; ++j)                     \
-                    if (!bulk_r) base[j] = Store<TS>::down(o[j]);                     \
-                if (!bulk_l) *MLB_T(i, Z, R, xl) = Store<TS>::down(g[opp(i)][0]);     \
+                PackIO<TS, V>::store_head(base, o, bulk_r);                           \
+                { const TS v0 = Store<TS>::down(g[opp(i)][0]);                        \
+                  if (!bulk_l) *MLB_T(i, Z, R, xl) = v0; }                            \
                 ++n;                                                                  \
             }
             MLB_DIRS(MLB_X)
@@ -1503,10 +1571,9 @@ aa_pull_vec_kernel(const AAArgs<TS> a)
                 T o[V];                                                               \
                 _Pragma("unroll") for (int j = 1; j < V; ++j) o[j] = g[opp(i)][j - 1]; \
                 o[0] = nb[n];                                                         \
-                if (bulk_l) PackIO<TS, V>::store(base, o);                            \
-                _Pragma("unroll") for (int j = 1; j < V; ++j)                         \
-                    if (!bulk_l) base[j] = Store<TS>::down(o[j]);                     \
-                if (!bulk_r) *MLB_T(i, Z, R, xr) = Store<TS>::down(g[opp(i)][V - 1]); \
+                PackIO<TS, V>::store_tail(base, o, bulk_l);                           \
+                { const TS v1 = Store<TS>::down(g[opp(i)][V - 1]);                    \
+                  if (!bulk_r) *MLB_T(i, Z, R, xr) = v1; }                            \
                 ++n;                                                                  \
             }
             MLB_DIRS(MLB_X)
