@@ -47,7 +47,9 @@ The one JSON line carries
   cpu_baseline_ref2d  the UNMODIFIED reference (lb2d, numba D2Q9, installed
              into baseline/_ref) on its own 2-D cavity, as context;
   extra      (N = 1 by default, `--extra` at N > 1) short device-timed runs
-             of the other BASELINE configurations.
+             of the other BASELINE configurations: c3-strong, c3-weak, c4, and
+             at N = 1 also c0 (64^3 fp64, L2-resident, loop replayed from a CUDA
+             graph) and c1 (the periodic 256^3 box, fp64 and fp32).
 
 `--impl reference` times the CPU port alone, on the same config, each step
 a bounded z-slice of the cavity so the run ends within a few minutes.  The
@@ -85,7 +87,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="default", choices=["default", "c3-weak", "c3-strong", "c4"],
+    ap.add_argument("--config", default="default", choices=["default", "c0", "c1", "c3-weak", "c3-strong", "c4"],
                     help="which BASELINE.json configuration to time (see the module docstring)")
     ap.add_argument("--edge", "--n", dest="n", type=int, default=0,
                     help="default config only: override the edge length (debug)")
@@ -136,6 +138,14 @@ class Workload:
             self.strong = scaling == "strong" and world > 1
             self.nz = e if (self.strong or world == 1) else e * world
             self.label = "configs[2]"
+        elif name == "c0":
+            # configs[0]: the reference's CPU-runnable case (parity config; here: throughput)
+            self.case, self.nx, self.ny, self.nz = "ldc", 64, 64, 64
+            self.strong, self.label = True, "configs[0]"
+        elif name == "c1":
+            # configs[1]: periodic box of the Taylor-Green case (all fluid, no walls)
+            self.case, self.nx, self.ny, self.nz = "periodic", 256, 256, 256
+            self.strong, self.label = True, "configs[1] geometry"
         elif name == "c3-weak":
             self.case, self.nx, self.ny, self.nz = "ldc", 1024, 1024, 128 * world
             self.strong, self.label = False, "configs[3] weak"
@@ -152,8 +162,8 @@ class Workload:
         if self.nz % world:
             raise SystemExit(f"{name}: {self.nz} planes do not split evenly over {world} ranks")
         self.nzl = self.nz // world
-        if self.case == "ldc":
-            self.re, self.u0 = RE, U0
+        if self.case in ("ldc", "periodic"):
+            self.re, self.u0 = (100.0 if name == "c0" else RE), U0
             self.wall_u, self.inlet_u, self.length = (U0, 0.0, 0.0), 0.0, self.ny
         else:
             self.re, self.u0 = CH_RE, CH_U0
@@ -170,6 +180,8 @@ class Workload:
         from paper_2409_16781_b200 import boundaries as B
         if self.case == "ldc":
             m = B.cavity_mask(self.nx, self.ny, 1, z_walls=False)
+        elif self.case == "periodic":
+            m = B.open_mask(self.nx, self.ny, 1)
         else:
             d = self.ny // 8    # the reference's obstacle placement (lb2d cases.py:62-75)
             obs = B.cylinder_cells(self.nx, self.ny, 1, d, 6.0 * d, self.ny / 2 + 0.5)
@@ -185,20 +197,22 @@ class Workload:
         out = np.empty((z1 - z0, self.ny, self.nx), dtype=np.uint8)
         for k, z in enumerate(range(z0, z1)):
             zz = z % self.nz
-            out[k] = B.SOLID if zz in (0, self.nz - 1) else sec
+            out[k] = B.SOLID if (zz in (0, self.nz - 1) and self.case != "periodic") else sec
         return out
 
     def init_values(self, dtype):
         """The 19 population values every cell starts from (uniform state)."""
         import numpy as np
         from paper_2409_16781_b200 import lattice as L
-        if self.case == "ldc":
+        if self.case in ("ldc", "periodic"):
             return np.asarray(L.W, dtype=np.float64).astype(dtype)
         return L.equilibrium(1.0, self.u0, 0.0, 0.0).astype(dtype)
 
     def describe(self, prec, transport=None):
         size = f"{self.nx}^3" if self.nx == self.ny == self.nz else f"{self.nx}x{self.ny}x{self.nz}"
         what = ("lid-driven cavity" if self.case == "ldc"
+                else "periodic box (the Taylor-Green case's geometry, uniform state)"
+                if self.case == "periodic"
                 else "channel past a bounce-back cylinder (inlet / outlet faces)")
         scal = f", z-slab {'strong' if self.strong else 'weak'} scaling" if self.world > 1 else ""
         cfg = {
@@ -208,8 +222,12 @@ class Workload:
             "decomposition": (f"{self.world} z-slab(s), 5-population halos" if self.world > 1
                               else "single GPU"),
             "blocks_per_gpu": 1 if self.inplace else 2,
-            "l2_policy": f"inputs exceed L2: {'one population block' if self.inplace else 'two population blocks'} of "
-                         f"{19 * self.nx * self.ny * self.nzl * PREC_BYTES[prec] / 1e9:.1f} GB per GPU vs 126 MB L2",
+            "l2_policy": (
+                f"inputs exceed L2: {'one population block' if self.inplace else 'two population blocks'} of "
+                f"{19 * self.nx * self.ny * self.nzl * PREC_BYTES[prec] / 1e9:.1f} GB per GPU vs 126 MB L2"
+                if 19 * self.nx * self.ny * self.nzl * PREC_BYTES[prec] * (1 if self.inplace else 2) > 126e6
+                else f"NOT flushed: the whole state ({19 * self.nx * self.ny * self.nzl * PREC_BYTES[prec] * (1 if self.inplace else 2) / 1e6:.0f} MB) "
+                     f"fits the 126 MB L2 - a small-domain figure, not an HBM figure"),
         }
         if transport:
             cfg["halo_transport"] = transport
@@ -924,24 +942,32 @@ def main():
         def on_alarm(signum, frame):
             raise TimeoutError("extra workloads timed out")
         signal.signal(signal.SIGALRM, on_alarm)
-        for name in ("c3-strong", "c3-weak", "c4"):
+        todo = [("c3-strong", "single", 20), ("c3-weak", "single", 20), ("c4", "single", 20)]
+        if world == 1:
+            todo += [("c0", "double", 100), ("c1", "double", 50), ("c1", "single", 50)]
+        for name, xprec, xsteps in todo:
             if world == 1 and name == "c3-weak":
                 continue        # 1024 x 1024 x 128 on one GPU says nothing c3-strong does not
+            key = name if name not in ("c0", "c1") else f"{name}-{PREC_TAG[xprec]}"
             try:
                 signal.alarm(300)
                 xw = Workload(name, world)
-                r = run_device(xw, args, "single", rank, world, device, fdev, 20, 3)
+                # (c0 replays its loop from a CUDA graph: captured during the warm-up)
+                xwarm = 64 if name == "c0" else 3
+                r = run_device(xw, args, xprec, rank, world, device, fdev, xsteps, xwarm)
                 signal.alarm(0)
-                extra[name] = {
-                    "workload": xw.describe("single", r["transport"])["workload"],
-                    "value": r["value"], "unit": "MLUPS", "steps": 20, "warmup": 3,
-                    "ms_per_step": r["ms"] / 20, "blocks_per_gpu": 1 if xw.inplace else 2,
+                extra[key] = {
+                    "workload": xw.describe(xprec, r["transport"])["workload"],
+                    "l2_policy": xw.describe(xprec)["l2_policy"],
+                    "value": r["value"], "unit": "MLUPS", "steps": xsteps, "warmup": xwarm,
+                    "bytes_per_update": 38 * PREC_BYTES[xprec],
+                    "ms_per_step": r["ms"] / xsteps, "blocks_per_gpu": 1 if xw.inplace else 2,
                     "nz_per_gpu": xw.nzl, "cells_per_gpu": r["cells_rank"], "kernel": r["kernel"],
                     "frac_of_hbm_peak": None, "host_us_per_step": r["host_us_per_step"],
                     "check": {"mass": r["diag"]["mass"], "max_u": r["diag"]["max_u"]}}
             except (Exception, SystemExit) as exc:   # never lose the main line to an extra
                 signal.alarm(0)
-                extra[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+                extra[key] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
                 if world > 1:
                     break       # the ranks may no longer be in step
 
@@ -984,7 +1010,7 @@ def main():
     if extra:
         for name, rec in extra.items():
             if "ms_per_step" in rec:
-                rec["frac_of_hbm_peak"] = (152 * rec["cells_per_gpu"]
+                rec["frac_of_hbm_peak"] = (rec["bytes_per_update"] * rec["cells_per_gpu"]
                                            / (rec["ms_per_step"] * 1e-3) / 1e9 / peak)
 
     ref2d = None
