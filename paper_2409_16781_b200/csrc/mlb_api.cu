@@ -817,7 +817,9 @@ int launch_open(mlb_plan *p, void *fpost, int z0, int z1, cudaStream_t st)
     if (o1 > o0) {
         const long long n = o1 - o0;
         const unsigned blocks = (unsigned)((n + 127) / 128);
-        T *tmp = static_cast<T *>(p->d_out_tmp);
+        // (each plane range its own part of the scratch: the boundary planes and the
+        // interior of a slab run this pass concurrently on two streams)
+        T *tmp = p->d_out_tmp ? static_cast<T *>(p->d_out_tmp) + o0 : nullptr;
         if (!p->out_chained) {
             mlb::outlet_kernel<T><<<blocks, 128, 0, st>>>(f, tmp, p->d_out + o0, n,
                                                           p->lay.pop, p->n_out, 0);

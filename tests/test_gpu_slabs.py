@@ -190,3 +190,44 @@ def test_inplace_slab_single_rank(geom, tag, variant, steps, overlap, rng):
         want.copy(), want.copy(), 2)
     np.testing.assert_array_equal(out, want2)
     ring.close()
+
+
+@pytest.mark.parametrize("tag", ["f32", "f64"])
+@pytest.mark.parametrize("c_loop", [True, False])
+def test_chained_outlets_with_boundary_and_interior_in_flight_together(tag, c_loop, rng):
+    """An outlet cell whose source is itself an outlet cell makes the open-boundary
+    pass gather-then-scatter through a scratch block (numpy evaluates the right-
+    hand side first, engine.py:179-180).  In the z-slab schedule the pass runs on
+    the boundary planes (high-priority stream) and on the interior (main stream)
+    AT THE SAME TIME: each plane range must use its own part of the scratch.
+    (Found by the fuzz suite at 4000 cases: the two launches shared it.)"""
+    from paper_2409_16781_b200 import slab
+    from paper_2409_16781_b200.kernels import KernelPlan
+    prec = {"f32": Precision.SINGLE, "f64": Precision.DOUBLE}[tag]
+    nx, ny, nz, steps = 96, 48, 24, 25
+    grid = B.channel_mask(nx, ny, nz, B.sphere_cells(nx, ny, nz, 10, 30.0, 24.0, 12.0),
+                          z_walls=False)
+    grid[nx - 2, 1:-1, :] = B.OUTLET          # two outlet columns: x = nx-1 copies x = nx-2
+    flags = B.flatten_mask(grid).reshape(nz, ny, nx)
+    f = random_block(rng, grid.size, prec.storage)
+    want = CpuOracle(nx, ny, nz, flags, 1.2, (0.0, 0.0, 0.0), 0.05, threads=8).run(
+        f.copy(), f.copy(), steps)
+    lo, hi = slab.slab_halo_flags(flags, nx, ny, 0, nz)
+    plan = KernelPlan(nx, ny, nz, Layout.ROW, prec, flags, 1.2, (0.0, 0.0, 0.0), inlet_u=0.05,
+                      halo_lo=lo, halo_hi=hi, slab=True)
+    with pytest.raises(ValueError, match="outlet"):
+        plan.set_passthrough(True)            # chained outlets: strict stores, list-driven pass
+    for rep in range(3):                      # a race shows up some of the time
+        a, b = plan.alloc(), plan.alloc()
+        for blk in (a, b):
+            blk.tensor.fill_(float("nan"))
+            plan.upload(f, blk)
+        ring = slab.PeerRing(plan, [a, b])
+        runner = slab.DistSlab(slab.CudaStepper(plan), nz, overlap=True, ring=ring, c_loop=c_loop)
+        runner.exchange(a)
+        newest, _ = runner.run(a, b, steps)
+        runner.finish()
+        got = np.empty_like(f)
+        plan.download(newest, got)
+        ring.close()
+        np.testing.assert_array_equal(got, want)
