@@ -1947,9 +1947,10 @@ int mlb_run_steps_host(mlb_plan *p, const void *h_in, void *h_out, void *d_a, vo
     if (!p->up_stream) MLB_CUDA(cudaStreamCreateWithFlags(&p->up_stream, cudaStreamNonBlocking));
     if (!p->down_stream) MLB_CUDA(cudaStreamCreateWithFlags(&p->down_stream, cudaStreamNonBlocking));
     const int nz = p->nz;
-    int cz = chunk_planes > 0 ? chunk_planes : (nz + 127) / 128;
-    // a chunk of a population should stay at least 1 MB (copy efficiency)
-    while (cz < nz && (size_t)cz * p->lay.plane * p->lay.itemsize < (1u << 20)) ++cz;
+    int cz = chunk_planes > 0 ? (chunk_planes < nz ? chunk_planes : nz) : (nz + 127) / 128;
+    // automatic choice: a chunk of a population should stay at least 1 MB (copy efficiency)
+    while (chunk_planes <= 0 && cz < nz && (size_t)cz * p->lay.plane * p->lay.itemsize < (1u << 20))
+        ++cz;
     const int C = (nz + cz - 1) / cz;
     auto zlo = [&](int c) { return c * cz; };
     auto zhi = [&](int c) { return (c + 1) * cz < nz ? (c + 1) * cz : nz; };

@@ -121,6 +121,27 @@ def test_random_case_every_kernel_family_bitwise(seed):
         np.testing.assert_array_equal(got, want, err_msg=f"in place, case {seed}")
     plan.close()
 
+    # the whole run on host blocks with upload, steps and download overlapped chunk by
+    # chunk (mlb_run_steps_host, one plane per chunk): needs a domain closed in z, so the
+    # same case with planes 0 and nz-1 walled off
+    if nz >= 4:
+        gz = grid.copy()
+        gz[:, :, 0] = B.SOLID
+        gz[:, :, -1] = B.MOVING_WALL
+        mz = B.flatten_mask(gz)
+        oz = CpuOracle(nx, ny, nz, mz, omega, wall_u, inlet_u,
+                       compute=np.float64 if prec is Precision.MIXED2 else None)
+        wz = oz.run(f.copy(), f.copy(), steps)
+        pz = KernelPlan(nx, ny, nz, Layout.ROW, prec, mz, omega, wall_u, inlet_u=inlet_u,
+                        defer_flags=bool(seed % 2))
+        pz.set_variant(variant)
+        a, b = pz.alloc(), pz.alloc()
+        out = np.empty_like(f)
+        _, _, _, overlapped = pz.run_host(f, out, a, b, steps, chunk_planes=1)
+        assert overlapped
+        np.testing.assert_array_equal(out, wz, err_msg=f"overlapped host run, case {seed}")
+        pz.close()
+
     # the z-slab driver, ring closed on the slab itself
     flags3 = mask.reshape(nz, ny, nx)
     lo, hi = slab.slab_halo_flags(flags3, nx, ny, 0, nz)
