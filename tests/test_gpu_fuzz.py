@@ -29,12 +29,18 @@ PACKS = {"f32": [1008, 1016, 1032, 2008, 2016, 2032], "f64": [1008, 1016, 1032],
          "f16": [2008, 2016, 2032, 3008, 3016, 3032, 4000], "m2": [2008, 2016, 2032, 4000]}
 
 
+BIG = __import__("os").environ.get("MLB_FUZZ_SCALE") == "big"
+
+
 def draw_case(seed):
     r = np.random.default_rng(seed)
     tag = ["f32", "f64", "f16", "m2"][r.integers(4)]
     aligned = r.random() < 0.7
     nx = int(r.integers(2, 19)) * 4 if aligned else int(r.integers(5, 40))
     ny, nz = int(r.integers(3, 9)), int(r.integers(3, 8))
+    if BIG:   # MLB_FUZZ_SCALE=big: grids on which concurrent launches really overlap
+        nx = int(r.integers(16, 41)) * 4 if aligned else int(r.integers(60, 170))
+        ny, nz = int(r.integers(8, 40)), int(r.integers(6, 24))
     grid = B.open_mask(nx, ny, nz)
     u = r.random(grid.shape)
     p_solid, p_move = r.choice([0.0, 0.05, 0.25]), r.choice([0.0, 0.03, 0.1])
