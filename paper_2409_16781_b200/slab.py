@@ -583,6 +583,19 @@ def open_inplace_runner(plan, f, rank=0, world=1, group=None, overlap=True):
             ring.close()
         raise RuntimeError("the in-place update over z-slabs needs peer memory between the "
                            "ranks (CUDA IPC): " + (err or "a peer rank could not map the ring"))
+    # Can every rank's slab be served in place (pack kernel, outlet cells inside their
+    # packs)?  The geometry differs from slab to slab, so one rank alone might refuse at
+    # its first launch while its neighbours wait for its step counter: ask all, agree.
+    below, above = ring.targets(0)
+    try:
+        plan.step_inplace_range(f, 0, 0, below, above)     # empty plane range: the checks only
+        why = None
+    except ValueError as exc:
+        why = str(exc)
+    if not _agree(why is None, world, group, plan.device):
+        ring.close()
+        raise ValueError("the in-place update cannot serve the slab of some rank"
+                         + (f" (this rank: {why})" if why else ""))
     runner = DistSlab(CudaStepper(plan), plan.nz, rank, world, group, overlap=overlap, ring=ring)
     runner.exchange(f)
     return runner

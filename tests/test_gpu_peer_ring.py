@@ -276,3 +276,91 @@ def test_peer_ring_does_not_depend_on_the_torch_allocator(tmp_path, monkeypatch)
     mp.spawn(_engine_worker, args=(2, _free_port(), "ldc", "f32", str(tmp_path), False),
              nprocs=2, join=True)
     assert all((tmp_path / f"ok{r}").exists() for r in range(2))
+
+
+def _random_worker(rank, world, port, seeds, out_dir):
+    """Many random cases through ONE set of processes: per case a fresh plan, ring
+    (IPC handles exchanged and mapped anew) and runner; rank 0 gathers and compares."""
+    signal.alarm(420)
+    import torch.distributed as dist
+    from paper_2409_16781_b200 import slab
+    from paper_2409_16781_b200.kernels import KernelPlan
+    from .test_gpu_fuzz import PREC, draw_case
+    _, fdev = init_ranks(rank, world, port)
+    bad = []
+    try:
+        for seed in seeds:
+            tag, grid, omega, wall_u, inlet_u, variant, steps = draw_case(seed)
+            prec = PREC[tag]
+            nx, ny, nz = grid.shape
+            if nz < world:
+                continue
+            flags = B.flatten_mask(grid).reshape(nz, ny, nx)
+            f = random_block(np.random.default_rng(1000 + seed), grid.size, prec.storage)
+            z0, z1 = slab.partition(nz, world)[rank]
+            n = z1 - z0
+            lo, hi = slab.exchange_flag_halos(flags[z0:z1], rank, world, device=fdev)
+            plan = KernelPlan(nx, ny, n, Layout.ROW, prec, flags[z0:z1], omega, wall_u,
+                              inlet_u=inlet_u, halo_lo=lo, halo_hi=hi, slab=True)
+            plan.set_variant(variant if variant != 4000 or seed % 2 else 0)
+            part = np.ascontiguousarray(f.reshape(19, nz, ny, nx)[:, z0:z1]).reshape(19, -1)
+            inplace = seed % 3 == 0 and 1000 <= variant < 4000
+            blocks = [plan.alloc()] if inplace else [plan.alloc(), plan.alloc()]
+            for blk in blocks:
+                blk.tensor.fill_(float("nan"))
+                plan.upload(part, blk)
+            if not inplace:
+                try:
+                    plan.set_passthrough(True)
+                except ValueError:
+                    pass
+            served = True
+            if inplace:
+                try:    # (raises on EVERY rank if some rank's slab cannot be served in place)
+                    runner = slab.open_inplace_runner(plan, blocks[0], rank, world,
+                                                      overlap=bool(seed % 2))
+                    runner.c_loop = bool(seed % 7)
+                    runner.run_inplace(blocks[0], steps)
+                    runner.normalize(blocks[0])
+                    newest, ring = blocks[0], runner.ring
+                except ValueError:
+                    served, ring = False, None
+            else:
+                ring = slab.PeerRing(plan, blocks, rank, world, wait_mode=2 if seed % 5 == 0 else 0)
+                runner = slab.DistSlab(slab.CudaStepper(plan), n, rank, world,
+                                       overlap=bool(seed % 2), ring=ring, c_loop=bool(seed % 7))
+                runner.exchange(blocks[0])
+                newest, _ = runner.run(blocks[0], blocks[1], steps)
+                runner.finish()
+            out = np.empty_like(part)
+            if served:
+                plan.download(newest, out)
+            if ring is not None:
+                ring.close()
+            plan.close()
+            parts = [None] * world
+            dist.all_gather_object(parts, out.reshape(19, n, ny, nx))
+            if rank == 0 and served:
+                got = np.concatenate(parts, axis=1).reshape(19, -1)
+                want = CpuOracle(nx, ny, nz, flags, omega, wall_u, inlet_u,
+                                 compute=np.float64 if prec is Precision.MIXED2 else None).run(
+                    f.copy(), f.copy(), steps)
+                if not np.array_equal(got, want):
+                    bad.append(seed)
+        if rank == 0:
+            open(os.path.join(out_dir, "bad.txt"), "w").write(" ".join(map(str, bad)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_ring_random_cases_across_processes(world, tmp_path):
+    """The fuzz suite's random cases (shapes, flags incl. chained outlets, dtypes,
+    variants) through the peer ring ACROSS processes: two blocks and in place,
+    overlap on / off, one-call loop and Python schedule, both wait mechanisms.
+    MLB_RING_CASES (default 16) cases per world size through one set of processes."""
+    import torch.multiprocessing as mp
+    n = int(os.environ.get("MLB_RING_CASES", "16"))
+    mp.spawn(_random_worker, args=(world, _free_port(), list(range(500, 500 + n)), str(tmp_path)),
+             nprocs=world, join=True)
+    assert open(tmp_path / "bad.txt").read().strip() == ""
