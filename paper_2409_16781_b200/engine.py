@@ -563,9 +563,22 @@ def _run_slabs(state, config, on_output, on_checkpoint, probe):
     flags = state.mask.reshape(nz, ny, nx)
     lo, hi = slab.slab_halo_flags(flags, nx, ny, z0, z1)
     tile = config.schedule.resolve(nx, ny, n, state.layout)
-    plan = KernelPlan(nx, ny, n, state.layout, state.precision, flags[z0:z1], state.params.omega,
-                      state.wall_u, tile, inlet_u=state.inlet_u, device=config.device,
-                      halo_lo=lo, halo_hi=hi, slab=True)
+    # (a slab the library refuses - e.g. an outlet cell at x = 0 in this rank's planes only -
+    # must stop EVERY rank, not leave the others waiting in the next collective)
+    plan, refused = None, None
+    try:
+        plan = KernelPlan(nx, ny, n, state.layout, state.precision, flags[z0:z1], state.params.omega,
+                          state.wall_u, tile, inlet_u=state.inlet_u, device=config.device,
+                          halo_lo=lo, halo_hi=hi, slab=True)
+    except (ValueError, MemoryError) as exc:
+        refused = exc
+    here = torch.device("cuda", torch.cuda.current_device() if config.device is None
+                        else int(config.device))
+    if not slab._agree(refused is None, world, None, here):
+        if plan is not None:
+            plan.close()
+        raise ValueError("engine.run: the slab of some rank was refused"
+                         + (f" (this rank: {refused})" if refused else ""))
     dev = plan.device
     dense = state.f_pre.data.reshape(Q, nz, ny, nx)
     mine = pinned_empty((Q, n * ny * nx), state.precision.storage)   # this rank's slab, contiguous
