@@ -260,6 +260,7 @@ class Session:
         self.pre = plan.alloc()
         self.post = None if self.inplace else plan.alloc()
         self.host_stale = False
+        self.carries_both = False
         self.upload()
 
     def normalize(self):
@@ -291,10 +292,13 @@ class Session:
         # Otherwise - or when the geometry chains outlet cells, where the
         # reference's result depends on stale never-written values and the
         # library refuses the mode - the strict never-written mode is used.
-        try:
-            self.plan.set_passthrough(same)
-        except ValueError:
-            self.plan.set_passthrough(False)
+        # A geometry that chains outlet cells also makes the SECOND block part of
+        # the state: the chained cell reads what this block held two steps ago.
+        # Such a state keeps its host copy of both blocks (sync_host materialises
+        # the second one), so a run split over several sessions - engine.step in
+        # a loop, checkpoint and carry on - follows the reference bit for bit.
+        self.carries_both = self.plan.outlets_chained
+        self.plan.set_passthrough(same and not self.carries_both)
         self.host_stale = False
 
     def sync_host(self):
@@ -302,6 +306,8 @@ class Session:
             return
         st = self.state
         self.normalize()
+        if self.carries_both and not self.inplace and st.f_post_ is None:
+            st.f_post                                   # downloads the second block
         self.plan.download(self.pre, st.f_pre.data, sync=False)
         if st.f_post_ is not None and not self.inplace:
             self.plan.download(self.post, st.f_post_.data, sync=False)
@@ -490,8 +496,11 @@ def _run_host_pipelined(state, config):
     try:
         a, b = plan.alloc(), plan.alloc()
         data = state.f_pre.data
-        _, _, ms, overlapped = plan.run_host(data, data, a, b, config.steps)
-        del a, b
+        _, other, ms, overlapped = plan.run_host(data, data, a, b, config.steps)
+        if plan.outlets_chained:
+            # the second block is part of such a state (see Session.upload)
+            plan.download(other, state.f_post.data)
+        del a, b, other
     finally:
         plan.close()
     state.t += config.steps

@@ -280,6 +280,23 @@ class KernelPlan:
         self.passthrough = bool(on)
         _cabi.check(self._lib.mlb_plan_set_passthrough(self._plan, int(self.passthrough)))
 
+    @property
+    def outlets_chained(self):
+        """True when an outlet cell copies from another outlet cell: the
+        reference then reads that cell's stale value in fpost (engine.py:179-180),
+        so the result depends on the history of BOTH blocks.  The library
+        refuses pass-through stores for exactly these geometries; that refusal
+        is the query."""
+        self.ensure_flags()
+        was = self.passthrough
+        try:
+            self.set_passthrough(True)
+        except ValueError:
+            self.passthrough = False
+            return True
+        self.set_passthrough(was)
+        return False
+
     def set_inplace_layout(self, mode):
         """Thread layout of the in-place pull half (include/mlb.h): 0 classic,
         1 row blocks, -1 auto.  Never changes bits."""

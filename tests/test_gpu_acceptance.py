@@ -227,6 +227,39 @@ def test_run_on_a_resident_state_keeps_the_device_steps():
         sess.close()
 
 
+def test_chained_outlets_carry_the_second_block_between_sessions():
+    """Where an outlet cell copies from another outlet cell the reference reads
+    that cell's STALE value in fpost (engine.py:179-180), so the second buffer
+    is part of the state (it is a field of the reference's SimState,
+    engine.py:89).  A run cut into separate sessions - engine.step in a loop,
+    run after run, the overlapped host run first - must therefore carry it:
+    found by the engine-sequence fuzz (case 73), where each new session
+    started its second block as a copy of the first."""
+    from oracle.cpu import CpuOracle
+    from paper_2409_16781_b200 import boundaries as B
+    from paper_2409_16781_b200.fields import Layout, PopulationField
+    from paper_2409_16781_b200.lattice import RelaxationParams
+    from .helpers import geometries3d, random_block
+    grid, wall_u, inlet_u = geometries3d()["open_chain"]
+    nx, ny, nz = grid.shape
+    mask = B.flatten_mask(grid)
+    for prec in (Precision.SINGLE, Precision.MIXED2):
+        f = random_block(np.random.default_rng(5), grid.size, prec.storage)
+        orc = CpuOracle(nx, ny, nz, mask, 1.1, wall_u, inlet_u,
+                        compute=np.float64 if prec is Precision.MIXED2 else None)
+        state = engine.SimState(
+            f_pre=PopulationField(f.copy(), nx, ny, nz, Layout.ROW), f_post_=None, mask=mask,
+            nx=nx, ny=ny, nz=nz, layout=Layout.ROW, precision=prec,
+            params=RelaxationParams.from_omega(1.1), wall_u=wall_u, inlet_u=inlet_u)
+        engine.run(state, RunConfig(steps=3, precision=prec))            # (host-run path if eligible)
+        for _ in range(4):
+            engine.step(state)
+        engine.run(state, RunConfig(steps=2, precision=prec, overlap_io=False))
+        assert state.t == 9
+        want = orc.run(f.copy(), f.copy(), 9)
+        np.testing.assert_array_equal(state.f_pre.data, want)
+
+
 def test_divergence_leaves_the_diverged_populations_in_the_host_arrays():
     """engine.py:258-259 of the reference raises with the diverged populations
     in state.f_pre at the reported step; here the host arrays are synchronised

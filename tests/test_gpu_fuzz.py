@@ -179,3 +179,94 @@ def test_random_case_every_kernel_family_bitwise(seed):
         np.testing.assert_array_equal(got, want, err_msg=f"in-place slab, case {seed}")
         ring.close()
     plan.close()
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("MLB_ENGINE_FUZZ_CASES", "40"))))
+def test_random_engine_sequences_bitwise(seed):
+    """The host layer on random cases: a random sequence of engine.run calls
+    (two blocks / in place, with and without the overlapped host path, with output
+    hooks), resident sessions advanced directly, host edits between runs, and a
+    checkpoint round trip in the middle - the final populations must be the
+    oracle's after the same total number of steps."""
+    import os
+    import tempfile
+    from paper_2409_16781_b200 import engine
+    from paper_2409_16781_b200.fields import PopulationField
+    from paper_2409_16781_b200.lattice import RelaxationParams
+    tag, grid, omega, wall_u, inlet_u, variant, steps = draw_case(7000 + seed)
+    if omega == 0.0:
+        omega = 0.7          # RelaxationParams wants omega in (0, 2)
+    prec = PREC[tag]
+    nx, ny, nz = grid.shape
+    mask = B.flatten_mask(grid)
+    r = np.random.default_rng(9000 + seed)
+    f = random_block(r, grid.size, prec.storage)
+    orc = CpuOracle(nx, ny, nz, mask, omega, wall_u, inlet_u,
+                    compute=np.float64 if prec is Precision.MIXED2 else None)
+
+    def make_state(data, t=0):
+        return engine.SimState(f_pre=PopulationField(data.copy(), nx, ny, nz, Layout.ROW),
+                               f_post_=None, mask=mask, nx=nx, ny=ny, nz=nz, layout=Layout.ROW,
+                               precision=prec, t=t, params=RelaxationParams.from_omega(omega),
+                               wall_u=wall_u, inlet_u=inlet_u)
+
+    # the oracle's two buffers travel with the sequence: a geometry that chains outlet
+    # cells reads stale values of the second one (engine.py:179-180 of the reference)
+    ora = {"pre": f.copy(), "post": f.copy()}
+
+    def oracle_steps(n):
+        newest = orc.run(ora["pre"], ora["post"], n)
+        if newest is not ora["pre"]:
+            ora["pre"], ora["post"] = ora["post"], ora["pre"]
+
+    state, total = make_state(f), 0
+    for _ in range(int(r.integers(2, 6))):
+        k = int(r.integers(1, 10))
+        op = int(r.integers(0, 5))
+        inplace = bool(r.integers(0, 2))
+        try:
+            if op == 0:      # plain run, maybe through the overlapped host path
+                engine.run(state, engine.RunConfig(steps=k, precision=prec, inplace=inplace,
+                                                   overlap_io=[None, False][int(r.integers(0, 2))]))
+            elif op == 1:    # run with an output hook (finite check + host sync at cadence)
+                seen = []
+                engine.run(state, engine.RunConfig(steps=k, precision=prec, inplace=inplace,
+                                                   output_every=2),
+                           on_output=lambda st: seen.append(st.t))
+                assert seen == [t for t in range(total + 1, total + k + 1) if t % 2 == 0]
+            elif op == 2:    # resident session advanced directly, then a run on top of it
+                sess = engine.open_session(state, engine.RunConfig(steps=1, precision=prec,
+                                                                   inplace=inplace))
+                sess.advance(k)
+                total += k
+                oracle_steps(k)
+                k = int(r.integers(1, 6))
+                engine.run(state, engine.RunConfig(steps=k, precision=prec, inplace=inplace))
+                sess.close()
+            elif op == 3:    # checkpoint round trip, then carry on from the restored state
+                with tempfile.TemporaryDirectory() as d:
+                    path = os.path.join(d, "c.mlb")
+                    engine.checkpoint(state, path)
+                    back = engine.restore(path)
+                assert back.t == state.t
+                # (the file holds the first buffer only; restore starts both identical,
+                # engine.py:329 of the reference)
+                ora["post"] = ora["pre"].copy()
+                state = make_state(back.f_pre.data, back.t)
+                engine.run(state, engine.RunConfig(steps=k, precision=prec, inplace=inplace))
+            else:            # the one-step convenience call, k times
+                for _ in range(k):
+                    engine.step(state)
+        except ValueError as exc:
+            # geometries the in-place update cannot serve are refused BEFORE any step
+            assert inplace and "in-place" in str(exc), exc
+            if state.session is not None:
+                state.session.close()
+            continue
+        total += k
+        oracle_steps(k)
+        assert state.t == total
+    want = ora["pre"]
+    if state.session is not None:
+        state.session.close()
+    np.testing.assert_array_equal(state.f_pre.data, want, err_msg=f"engine sequence, case {seed}")
