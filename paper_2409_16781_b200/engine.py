@@ -594,17 +594,29 @@ def _run_slabs(state, config, on_output, on_checkpoint, probe):
     np.copyto(mine.reshape(Q, n, ny, nx), dense[:, z0:z1])
     a = plan.alloc()
     plan.upload(mine, a)
+    mine2, carry = None, False
     if config.inplace:
         # one block per rank (AA pattern over peer memory)
         b = None
         runner, transport = slab.open_inplace_runner(plan, a, rank, world), "peer"
     else:
         b = plan.alloc()
-        b.tensor.copy_(a.tensor)
-        try:
-            plan.set_passthrough(True)      # both blocks identical (engine.py:148)
-        except ValueError:
-            plan.set_passthrough(False)
+        same = state.f_post_ is None
+        if same:
+            b.tensor.copy_(a.tensor)        # both blocks identical (engine.py:148)
+        else:
+            # the host holds a second buffer: it is part of the state (engine.py:89)
+            mine2 = pinned_empty((Q, n * ny * nx), state.precision.storage)
+            np.copyto(mine2.reshape(Q, n, ny, nx),
+                      state.f_post_.data.reshape(Q, nz, ny, nx)[:, z0:z1])
+            plan.upload(mine2, b)
+            same = bool(torch.equal(a.tensor[:, 1:-1, :, :nx], b.tensor[:, 1:-1, :, :nx]))
+        chained = plan.outlets_chained
+        plan.set_passthrough(same and not chained)      # per slab: never changes bits
+        # Chained outlet cells read stale values of the second block (Session.upload), and a
+        # second buffer that differs from the first is state too: if ANY rank has either, every
+        # rank brings its second block back to the host arrays as well (collective decision).
+        carry = not slab._agree(same and not chained, world, None, here)
         runner, transport = slab.open_runner(plan, a, b, rank, world, transport=config.transport)
     pre, post = a, b
 
@@ -635,23 +647,27 @@ def _run_slabs(state, config, on_output, on_checkpoint, probe):
 
     def sync_host():
         """This rank's slab into the host arrays; all slabs with config.gather."""
-        plan.download(pre, mine)
-        np.copyto(dense[:, z0:z1], mine.reshape(Q, n, ny, nx))
-        if state.f_post_ is not None:
-            np.copyto(state.f_post_.data, state.f_pre.data)
-        if not config.gather:
-            return
+        nonlocal mine2
+        blocks = [(pre, mine, dense)]
+        if carry:
+            if mine2 is None:
+                mine2 = pinned_empty((Q, n * ny * nx), state.precision.storage)
+            blocks.append((post, mine2, state.f_post.data.reshape(Q, nz, ny, nx)))
         parts = slab.partition(nz, world)
         biggest = max(e - s for s, e in parts)
-        tdt = pre.tensor.dtype
-        scratch = torch.empty((Q, biggest, ny, nx), dtype=tdt, device=dev)
-        own = pre.tensor[:, 1:-1, :, :nx].contiguous()
-        for r, (s0, s1) in enumerate(parts):
-            buf = own if r == rank else scratch[:, :s1 - s0].contiguous()
-            dist.broadcast(buf, src=r)
-            if r != rank:
-                np.copyto(dense[:, s0:s1], buf.cpu().numpy())
-        if state.f_post_ is not None:
+        for blk, stage, whole in blocks:
+            plan.download(blk, stage)
+            np.copyto(whole[:, z0:z1], stage.reshape(Q, n, ny, nx))
+            if not config.gather:
+                continue
+            scratch = torch.empty((Q, biggest, ny, nx), dtype=blk.tensor.dtype, device=dev)
+            own = blk.tensor[:, 1:-1, :, :nx].contiguous()
+            for r, (s0, s1) in enumerate(parts):
+                buf = own if r == rank else scratch[:, :s1 - s0].contiguous()
+                dist.broadcast(buf, src=r)
+                if r != rank:
+                    np.copyto(whole[:, s0:s1], buf.cpu().numpy())
+        if state.f_post_ is not None and not carry:
             np.copyto(state.f_post_.data, state.f_pre.data)
 
     owner = probe is not None and z0 <= probe[2] < z1

@@ -265,6 +265,55 @@ def test_inplace_slabs_across_processes(geom, tag, variant, world, steps, overla
     np.testing.assert_array_equal(got.reshape(19, -1), want)
 
 
+def _chained_worker(rank, world, port, tag, out_dir):
+    signal.alarm(240)
+    import torch.distributed as dist
+    from paper_2409_16781_b200 import engine
+    from paper_2409_16781_b200.fields import PopulationField
+    from paper_2409_16781_b200.lattice import RelaxationParams
+    init_ranks(rank, world, port)
+    try:
+        prec = {"f32": Precision.SINGLE, "m2": Precision.MIXED2}[tag]
+        grid = B.open_mask(16, 6, 9)
+        grid[5, 1:5, :] = B.INLET
+        grid[13:16, 2:4, 1:8] = B.OUTLET        # three outlet cells in a row: chained
+        grid[9, 3, 2] = B.SOLID
+        grid[:, 0, :] = B.SOLID
+        nx, ny, nz = grid.shape
+        mask = B.flatten_mask(grid)
+        f = random_block(np.random.default_rng(11), grid.size, prec.storage)
+        state = engine.SimState(
+            f_pre=PopulationField(f.copy(), nx, ny, nz, Layout.ROW), f_post_=None, mask=mask,
+            nx=nx, ny=ny, nz=nz, layout=Layout.ROW, precision=prec,
+            params=RelaxationParams.from_omega(1.1), wall_u=(0.0, 0.0, 0.0), inlet_u=0.04)
+        # one run cut into three distributed runs, then two steps alone on this GPU
+        for k in (3, 4, 2):
+            rs = engine.run(state, engine.RunConfig(steps=k, precision=prec))
+            assert rs.transport == "peer", rs.transport
+        assert state.f_post_ is not None            # the second buffer came back with the first
+        engine.run(state, engine.RunConfig(steps=2, precision=prec, distributed=False))
+        want = CpuOracle(nx, ny, nz, mask, 1.1, (0.0, 0.0, 0.0), 0.04,
+                         compute=np.float64 if prec is Precision.MIXED2 else None).run(
+            f.copy(), f.copy(), 11)
+        np.testing.assert_array_equal(state.f_pre.data, want)
+        open(os.path.join(out_dir, f"ok{rank}"), "w").write("ok")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("tag,world", [("f32", 2), ("m2", 3)])
+def test_chained_outlets_carry_the_second_block_between_distributed_runs(tag, world, tmp_path):
+    """Chained outlet cells read stale values of the SECOND buffer
+    (engine.py:179-180 of the reference), so a run cut into several
+    engine.run calls must carry it - under a process group too: every rank
+    brings its slab of both blocks back to the (gathered) host arrays and the
+    next run uploads both.  Ends bitwise on the oracle's unbroken run."""
+    import torch.multiprocessing as mp
+    mp.spawn(_chained_worker, args=(world, _free_port(), tag, str(tmp_path)), nprocs=world,
+             join=True)
+    assert all((tmp_path / f"ok{r}").exists() for r in range(world))
+
+
 def test_peer_ring_does_not_depend_on_the_torch_allocator(tmp_path, monkeypatch):
     """The population blocks are cudaMalloc memory from the library
     (KernelPlan.alloc -> mlb_block_alloc), so they can be exported over CUDA IPC
