@@ -185,9 +185,10 @@ def test_random_case_every_kernel_family_bitwise(seed):
 def test_random_engine_sequences_bitwise(seed):
     """The host layer on random cases: a random sequence of engine.run calls
     (two blocks / in place, with and without the overlapped host path, with output
-    hooks), resident sessions advanced directly, host edits between runs, and a
-    checkpoint round trip in the middle - the final populations must be the
-    oracle's after the same total number of steps."""
+    hooks), resident sessions advanced directly, host edits between runs, probed
+    runs, diagnostics calls and a checkpoint round trip in the middle - the final
+    populations must be the oracle's after the same sequence (the oracle carries
+    both of its buffers along, as the reference's SimState does)."""
     import os
     import tempfile
     from paper_2409_16781_b200 import engine
@@ -222,10 +223,36 @@ def test_random_engine_sequences_bitwise(seed):
     state, total = make_state(f), 0
     for _ in range(int(r.integers(2, 6))):
         k = int(r.integers(1, 10))
-        op = int(r.integers(0, 5))
+        op = int(r.integers(0, 8))
         inplace = bool(r.integers(0, 2))
         try:
-            if op == 0:      # plain run, maybe through the overlapped host path
+            if op == 5:      # a host edit between runs (fluid cells: the reference's f_pre only)
+                fluid = np.flatnonzero(mask == B.FLUID)
+                if fluid.size:
+                    cells = r.choice(fluid, size=min(5, fluid.size), replace=False)
+                    q = int(r.integers(0, 19))
+                    vals = random_block(r, cells.size, prec.storage)[q]
+                    state.f_pre.data[q, cells] = vals
+                    ora["pre"][q, cells] = vals
+                k = 0
+            elif op == 6:    # diagnostics of a host state: a temporary session, nothing changes
+                rho, ux, uy, uz = state.macro()
+                want_rho = ora["pre"].astype(np.float64).sum(axis=0).reshape(nz, ny, nx)
+                np.testing.assert_allclose(rho.transpose(2, 1, 0), want_rho, rtol=1e-6)
+                d = state.diagnostics()
+                assert d["fluid_cells"] == int(np.count_nonzero(mask == B.FLUID))
+                k = 0
+            elif op == 7:    # a probed run: one step per launch, a device-side series
+                fluid = np.flatnonzero(mask == B.FLUID)
+                cell = int(fluid[0]) if fluid.size else 0
+                pz, py, px = np.unravel_index(cell, (nz, ny, nx))
+                stats = engine.run(state, engine.RunConfig(steps=k, precision=prec,
+                                                           inplace=inplace),
+                                   probe=(int(px), int(py), int(pz)))
+                assert stats.probe_samples.shape == (k, 4)
+            if op >= 5:
+                pass
+            elif op == 0:    # plain run, maybe through the overlapped host path
                 engine.run(state, engine.RunConfig(steps=k, precision=prec, inplace=inplace,
                                                    overlap_io=[None, False][int(r.integers(0, 2))]))
             elif op == 1:    # run with an output hook (finite check + host sync at cadence)
