@@ -413,3 +413,74 @@ def test_peer_ring_random_cases_across_processes(world, tmp_path):
     mp.spawn(_random_worker, args=(world, _free_port(), list(range(500, 500 + n)), str(tmp_path)),
              nprocs=world, join=True)
     assert open(tmp_path / "bad.txt").read().strip() == ""
+
+
+def _random_engine_worker(rank, world, port, seeds, out_dir):
+    """Random cases through the DRIVER call under a process group: per case two
+    or three engine.run calls (two blocks / in place, with output hooks), the
+    oracle carrying both of its buffers along; every rank holds the gathered
+    state and compares."""
+    signal.alarm(420)
+    import torch.distributed as dist
+    from paper_2409_16781_b200 import engine
+    from paper_2409_16781_b200.fields import PopulationField
+    from paper_2409_16781_b200.lattice import RelaxationParams
+    from .test_gpu_fuzz import PREC, draw_case
+    init_ranks(rank, world, port)
+    bad, ran, refused = [], 0, 0
+    try:
+        for seed in seeds:
+            tag, grid, omega, wall_u, inlet_u, _, _ = draw_case(seed)
+            if omega == 0.0:
+                omega = 0.7
+            prec = PREC[tag]
+            nx, ny, nz = grid.shape
+            if nz < world:
+                continue
+            mask = B.flatten_mask(grid)
+            r = np.random.default_rng(3000 + seed)
+            f = random_block(r, grid.size, prec.storage)
+            orc = CpuOracle(nx, ny, nz, mask, omega, wall_u, inlet_u,
+                            compute=np.float64 if prec is Precision.MIXED2 else None)
+            pre, post = f.copy(), f.copy()
+            state = engine.SimState(
+                f_pre=PopulationField(f.copy(), nx, ny, nz, Layout.ROW), f_post_=None, mask=mask,
+                nx=nx, ny=ny, nz=nz, layout=Layout.ROW, precision=prec,
+                params=RelaxationParams.from_omega(omega), wall_u=wall_u, inlet_u=inlet_u)
+            for _ in range(int(r.integers(2, 4))):
+                k = int(r.integers(1, 8))
+                inplace = bool(r.integers(0, 2))
+                every = int(r.integers(0, 3))
+                seen = []
+                try:
+                    engine.run(state, engine.RunConfig(steps=k, precision=prec, inplace=inplace,
+                                                       output_every=every),
+                               on_output=(lambda st: seen.append(st.t)) if every else None)
+                except ValueError:      # refused on EVERY rank, before any step
+                    refused += 1
+                    continue
+                ran += 1
+                newest = orc.run(pre, post, k)
+                if newest is not pre:
+                    pre, post = post, pre
+                if not np.array_equal(state.f_pre.data, pre):
+                    bad.append(seed)
+        open(os.path.join(out_dir, f"bad{rank}.txt"), "w").write(
+            f"{ran} {refused} " + " ".join(map(str, bad)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_engine_run_random_cases_across_processes(world, tmp_path):
+    """The fuzz suite's random cases through engine.run under torch.distributed:
+    runs cut into pieces, two blocks and in place, hooks, chained outlet cells
+    (the second block travels).  MLB_RING_CASES (default 16) cases per world size."""
+    import torch.multiprocessing as mp
+    n = int(os.environ.get("MLB_RING_CASES", "16"))
+    mp.spawn(_random_engine_worker, args=(world, _free_port(), list(range(800, 800 + n)),
+                                          str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        ran, refused, *bad = open(tmp_path / f"bad{r}.txt").read().split()
+        assert not bad, bad
+        assert int(ran) > 0
