@@ -290,6 +290,15 @@ def test_random_engine_sequences_bitwise(seed):
             if state.session is not None:
                 state.session.close()
             continue
+        except engine.DivergenceError:
+            # random populations may blow up: the finite check at output cadence then
+            # raises at the step the ORACLE's populations turn non-finite too, with the
+            # diverged populations in the host arrays (engine.py:258-259 of the reference)
+            assert op == 1
+            oracle_steps(state.t - total)
+            assert not np.isfinite(ora["pre"].astype(np.float64)).all()
+            total = state.t
+            break
         total += k
         oracle_steps(k)
         assert state.t == total
