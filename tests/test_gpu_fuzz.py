@@ -223,7 +223,7 @@ def test_random_engine_sequences_bitwise(seed):
     state, total = make_state(f), 0
     for _ in range(int(r.integers(2, 6))):
         k = int(r.integers(1, 10))
-        op = int(r.integers(0, 8))
+        op = int(r.integers(0, 9))
         inplace = bool(r.integers(0, 2))
         try:
             if op == 5:      # a host edit between runs (fluid cells: the reference's f_pre only)
@@ -250,6 +250,9 @@ def test_random_engine_sequences_bitwise(seed):
                                                            inplace=inplace),
                                    probe=(int(px), int(py), int(pz)))
                 assert stats.probe_samples.shape == (k, 4)
+            elif op == 8:    # the host asks for its second buffer (materialised on first use)
+                assert state.f_post.data.shape == state.f_pre.data.shape
+                k = 0
             if op >= 5:
                 pass
             elif op == 0:    # plain run, maybe through the overlapped host path
@@ -302,6 +305,13 @@ def test_random_engine_sequences_bitwise(seed):
         total += k
         oracle_steps(k)
         assert state.t == total
+        if k and state.f_post_ is not None:
+            # after a two-block run the buffer swapped out last is the previous step's
+            # state in the reference too; an in-place run has no second block (copy)
+            ran_inplace = inplace and op in (0, 1, 2, 7)
+            want_post = ora["pre"] if ran_inplace else ora["post"]
+            np.testing.assert_array_equal(state.f_post_.data, want_post,
+                                          err_msg=f"second buffer, case {seed}, op {op}")
     want = ora["pre"]
     if state.session is not None:
         state.session.close()
