@@ -22,6 +22,7 @@ Diagnostics (`macro`, `diagnostics`, `check_finite`, the per-step probe)
 execute on the device too; there is no CPU compute path in this package.
 """
 
+import contextlib
 import struct
 from dataclasses import dataclass, field
 
@@ -244,6 +245,27 @@ def build_plan(state, config, defer_flags=False):
                       defer_flags=defer_flags)
 
 
+@contextlib.contextmanager
+def _hooks_read_only(state):
+    """While a hook runs inside `run` the DEVICE holds the state the next step
+    continues from, so an edit of the host arrays would be silently lost (the
+    reference, all on the host, would step on from it).  The hook therefore
+    sees READ-ONLY views: an editing hook fails loudly ("assignment
+    destination is read-only") instead of being ignored;
+    `state.session.host_edit()` is the way to edit a resident state."""
+    fields = [f for f in (state.f_pre, state.f_post_) if f is not None]
+    kept = [f.data for f in fields]
+    for f in fields:
+        view = f.data.view()
+        view.flags.writeable = False
+        f.data = view
+    try:
+        yield
+    finally:
+        for f, data in zip(fields, kept):
+            f.data = data
+
+
 class Session:
     """A state resident on the GPU: two device blocks and the plan.
 
@@ -315,6 +337,34 @@ class Session:
         if st.f_post_ is not None and self.inplace:
             np.copyto(st.f_post_.data, st.f_pre.data)  # there is no second device block
         self.host_stale = False
+
+    def hooks_read_only(self):
+        return _hooks_read_only(self.state)
+
+    @contextlib.contextmanager
+    def host_edit(self):
+        """Edit the populations of a resident state on the host:
+
+            with state.session.host_edit() as st:
+                st.f_pre.data[q, cells] = ...
+
+        brings the host arrays up to date, hands out the writable arrays and
+        uploads them again on exit (usable inside hooks)."""
+        self.sync_host()
+        st = self.state
+        fields = [f for f in (st.f_pre, st.f_post_) if f is not None]
+        kept = [f.data for f in fields]
+        for f in fields:
+            base = f.data
+            while not base.flags.writeable and isinstance(base.base, np.ndarray):
+                base = base.base
+            f.data = base
+        try:
+            yield st
+        finally:
+            self.upload()
+            for f, data in zip(fields, kept):
+                f.data = data
 
     def advance(self, nsteps, timed=False):
         """`nsteps` x (fused update, open-boundary pass, swap)."""
@@ -440,12 +490,14 @@ def run(state, config, on_output=None, on_checkpoint=None, probe=None):
                 state.check_finite()
                 if on_output is not None:
                     sess.sync_host()
-                    on_output(state)
+                    with sess.hooks_read_only():
+                        on_output(state)
             if (config.checkpoint_every and state.t < end_t
                     and state.t % config.checkpoint_every == 0):
                 if on_checkpoint is not None:
                     sess.sync_host()
-                    on_checkpoint(state)
+                    with sess.hooks_read_only():
+                        on_checkpoint(state)
         sess.sync_host()
         torch.cuda.current_stream(dev).synchronize()
     except BaseException:
@@ -706,10 +758,12 @@ def _run_slabs(state, config, on_output, on_checkpoint, probe):
                     raise DivergenceError(f"divergence at step {state.t}")
                 if on_output is not None:
                     sync_host()
-                    on_output(state)
+                    with _hooks_read_only(state):
+                        on_output(state)
             if hook_ckp and on_checkpoint is not None:
                 sync_host()
-                on_checkpoint(state)
+                with _hooks_read_only(state):
+                    on_checkpoint(state)
         settle()
         sync_host()
         torch.cuda.synchronize(dev)

@@ -260,6 +260,45 @@ def test_chained_outlets_carry_the_second_block_between_sessions():
         np.testing.assert_array_equal(state.f_pre.data, want)
 
 
+def test_a_hook_that_edits_the_populations_is_loud_or_goes_through_host_edit():
+    """The reference's hooks see the live host arrays (engine.py:260-265): an
+    edit made in a hook is what the next step continues from.  Here the next
+    step continues from the device, so a hook sees read-only views - a plain
+    edit raises instead of being silently lost - and `session.host_edit()`
+    is the edit that counts: the run equals the oracle's with the same edit
+    at the same step."""
+    from oracle.cpu import CpuOracle
+    spec = CaseSpec("ldc", 20, 12, 9, re=80.0, u0=0.08)
+    state = cases.init(spec, Precision.DOUBLE)
+    f0 = state.f_pre.data.copy()
+    cell = int(np.flatnonzero(state.mask == 0)[7])
+
+    def bad_hook(st):
+        st.f_pre.data[3, cell] = 0.5
+
+    with pytest.raises(ValueError, match="read-only"):
+        engine.run(state, RunConfig(steps=4, precision=Precision.DOUBLE, output_every=2),
+                   on_output=bad_hook)
+    assert state.f_pre.data.flags.writeable          # the views are gone again
+    state.f_pre.data[:] = f0
+    state.t = 0
+
+    def good_hook(st):
+        if st.t == 2:
+            with st.session.host_edit() as s:
+                s.f_pre.data[3, cell] = 0.5
+            assert not st.f_pre.data.flags.writeable  # back to the hook's read-only view
+
+    engine.run(state, RunConfig(steps=5, precision=Precision.DOUBLE, output_every=2),
+               on_output=good_hook)
+    orc = CpuOracle(20, 12, 9, state.mask, state.params.omega, state.wall_u)
+    a, b = f0.copy(), f0.copy()
+    mid = orc.run(a, b, 2)
+    mid[3, cell] = 0.5
+    want = orc.run(mid, b if mid is a else a, 3)
+    np.testing.assert_array_equal(state.f_pre.data, want)
+
+
 def test_divergence_leaves_the_diverged_populations_in_the_host_arrays():
     """engine.py:258-259 of the reference raises with the diverged populations
     in state.f_pre at the reported step; here the host arrays are synchronised
