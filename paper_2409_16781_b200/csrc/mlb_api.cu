@@ -1816,16 +1816,16 @@ int mlb_diagnostics(mlb_plan *p, const void *d_f, double h_out[8], void *stream)
     const int nb = p->diag_blocks, nt = mlb::DIAG_THREADS;
     if (p->dtype == MLB_F32 || p->dtype == MLB_F32C64) {
         const float *f = static_cast<const float *>(d_f);
-        if (packs) mlb::diag_vec_kernel<float, 4><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
-        else mlb::diag_kernel<float><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
+        if (packs) mlb::diag_vec_kernel<float, 4, false><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
+        else mlb::diag_kernel<float, 1><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
     } else if (p->dtype == MLB_F64) {
         const double *f = static_cast<const double *>(d_f);
-        if (packs) mlb::diag_vec_kernel<double, 2><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
-        else mlb::diag_kernel<double><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
+        if (packs) mlb::diag_vec_kernel<double, 2, true><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
+        else mlb::diag_kernel<double, 2><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
     } else {
         const __half *f = static_cast<const __half *>(d_f);
-        if (packs) mlb::diag_vec_kernel<__half, 4><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
-        else mlb::diag_kernel<__half><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
+        if (packs) mlb::diag_vec_kernel<__half, 4, true><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
+        else mlb::diag_kernel<__half, 1><<<nb, nt, 0, S(stream)>>>(f, ct, p->g, p->d_partials);
     }
     MLB_LAUNCHED();
     mlb::diag_final_kernel<<<1, mlb::DIAG_THREADS, 0, S(stream)>>>(p->d_partials,

@@ -1909,7 +1909,7 @@ __global__ void halo_copy_kernel(const void *__restrict__ src, void *__restrict_
 
 // ---------------------------------------------------------------------------
 // Macroscopic fields (engine.py:104-118): float64, all cells, true division.
-template <typename T>
+template <typename T, bool INCELL = false>
 __device__ __forceinline__ void cell_moments(const T *__restrict__ f, long long d,
                                              long long pop, double &r, double &mx,
                                              double &my, double &mz, int *bad)
@@ -1918,13 +1918,21 @@ __device__ __forceinline__ void cell_moments(const T *__restrict__ f, long long 
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
         v[i] = (double)Store<T>::up(f[(long long)i * pop + d]);
-        if (bad && !isfinite(v[i]))
+        if (!INCELL && bad && !isfinite(v[i]))
             ++*bad;
     }
     r = v[0];
 #pragma unroll
     for (int i = 1; i < Q; ++i)
         r = r + v[i];
+    // INCELL: the values are tested only where the cell's sum is non-finite, and re-read
+    // for it (cache hits, and rare) rather than kept in registers - see diag_kernel
+    if (INCELL && bad && !isfinite(r)) {
+#pragma unroll 1
+        for (int i = 0; i < Q; ++i)
+            if (!isfinite((double)Store<T>::up(f[(long long)i * pop + d])))
+                ++*bad;
+    }
     mx = v[1] - v[3] + v[5] - v[6] - v[7] + v[8] + v[11] - v[12] - v[13] + v[14];
     my = v[2] - v[4] + v[5] + v[6] - v[7] - v[8] + v[15] - v[16] - v[17] + v[18];
     mz = v[9] - v[10] + v[11] + v[12] - v[13] - v[14] + v[15] + v[16] - v[17] - v[18];
@@ -2076,7 +2084,15 @@ __device__ __forceinline__ void diag_block_reduce(double (&acc)[DIAG_N], double 
     }
 }
 
-template <typename T>
+// LAZY: how non-finite VALUES are counted.  0: every value is tested as it is converted.
+// 1: only a thread whose mass sum says it met one counts - a NaN or an infinity among the
+// terms makes every later partial sum non-finite (the converse, finite float64 terms
+// overflowing, takes the exact count and finds none) - by walking its cells again after
+// the loop; the common case then pays nothing per value.  2 (one cell per thread only):
+// the same test per cell, on the cell's own sum.  All give the same count; which one an
+// instantiation uses was chosen by measurement (removing the per-value tests changes the
+// register allocation, and with it how many loads the compiler keeps in flight).
+template <typename T, int LAZY>
 __global__ void __launch_bounds__(DIAG_THREADS)
 diag_kernel(const T *__restrict__ f, const ClsTab ct, const Geom gm,
             double *__restrict__ partials)
@@ -2093,7 +2109,10 @@ diag_kernel(const T *__restrict__ f, const ClsTab ct, const Geom gm,
             const long long d = base + x;
             double rr, mx, my, mz;
             int bad = 0;
-            cell_moments<T>(f, d, gm.pop, rr, mx, my, mz, &bad);
+            if (LAZY == 1)
+                cell_moments<T>(f, d, gm.pop, rr, mx, my, mz, nullptr);
+            else
+                cell_moments<T, LAZY == 2>(f, d, gm.pop, rr, mx, my, mz, &bad);
             acc[0] += rr;
             acc[6] += (double)bad;
             const uint32_t kd = ct.kind[d];
@@ -2110,11 +2129,24 @@ diag_kernel(const T *__restrict__ f, const ClsTab ct, const Geom gm,
             }
         }
     }
+    if (LAZY == 1 && !isfinite(acc[0])) {
+        int bad = 0;
+        for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+            const int lz = (int)(r / gm.ny), y = (int)(r % gm.ny);
+            const long long base = (long long)(lz + 1) * gm.plane + (long long)y * gm.xp;
+            for (int x = threadIdx.x; x < gm.nx; x += DIAG_THREADS)
+#pragma unroll 1
+                for (int i = 0; i < Q; ++i)
+                    if (!isfinite((double)Store<T>::up(f[(long long)i * gm.pop + base + x])))
+                        ++bad;
+        }
+        acc[6] = (double)bad;  // (0 so far)
+    }
     diag_block_reduce(acc, partials + (long long)blockIdx.x * DIAG_N);
 }
 
 // pack form: a fixed assignment of packs to threads, cells of a pack in order
-template <typename TS, int V>
+template <typename TS, int V, bool LAZY>
 __global__ void __launch_bounds__(DIAG_THREADS)
 diag_vec_kernel(const TS *__restrict__ f, const ClsTab ct, const Geom gm,
                 double *__restrict__ partials)
@@ -2138,7 +2170,10 @@ diag_vec_kernel(const TS *__restrict__ f, const ClsTab ct, const Geom gm,
             const uint32_t kpack = KindIO<V>::load(ct.kind + d);
             double rr[V], mx[V], my[V], mz[V];
             int bad = 0;
-            pack_moments<TS, V>(f, d, gm.pop, rr, mx, my, mz, &bad);
+            if (LAZY)
+                pack_moments<TS, V>(f, d, gm.pop, rr, mx, my, mz, nullptr);
+            else
+                pack_moments<TS, V>(f, d, gm.pop, rr, mx, my, mz, &bad);
             acc[6] += (double)bad;
 #pragma unroll
             for (int j = 0; j < V; ++j) {
@@ -2158,6 +2193,27 @@ diag_vec_kernel(const TS *__restrict__ f, const ClsTab ct, const Geom gm,
                 }
             }
         }
+    }
+    if (LAZY && !isfinite(acc[0])) {  // see diag_kernel: the exact count, only where the sum asks for it
+        using T = typename Store<TS>::C;
+        int bad = 0;
+        for (long long row = (long long)blockIdx.x * rpi + sub; sub < rpi && row < rows;
+             row += (long long)gridDim.x * rpi) {
+            const int lz = (int)(row / gm.ny), y = (int)(row - (long long)lz * gm.ny);
+            for (int x0 = pk0 * V; x0 < gm.nx; x0 += DIAG_THREADS * V) {
+                const long long d = (long long)(lz + 1) * gm.plane + (long long)y * gm.xp + x0;
+#pragma unroll 1
+                for (int i = 0; i < Q; ++i) {
+                    T w[V];
+                    PackIO<TS, V>::load(f + (long long)i * gm.pop + d, w);
+#pragma unroll
+                    for (int j = 0; j < V; ++j)
+                        if (!isfinite(w[j]))
+                            ++bad;
+                }
+            }
+        }
+        acc[6] = (double)bad;  // (0 so far)
     }
     diag_block_reduce(acc, partials + (long long)blockIdx.x * DIAG_N);
 }

@@ -286,6 +286,37 @@ def test_macro_bitwise_and_diagnostics(tag, rng):
     assert plan.diagnostics(d)["nonfinite"] == 2
 
 
+@pytest.mark.parametrize("geom", ["channel40", "channel"])  # pack kernel / one cell per thread
+@pytest.mark.parametrize("tag", ["f64", "f32", "f16"])
+def test_nonfinite_count_is_exact(tag, geom, rng):
+    """The diagnostics count non-finite VALUES (the oracle's definition), and the
+    kernels look at the individual values only where a cell's sum is non-finite:
+    several per cell, +inf and -inf in one cell (their sum is a NaN), wall cells,
+    and - in float64 - finite terms whose sum overflows (not a non-finite value)."""
+    grid, wall_u, inlet_u = geometries3d()[geom]
+    prec = PREC[tag]
+    f = random_block(rng, grid.size, prec.storage)
+    plan = make_plan(grid, prec, 1.0, wall_u, inlet_u)
+    d = plan.alloc()
+    if tag == "f64":
+        big = f.copy()
+        big[:, 7] = 1.7e308  # 19 finite terms, an infinite sum
+        big[2, 9] = -1.7e308
+        plan.upload(big, d)
+        assert plan.diagnostics(d)["nonfinite"] == 0
+    cells = rng.choice(grid.size, size=40, replace=False)
+    for n, c in enumerate(cells):
+        qs = rng.choice(19, size=1 + n % 5, replace=False)
+        f[qs, c] = rng.choice([np.nan, np.inf, -np.inf], size=len(qs))
+    f[[1, 3], cells[0]] = [np.inf, -np.inf]
+    f[:, cells[1]] = np.nan
+    want = int(np.count_nonzero(~np.isfinite(f)))
+    assert want > 40
+    plan.upload(f, d)
+    assert plan.diagnostics(d)["nonfinite"] == want
+    assert make_oracle(grid, 1.0, wall_u, inlet_u, prec).diagnostics(f)["nonfinite"] == want
+
+
 def test_ldc64_fp64_100_steps_bitwise():
     """BASELINE.json config 1: D3Q19 BGK lid-driven cavity 64^3, 100 steps,
     fp64, through the reference-shaped API (cases.init + engine.run)."""
