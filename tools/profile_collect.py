@@ -35,6 +35,7 @@ traffic = {}
 names = [(f"{k}_{t}_512", f"{'step_kernel' if k == 'step' else k}_{t}_512")
          for t in ("f32", "f64", "f16", "m2") for k in ("step", "aa_pull", "aa_local")]
 names += [("stage_f16_512", "stage_f16_512"), ("aa_pull_rowb_f32_512", "aa_pull_rowb_f32_512")]
+names += [(f"diag_{t}_512", f"diag_{t}_512") for t in ("f32", "f64", "f16")]
 for name, key in names:
     summary = os.path.join(OUT, f"ncu_{name}.txt")
     if not os.path.exists(summary):

@@ -29,4 +29,9 @@ for pt in single:f32 double:f64 mixed1:f16 mixed2:m2; do
 done
 cap stage_f16_512 step_stage python tools/one.py 512x512x512 mixed1 4000 4
 cap aa_pull_rowb_f32_512 aa_pull python tools/aa_one.py single 1
+# diagnostics (pack form): tools/diag_time.py launches the kernel 6 times per storage type, fp32 / fp64 / fp16 in turn
+cap_s() { local s=$1 name=$2 regex=$3; shift 3; $NCU --set full --import-source on -k regex:$regex -s $s -c 1 -f -o $OUT/$name "$@" > /dev/null 2>&1; python tools/ncu_summary.py $OUT/$name.ncu-rep > $OUT/ncu_$name.txt 2>&1; rm -f $OUT/$name.ncu-rep; head -3 $OUT/ncu_$name.txt; }
+cap_s 1 diag_f32_512 diag_vec_kernel python tools/diag_time.py 512
+cap_s 7 diag_f64_512 diag_vec_kernel python tools/diag_time.py 512
+cap_s 13 diag_f16_512 diag_vec_kernel python tools/diag_time.py 512
 ls -la $OUT
